@@ -1,0 +1,50 @@
+# Build of the B200 function-execution path.
+#   make            -> paper_2303_05601_b200/_lib/libgpufaas_b200.so (host C++ + sm_100a CUDA)
+#   make oracle     -> oracle/_build/liboracle.so (test-only C restatement)
+#   make ref        -> oracle/_ref/* (unmodified reference, compiled in place; test-only)
+# No -ffast-math and -ffp-contract=off on host code: the control plane's double
+# arithmetic must match the reference bit for bit.
+
+JSONDIR ?= /opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann
+CUDA    ?= /usr/local/cuda
+NVCC    := $(CUDA)/bin/nvcc
+CXX     ?= g++
+PKG     := paper_2303_05601_b200
+OUT     := $(PKG)/_lib
+OBJ     := build/obj
+ARCH    := -gencode arch=compute_100a,code=sm_100a
+INC     := -Iinclude -I$(PKG)/csrc/host -I$(PKG)/csrc/device -I$(JSONDIR)
+CXXFLAGS := -std=c++20 -O2 -fPIC -ffp-contract=off -Wall -Wextra $(INC) -I$(CUDA)/include
+NVFLAGS  := -std=c++20 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -ffp-contract=off \
+            --expt-relaxed-constexpr -Xptxas -v $(INC)
+
+HOST_SRCS := $(wildcard $(PKG)/csrc/host/*.cpp) $(wildcard $(PKG)/csrc/capi/*.cpp)
+CU_SRCS   := $(wildcard $(PKG)/csrc/device/*.cu) $(wildcard $(PKG)/csrc/capi/*.cu)
+HOST_OBJS := $(patsubst $(PKG)/csrc/%.cpp,$(OBJ)/%.o,$(HOST_SRCS))
+CU_OBJS   := $(patsubst $(PKG)/csrc/%.cu,$(OBJ)/%.cu.o,$(CU_SRCS))
+HDRS      := $(wildcard include/*.h include/gpufaas/*.hpp $(PKG)/csrc/*/*.hpp $(PKG)/csrc/*/*.cuh)
+
+.PHONY: all product oracle ref clean
+all: product
+product: $(OUT)/libgpufaas_b200.so
+
+$(OBJ)/%.o: $(PKG)/csrc/%.cpp $(HDRS)
+	@mkdir -p $(dir $@)
+	$(CXX) $(CXXFLAGS) -c $< -o $@
+
+$(OBJ)/%.cu.o: $(PKG)/csrc/%.cu $(HDRS)
+	@mkdir -p $(dir $@)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $@.ptxas.txt || (cat $@.ptxas.txt; false)
+
+$(OUT)/libgpufaas_b200.so: $(HOST_OBJS) $(CU_OBJS)
+	@mkdir -p $(OUT)
+	$(NVCC) -shared $(ARCH) -cudart static -o $@ $^ -lpthread -ldl -lrt
+
+oracle:
+	$(MAKE) -C oracle oracle
+
+ref:
+	$(MAKE) -C oracle ref
+
+clean:
+	rm -rf build $(OUT)

@@ -1,0 +1,192 @@
+/* gpufaas_b200.h — C-ABI of the B200 GPU function-execution path.
+ *
+ * Host code (the C++ control plane under include/gpufaas/) reaches CUDA only
+ * through these entry points: plain pointers, sizes and int status codes, no
+ * exceptions and no torch types across the boundary. The reference has no FFI
+ * of its own; each entry point names the reference interface
+ * whose profiled constant it replaces with real device work:
+ *
+ *   gfx_arena_create   <- GpuState::capacity_mb_ accounting
+ *                         (proj/include/gpufaas/cluster.hpp:74-77)
+ *   gfx_load_h2d       <- profile.load_time_us charged on a miss
+ *                         (proj/src/cluster.cpp:163-167)
+ *   gfx_fetch_p2p      <- the false-miss reload (proj/src/sched.cpp:117,127;
+ *                         locations(): proj/src/cluster.cpp:69-72)
+ *   gfx_evict          <- ClusterState::evict_one (proj/src/cluster.cpp:117-129)
+ *   gfx_infer          <- profile.infer_time_us (proj/src/cluster.cpp:161,167)
+ *   gfx_event_*        <- ClusterState::complete (proj/src/cluster.cpp:176-187)
+ *   gfx_replay         <- run_stream (proj/src/engine.cpp:100-173) driving
+ *                         one GPU manager per device
+ *   gfx_sim_*          <- run()/run_stream() of the control plane alone, with
+ *                         canonical digests (see oracle/gpufaas_oracle.h)
+ *
+ * Status codes: 0 = ok, GFX_ERR_DOMAIN (1) = the reference's std::runtime_error
+ * class (bad input, model cannot fit, ...), GFX_ERR_INTERNAL (2) = its
+ * std::logic_error class (invariant violation), GFX_ERR_CUDA (3) = CUDA
+ * failure or no device. gfx_last_error() holds the message (thread-local).
+ * INTEGRATION.md shows the ctypes / C++ bindings.
+ */
+#ifndef GPUFAAS_B200_H
+#define GPUFAAS_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GFX_OK 0
+#define GFX_ERR_DOMAIN 1
+#define GFX_ERR_INTERNAL 2
+#define GFX_ERR_CUDA 3
+
+#define GFX_PAGE_BYTES (2u << 20) /* HBM arena page: 2 MiB */
+#define GFX_MAX_PAGES 192         /* largest model: 384 MiB */
+#define GFX_MAX_LAYERS 16
+
+/* ---------------------------------------------------------------- sim ABI */
+typedef struct {
+    int32_t gpu_count;
+    int32_t policy; /* 0 lb, 1 lalb, 2 lalbo3 */
+    int32_t o3_limit;
+    int32_t working_set;
+    int32_t per_minute_total;
+    int32_t duration_minutes;
+    int32_t use_synthetic_trace;
+    int32_t syn_function_count;
+    int32_t syn_minutes;
+    int32_t syn_draws_per_minute;
+    int32_t debug_checks;
+    int32_t log_events; /* 0 none, 1 events, 2 events + cache contents */
+    int32_t use_reference_scheduler; /* unused by the product */
+    int32_t pad_;
+    double capacity_mb;
+    double syn_zipf_exponent;
+    uint64_t seed;
+    uint64_t syn_seed;
+} gfx_sim_config;
+
+const char* gfx_sim_last_error(void);
+void* gfx_sim_run(const char* catalog_csv, const char* trace_csv, const gfx_sim_config* cfg);
+void* gfx_sim_run_stream(const char* catalog_csv, const gfx_sim_config* cfg, int n,
+                         const int32_t* model_idx, const int64_t* arrival_us);
+int64_t gfx_sim_num_decisions(void* h);
+int64_t gfx_sim_num_requests(void* h);
+double gfx_sim_run_ns(void* h);
+void gfx_sim_get_decisions(void* h, int32_t* ints7, int64_t* times3);
+void gfx_sim_get_requests(void* h, int32_t* model_idx, int64_t* arrival, int64_t* dispatched,
+                          int64_t* completed, int32_t* skip);
+uint64_t gfx_sim_decision_digest(void* h);
+uint64_t gfx_sim_request_digest(void* h);
+uint64_t gfx_sim_log_digest(void* h);
+int64_t gfx_sim_log_size(void* h);
+const char* gfx_sim_log(void* h);
+const char* gfx_sim_report_json(void* h);
+void gfx_sim_free(void* h);
+
+/* ------------------------------------------------------------ data plane */
+typedef struct gfx_arena_s* gfx_arena_t; /* one per device: the GPU manager */
+typedef struct gfx_event_s* gfx_event_t;
+
+#define GFX_MODEL_MLP 1 /* fp32 MLP classifier: relu(xW^T+b) ... softmax */
+
+typedef struct {
+    int32_t family;             /* GFX_MODEL_* */
+    int32_t n_layers;           /* linear layers */
+    int32_t dims[GFX_MAX_LAYERS + 1]; /* dims[0] = input features, dims[L] = classes */
+    int32_t batch;              /* rows per request (32) */
+    int32_t pad_;
+    uint64_t seed;              /* parameter stream */
+} gfx_model_desc;
+
+const char* gfx_last_error(void);
+int gfx_device_count(int* out);
+int gfx_device_init(int dev, int enable_peers);
+
+/* Model repository in pinned host memory (the paper's host-side model store).
+ * Builds the model's parameter blob; idx is the catalog row. */
+int gfx_model_register(int model_idx, const gfx_model_desc* desc);
+int gfx_model_bytes(int model_idx, uint64_t* bytes);
+int gfx_model_pages(int model_idx, int32_t* pages);
+int gfx_models_clear(void);
+
+/* Pre-allocated HBM arena of `capacity_bytes` (multiple of GFX_PAGE_BYTES)
+ * plus the manager's streams and workspaces on device `dev`. */
+int gfx_arena_create(int dev, uint64_t capacity_bytes, gfx_arena_t* out);
+int gfx_arena_destroy(gfx_arena_t a);
+int gfx_arena_reset(gfx_arena_t a); /* synchronise, evict everything */
+int gfx_arena_free_pages(gfx_arena_t a, int32_t* out);
+int gfx_arena_resident(gfx_arena_t a, int model_idx, int32_t* out);
+
+/* Cache operations. Each is asynchronous on the manager's streams; `done`
+ * (optional) receives an event that fires when the operation completes. */
+int gfx_load_h2d(gfx_arena_t a, int model_idx, gfx_event_t* done);
+int gfx_fetch_p2p(gfx_arena_t dst, gfx_arena_t src, int model_idx, gfx_event_t* done);
+int gfx_evict(gfx_arena_t a, int model_idx);
+/* One batched inference of a resident model. in: [batch x dims[0]] fp32,
+ * out: [2][batch x classes] fp32 (logits then softmax probabilities). Both
+ * are DEVICE pointers on the arena's device. */
+int gfx_infer(gfx_arena_t a, int model_idx, const float* in, float* out, int batch, gfx_event_t* done);
+
+int gfx_event_query(gfx_event_t e); /* 0 done, 1 pending */
+int gfx_event_sync(gfx_event_t e);
+int gfx_event_release(gfx_event_t e);
+
+/* Copy helpers for tests / e2e (host<->device through the manager's stream). */
+int gfx_device_alloc(gfx_arena_t a, uint64_t bytes, void** out);
+int gfx_device_free(gfx_arena_t a, void* p);
+int gfx_memcpy_h2d(gfx_arena_t a, void* dst, const void* src, uint64_t bytes);
+int gfx_memcpy_d2h(gfx_arena_t a, void* dst, const void* src, uint64_t bytes);
+int gfx_synchronize(gfx_arena_t a);
+/* Fill `n` fp32 values on device with the parameter stream (seed, tensor). */
+int gfx_fill_params(gfx_arena_t a, float* dst, uint64_t n, uint64_t seed, uint32_t tensor, float scale);
+uint64_t gfx_input_seed(int request_id);
+
+/* ---------------------------------------------------------------- replay */
+/* Trace replay: the control plane (scheduler + cluster state, bit-exact with
+ * the reference) drives one GPU manager per device; every dispatch becomes
+ * evict -> (H2D | NVLink P2P) -> batched inference in decision order. */
+typedef struct {
+    const char* catalog_csv;
+    const char* trace_csv;       /* NULL -> synthetic trace of cfg */
+    gfx_sim_config cfg;
+    int32_t n_devices;           /* devices backing cfg.gpu_count GPUs (1 or cfg.gpu_count) */
+    int32_t first_device;
+    int32_t only_gpu;            /* >= 0: execute only this GPU's decisions (one rank per GPU) */
+    int32_t use_p2p;             /* false misses fetch from the peer holder over NVLink */
+    int32_t host_io;             /* 1: inputs from pinned host, outputs back to host (e2e) */
+    int32_t record_kernels;      /* per-launch CUDA-event timing of the inference kernels */
+    int32_t record_requests;     /* per-request service-time events */
+    int32_t keep_outputs;        /* keep every request's output (parity checks) */
+    const float* host_inputs;    /* host_io: [n_requests][batch*dims0] pinned, else NULL */
+    float* host_outputs;         /* host_io/keep_outputs: [n_requests][2*batch*classes] or NULL */
+} gfx_replay_args;
+
+typedef struct {
+    int64_t n_requests;
+    int64_t n_decisions;
+    int64_t hits, misses, false_misses, local_enqueues, evictions;
+    int64_t loads_h2d, loads_p2p;
+    int64_t kernel_launches;
+    uint64_t decision_digest;
+    uint64_t h2d_bytes;          /* model weight bytes host->device */
+    uint64_t p2p_bytes;
+    uint64_t io_h2d_bytes;       /* request inputs (host_io) */
+    uint64_t io_d2h_bytes;       /* request outputs (host_io) */
+    double device_ms;            /* CUDA-event time of the whole replay (max over devices) */
+    double host_ms;              /* wall time of the call */
+    double sched_ms;             /* host time spent in the control plane */
+    double kernel_ms;            /* sum of inference-kernel event times (record_kernels) */
+    double h2d_ms;               /* sum of model-load event times */
+    double service_p50_ms, service_p99_ms; /* per-request device service time (record_requests) */
+    double sim_p50_s, sim_p99_s, sim_avg_latency_s; /* virtual-time latency from the schedule */
+    double mlp_flops;            /* algorithmic flops of all inferences */
+    double mlp_weight_bytes;     /* algorithmic weight+activation bytes of all inferences */
+} gfx_replay_result;
+
+int gfx_replay(const gfx_replay_args* args, gfx_replay_result* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GPUFAAS_B200_H */
