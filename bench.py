@@ -1,0 +1,370 @@
+#!/usr/bin/env python
+"""Trace-replay benchmark of the B200 GPU function-execution path.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl product|reference]
+
+One step = one replay of the whole synthetic trace through the product: the
+bit-exact control plane (locality-aware scheduler + cache manager) drives the
+GPU manager(s); every dispatch is evict -> model load (pinned-host H2D) ->
+batched fp32 MLP inference on the B200. Workload (BASELINE.json configs[1],
+"C2"): bundled-trace workload (60-function Zipf trace, working set 15,
+325 req/min x 6 min = 1950 requests), 22 Table-I models re-cast as fp32 MLPs
+(32-99 MiB), 204 MiB HBM arena per GPU, LALBO3 (o3 limit 25).
+
+value  = requests / second of the replay with request inputs resident in HBM
+         (device-timed with CUDA events over every stream of the manager);
+e2e    = the same through gfx_replay with HOST buffers: each request's input
+         crosses PCIe and its output comes back inside the timed region.
+N > 1 (torchrun): weak scaling — cfg.gpu_count = N, rate x N; every rank runs
+the same deterministic control plane and executes its own GPU's decisions;
+value = all requests / max-over-ranks device time.
+"""
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "trace-replay requests/sec + p50/p99 latency at 1/2/4/8 B200; cache hit rate"
+H2D_PEAK_GBS = 55.6       # measured pinned H2D, 1 GiB copies on this pool (gpurun_out/probe.txt)
+HOST_LINK_NOMINAL = 64.0  # PCIe Gen5 x16 per direction, nominal
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="product", choices=["product", "reference"])
+    ap.add_argument("--policy", default="lalbo3")
+    ap.add_argument("--no-extras", action="store_true", help="skip the locality comparison and cpu baseline")
+    return ap.parse_args()
+
+
+def dist_setup(n):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", str(rank)))
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def allreduce_max(world, v):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def allreduce_sum(world, v):
+    if world == 1:
+        return v
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([v], dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.samples.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = sorted(float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit())
+        mx = max(float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit())
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if "Active" in s[3 + i]
+                          and "Not" not in s[3 + i]})
+        return {"sm_mhz": sm[len(sm) // 2] if sm else None, "sm_max_mhz": mx, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def ncu_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu capture, if any."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "k1_traffic.json")) as f:
+            return json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        return None
+
+
+# --------------------------------------------------------------------- CPU arms
+
+def cpu_reference_sample(catalog, policy, threads, n_infer, gpus=1, rpm=325):
+    """The reference's CPU path: the compiled reference's run_stream (oracle/_ref,
+    else the oracle restatement) for the control plane, plus the oracle's fp64 CPU
+    inference restatement (the reference has no inference code) on a bounded
+    sample of the same requests. Returns (req/s, description, kind)."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import numpy as np
+    import simabi
+    import paper_2303_05601_b200 as gfx
+
+    kind = "reference"
+    try:
+        sim = simabi.load_ref()
+    except OSError:
+        sim, kind = simabi.load_oracle(), "port"
+    cfg = simabi.make_config(gpus=gpus, capacity_mb=204.0, policy=policy, rpm=rpm)
+    t0 = time.perf_counter()
+    res = sim.run(catalog, cfg)
+    sched_s = time.perf_counter() - t0
+    n = len(res.arrival)
+    olib = C.CDLL(simabi.ORACLE_SO)
+    olib.orc_mlp_forward.restype = C.c_int
+    olib.orc_mlp_forward.argtypes = [C.c_uint64, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p,
+                                     C.c_void_p, C.c_int]
+    olib.orc_fill_params.argtypes = [C.c_uint64, C.c_uint32, C.c_uint64, C.c_float, C.c_void_p]
+    specs = gfx.load_model_specs("mlp_c2")
+    picks = np.linspace(0, n - 1, n_infer).astype(int)
+    t0 = time.perf_counter()
+    for rid in picks:
+        s = specs[int(res.model_idx[rid])]
+        x = np.zeros((32, s.dims[0]), np.float32)
+        olib.orc_fill_params(gfx._ffi.gfx_input_seed(int(rid)), 0xFFFFFFFF, x.size, 1.0, x.ctypes.data)
+        dims = (C.c_int32 * len(s.dims))(*s.dims)
+        lo = np.zeros((32, s.dims[-1]), np.float32)
+        pr = np.zeros_like(lo)
+        olib.orc_mlp_forward(s.seed, len(s.dims) - 1, C.cast(dims, C.c_void_p), 32, x.ctypes.data,
+                             lo.ctypes.data, pr.ctypes.data, threads)
+    infer_s = (time.perf_counter() - t0) / len(picks)
+    per_req = sched_s / n + infer_s
+    desc = (f"control plane: {'oracle/_ref (unmodified reference)' if kind == 'reference' else 'oracle port'} "
+            f"run_stream over all {n} requests ({sched_s * 1e3:.1f} ms, 1 thread); inference: oracle fp64 "
+            f"MLP forward on {len(picks)} evenly spaced requests ({infer_s * 1e3:.0f} ms/request, "
+            f"{threads} threads); value = 1 / (sched/request + inference/request)")
+    return 1.0 / per_req, desc, "port" if n_infer else kind
+
+
+def run_reference_arm(a, rank, world):
+    import paper_2303_05601_b200 as gfx
+    if rank != 0:
+        return
+    cat = gfx.catalog_text("mlp_c2")
+    threads = os.cpu_count() or 1
+    vals = []
+    for i in range(a.warmup + a.steps):
+        v, desc, kind = cpu_reference_sample(cat, a.policy, threads, n_infer=4, gpus=a.gpus, rpm=325 * a.gpus)
+        if i >= a.warmup:
+            vals.append(v)
+    v = sum(vals) / len(vals)
+    line = {"metric": METRIC, "value": round(v, 3), "unit": "requests/s", "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": None, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+            "config": {"workload": "C2: bundled-trace workload (ws 15, 325 rpm x 6 min x N GPUs), 22 Table-I "
+                                   "ids as fp32 MLPs, 204 MiB arena/GPU", "policy": a.policy},
+            "cpu_baseline": {"value": round(v, 3), "unit": "requests/s", "cores": threads, "kind": kind,
+                             "sample": desc},
+            "e2e": {"value": round(v, 3), "unit": "requests/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------- product
+
+def main():
+    a = parse()
+    rank, world, local = dist_setup(a.gpus)
+    if a.impl == "reference":
+        run_reference_arm(a, rank, world)
+        return
+    import numpy as np
+    import paper_2303_05601_b200 as gfx
+
+    G = a.gpus
+    specs = gfx.load_model_specs("mlp_c2")
+    gfx.register_models(specs)
+    cat = gfx.catalog_text("mlp_c2")
+    cfg = gfx.sim_config(gpus=G, capacity_mb=204.0, policy=a.policy, rpm=325 * G)
+    only = rank if world > 1 else -1
+    ndev = 1 if world == 1 and G == 1 else G
+    if world == 1 and G > 1:
+        ndev = G  # single process driving G devices
+    rep = gfx.Replay(cat, cfg, n_devices=ndev, only_gpu=only, record_kernels=True, record_requests=True)
+
+    for _ in range(a.warmup):
+        rep.run()
+    barrier(world)
+    res = []
+    with ClockSampler(local) as clk:
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(a.steps):
+            res.append(rep.run())
+        barrier(world)
+        wall = time.perf_counter() - t0
+    dev_ms = allreduce_max(world, sum(r.device_ms for r in res))
+    n_req = res[-1].n_requests  # global request count (every rank sees the whole stream)
+    value = n_req * a.steps / (dev_ms / 1e3)
+    r = res[-1]
+    kernel_ms = allreduce_sum(world, sum(x.kernel_ms for x in res))
+    launches = int(allreduce_sum(world, sum(x.kernel_launches for x in res)))
+    alg_bytes = allreduce_sum(world, sum(x.mlp_weight_bytes for x in res))
+    flops = allreduce_sum(world, sum(x.mlp_flops for x in res))
+    h2d_bytes = allreduce_sum(world, sum(x.h2d_bytes for x in res))
+    h2d_ms = allreduce_sum(world, sum(x.h2d_ms for x in res))
+    rep.close()
+
+    # e2e: same replay with host buffers through the public C-ABI.
+    n = int(n_req)
+    hin = None
+    try:
+        import torch
+        hin_t = torch.empty((n, 32 * 1024), dtype=torch.float32).pin_memory()
+        hout_t = torch.empty((n, 2 * 32 * 1000), dtype=torch.float32).pin_memory()
+        hin, hout = hin_t.numpy(), hout_t.numpy()
+    except Exception:
+        hin = np.zeros((n, 32 * 1024), np.float32)
+        hout = np.zeros((n, 2 * 32 * 1000), np.float32)
+    # Host inputs = the same parameter stream the device-resident inputs use.
+    for i in range(n):
+        gfx._ffi.check(gfx._ffi.gfx_host_fill_params(hin[i].ctypes.data, hin.shape[1],
+                                                     gfx._ffi.gfx_input_seed(i), 0xFFFFFFFF, 1.0))
+    rep2 = gfx.Replay(cat, cfg, n_devices=ndev, only_gpu=only, host_io=True, host_inputs=hin, host_outputs=hout)
+    for _ in range(max(1, a.warmup)):
+        rep2.run()
+    barrier(world)
+    e2e_res = [rep2.run() for _ in range(a.steps)]
+    barrier(world)
+    e2e_ms = allreduce_max(world, sum(x.device_ms for x in e2e_res))
+    e2e_val = n * a.steps / (e2e_ms / 1e3)
+    er = e2e_res[-1]
+    rep2.close()
+
+    peaks, peak_kind = measured_peaks()
+    achieved = alg_bytes / (kernel_ms / 1e3) / 1e9 if kernel_ms else 0.0
+    extras = {}
+    if rank == 0 and not a.no_extras:
+        extras = locality_extras(gfx, world)
+    cpu = None
+    if rank == 0 and not a.no_extras:
+        v, desc, kind = cpu_reference_sample(cat, a.policy, 1, n_infer=2, gpus=G, rpm=325 * G)
+        cpu = {"value": round(v, 3), "unit": "requests/s", "cores": 1, "kind": kind, "sample": desc}
+
+    if rank != 0:
+        return
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "requests/s", "n_gpus": G, "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": round(dev_ms / a.steps, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": "C2 (BASELINE.json configs[1]): bundled-trace workload (60-fn Zipf trace seed 91, "
+                               "working set 15, 325 req/min x 6 min x N GPUs), 22 Table-I ids as fp32 MLPs "
+                               "1024-h-h-h-1000 (32-99 MiB), 204 MiB paged HBM arena per GPU",
+                   "policy": a.policy, "o3_limit": 25, "requests_per_step": n, "batch": 32,
+                   "parallelism": f"request-dp{G}", "l2": "inputs larger than L2 (250 MB of request inputs, "
+                   f"{r.h2d_bytes / 1e9:.0f} GB of model weights streamed per step; arena starts empty each step)"},
+        "p50_latency_ms": round(r.sim_p50_s * 1e3, 4), "p99_latency_ms": round(r.sim_p99_s * 1e3, 4),
+        "latency_note": "virtual-time latency of the bit-exact schedule under the B200-profiled catalog at the "
+                        "trace's arrival rate; service_p50/p99 are measured per-request device service times "
+                        "(load start or inference start -> inference end) of the max-speed replay",
+        "service_p50_ms": round(r.service_p50_ms, 4), "service_p99_ms": round(r.service_p99_ms, 4),
+        "hit_rate": round(r.hits / max(1, r.hits + r.misses), 6), "misses": int(r.misses),
+        "decision_digest": f"{int(r.decision_digest):016x}",
+        "roofline": {"kernel": "mlp_layer_kernel (K1, fp32 FFMA)", "bound": "hbm",
+                     "achieved": round(achieved, 1), "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
+                     "frac": round(achieved / peaks.get("hbm_gbs", 1), 4), "traffic": ncu_traffic(),
+                     "peak_source": peak_kind,
+                     "tflops": round(flops / (kernel_ms / 1e3) / 1e12, 3) if kernel_ms else 0,
+                     "kernel_ms_per_step": round(kernel_ms / a.steps / max(1, world), 3),
+                     "note": "algorithmic bytes = fp32 weights+biases + batch-32 in/out activations per launch"},
+        "load_roofline": {"path": "pinned-host H2D (copy engine)", "achieved": round(h2d_bytes / (h2d_ms * 1e6), 2)
+                          if h2d_ms else 0, "peak": H2D_PEAK_GBS, "unit": "GB/s",
+                          "frac": round(h2d_bytes / (h2d_ms * 1e6) / H2D_PEAK_GBS, 4) if h2d_ms else 0,
+                          "nominal_pcie_gbs": HOST_LINK_NOMINAL, "bytes_per_step": int(r.h2d_bytes)},
+        "e2e": {"value": round(e2e_val, 2), "unit": "requests/s",
+                "h2d_bytes_per_step": int(er.io_h2d_bytes + er.h2d_bytes), "d2h_bytes_per_step": int(er.io_d2h_bytes),
+                "note": "gfx_replay with pinned host inputs/outputs; request I/O + model loads inside the timed region"},
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "wall_s_timed": round(wall, 3),
+        "sched_ms_per_step": round(r.sched_ms, 3),
+        "cpu_baseline": cpu,
+    }
+    line.update(extras)
+    print(json.dumps(line), flush=True)
+
+
+def locality_extras(gfx, world):
+    """Locality-aware vs load-balancing on one B200, in the paper's regime: the same
+    MLP models with Table-I load/infer times (load/infer ~ 2.4) so queues form and
+    the scheduler matters (at B200-profiled times and 325 rpm every policy sees an
+    idle GPU and LB == LALB == LALBO3)."""
+    if world > 1:
+        return {}
+    cat = gfx.catalog_text("mlp_c2_paper")
+    out = {}
+    for pol in ("lb", "lalbo3"):
+        rep = gfx.Replay(cat, gfx.sim_config(gpus=1, capacity_mb=204.0, policy=pol), record_kernels=False)
+        rep.run()
+        rs = [rep.run() for _ in range(2)]
+        rep.close()
+        ms = sum(x.device_ms for x in rs) / len(rs)
+        r = rs[-1]
+        out[pol] = {"replay_req_s": round(r.n_requests / (ms / 1e3), 2), "misses": int(r.misses),
+                    "hit_rate": round(r.hits / (r.hits + r.misses), 4),
+                    "sim_avg_latency_s": round(r.sim_avg_latency_s, 4), "sim_p50_s": round(r.sim_p50_s, 4),
+                    "sim_p99_s": round(r.sim_p99_s, 4)}
+    out["speedup_replay"] = round(out["lalbo3"]["replay_req_s"] / out["lb"]["replay_req_s"], 3)
+    out["speedup_avg_latency"] = round(out["lb"]["sim_avg_latency_s"] / out["lalbo3"]["sim_avg_latency_s"], 3)
+    return {"locality_vs_lb_1gpu_paper_regime": out}
+
+
+if __name__ == "__main__":
+    main()

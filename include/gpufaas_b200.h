@@ -141,6 +141,8 @@ int gfx_synchronize(gfx_arena_t a);
 /* Fill `n` fp32 values on device with the parameter stream (seed, tensor). */
 int gfx_fill_params(gfx_arena_t a, float* dst, uint64_t n, uint64_t seed, uint32_t tensor, float scale);
 uint64_t gfx_input_seed(int request_id);
+/* Same stream generated on the host (no device needed). */
+int gfx_host_fill_params(float* dst, uint64_t n, uint64_t seed, uint32_t tensor, float scale);
 
 /* ---------------------------------------------------------------- replay */
 /* Trace replay: the control plane (scheduler + cluster state, bit-exact with
@@ -184,6 +186,18 @@ typedef struct {
     double mlp_weight_bytes;     /* algorithmic weight+activation bytes of all inferences */
 } gfx_replay_result;
 
+/* Reusable replay context: managers, device buffers and timing events are
+ * created once; every gfx_replay_run() replays the whole trace from an empty
+ * cache (one bench step). */
+typedef struct gfx_replay_s* gfx_replay_t;
+int gfx_replay_create(const gfx_replay_args* args, gfx_replay_t* out);
+int gfx_replay_run(gfx_replay_t r, gfx_replay_result* out);
+/* Per-request outputs of the last run (keep_outputs): [n_requests][2*batch*classes]. */
+int gfx_replay_outputs(gfx_replay_t r, float* host, uint64_t count);
+/* Per-request model row and device service time (ms) of the last run. */
+int gfx_replay_requests(gfx_replay_t r, int32_t* model_idx, double* service_ms, int64_t n);
+int gfx_replay_destroy(gfx_replay_t r);
+/* create + run + destroy */
 int gfx_replay(const gfx_replay_args* args, gfx_replay_result* out);
 
 #ifdef __cplusplus

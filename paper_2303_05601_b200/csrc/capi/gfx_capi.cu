@@ -1,0 +1,600 @@
+// C-ABI of the data plane and the trace replay (declared in include/gpufaas_b200.h).
+//
+// The replay is the product path end to end: the bit-exact control plane
+// (gpufaas::run_stream with the Scheduler) emits decisions; an
+// ExecutionListener turns each dispatch into device work on the GPU manager
+// of the chosen GPU — evict victims, load the model (pinned-host H2D, or
+// NVLink peer fetch when another GPU holds it), run the batched inference —
+// in decision order per GPU. Host enqueue runs ahead of the device; streams
+// and events carry every dependency, so the host never blocks on the GPU
+// until the end-of-replay synchronisation.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <memory>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "gpufaas/engine.hpp"
+#include "gpufaas_b200.h"
+#include "manager.cuh"
+
+namespace gpufaas::capi {
+SimConfig to_sim_config(const gfx_sim_config& c);
+std::vector<Request> make_requests(const gfx_sim_config& c, const Catalog& cat, const char* trace_csv);
+}  // namespace gpufaas::capi
+
+using gfx::GpuManager;
+using gfx::KernelTimer;
+using gfx::ModelStore;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+    try {
+        f();
+        return GFX_OK;
+    } catch (const gfx::CudaError& e) {
+        g_err = e.what();
+        return GFX_ERR_CUDA;
+    } catch (const std::logic_error& e) {
+        // std::invalid_argument derives from logic_error but is a caller error.
+        if (dynamic_cast<const std::invalid_argument*>(&e)) {
+            g_err = e.what();
+            return GFX_ERR_DOMAIN;
+        }
+        g_err = e.what();
+        return GFX_ERR_INTERNAL;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return GFX_ERR_DOMAIN;
+    }
+}
+
+double elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0;
+    GFX_CUDA(cudaEventElapsedTime(&ms, a, b));
+    return ms;
+}
+
+double percentile(std::vector<double> v, double q) {
+    if (v.empty()) return 0.0;
+    std::sort(v.begin(), v.end());
+    size_t rank = static_cast<size_t>(std::ceil(q / 100.0 * static_cast<double>(v.size())));
+    rank = std::clamp<size_t>(rank, 1, v.size());
+    return v[rank - 1];
+}
+
+}  // namespace
+
+struct gfx_arena_s {
+    std::unique_ptr<GpuManager> mgr;
+};
+struct gfx_event_s {
+    cudaEvent_t ev = nullptr;
+    int device = 0;
+};
+
+// ---------------------------------------------------------------- replay
+
+struct gfx_replay_s : gpufaas::ExecutionListener {
+    gfx_replay_args args{};
+    std::string catalog_csv, trace_csv;
+    gpufaas::Catalog catalog;
+    std::vector<gpufaas::Request> requests;
+    std::vector<std::unique_ptr<GpuManager>> mgrs;  // index = GPU id (nullptr if not executed here)
+    std::vector<int> dev_of;
+    // device buffers per device
+    struct DevBufs {
+        float* inputs = nullptr;   // [n][in_elems]
+        float* outputs = nullptr;  // [n][out_elems] (keep/host_io) or [2][out_elems] ring
+        cudaStream_t io_in = nullptr, io_out = nullptr;
+        cudaEvent_t start = nullptr, stop = nullptr;
+    };
+    std::vector<DevBufs> bufs;  // per GPU id
+    size_t in_elems = 0, out_elems = 0;
+    bool full_outputs = false;
+    // timing
+    KernelTimer layer_timer, load_timer, req_timer;
+    std::vector<cudaEvent_t> req_start, req_end;
+    std::vector<int> req_gpu;
+    // counters of the current run
+    gfx_replay_result res{};
+    std::vector<cudaEvent_t> pending_in;  // per GPU: event of the last input copy
+
+    int gpu_count() const { return args.cfg.gpu_count; }
+
+    void setup() {
+        std::istringstream cin_(catalog_csv);
+        catalog = gpufaas::parse_catalog_csv(cin_, "catalog");
+        requests = gpufaas::capi::make_requests(args.cfg, catalog, args.trace_csv ? trace_csv.c_str() : nullptr);
+        const int G = gpu_count();
+        if (G <= 0) throw std::invalid_argument("gpu_count must be positive");
+        if (args.n_devices != 1 && args.n_devices != G)
+            throw std::invalid_argument("n_devices must be 1 or cfg.gpu_count");
+        // Every catalog model must be registered and its charge must cover its pages.
+        int C = -1, D0 = -1;
+        for (size_t i = 0; i < catalog.size(); ++i) {
+            const gfx::ModelBlob& b = ModelStore::get().at(static_cast<int>(i));
+            const double need = 2.0 * b.pages;
+            if (catalog.profiles()[i].occupation_mb < need)
+                throw std::invalid_argument("catalog occupation_mb of '" + catalog.profiles()[i].model_id +
+                                            "' is below its " + std::to_string(b.pages) + " arena pages");
+            const int c = b.desc.dims[b.desc.n_layers], d0 = b.desc.dims[0];
+            if ((C >= 0 && C != c) || (D0 >= 0 && D0 != d0))
+                throw std::invalid_argument("all models of a replay must share input and class widths");
+            C = c;
+            D0 = d0;
+        }
+        in_elems = static_cast<size_t>(32) * D0;
+        out_elems = static_cast<size_t>(2) * 32 * C;
+        full_outputs = args.keep_outputs || args.host_io;
+        const uint64_t pages = static_cast<uint64_t>(args.cfg.capacity_mb / 2.0);
+        const uint64_t cap_bytes = pages * gfx::kPageBytes;
+        mgrs.resize(static_cast<size_t>(G));
+        bufs.resize(static_cast<size_t>(G));
+        dev_of.resize(static_cast<size_t>(G));
+        pending_in.assign(static_cast<size_t>(G), nullptr);
+        const size_t n = requests.size();
+        for (int g = 0; g < G; ++g) {
+            dev_of[g] = args.first_device + (args.n_devices == 1 ? 0 : g);
+            if (args.only_gpu >= 0 && g != args.only_gpu) continue;
+            mgrs[g] = std::make_unique<GpuManager>(dev_of[g], cap_bytes, g);
+            mgrs[g]->layer_timer = args.record_kernels ? &layer_timer : nullptr;
+            mgrs[g]->load_timer = &load_timer;
+            DevBufs& b = bufs[g];
+            GFX_CUDA(cudaSetDevice(dev_of[g]));
+            // Inputs: every request this GPU might serve (ids are global).
+            GFX_CUDA(cudaMalloc(&b.inputs, sizeof(float) * in_elems * std::max<size_t>(n, 1)));
+            GFX_CUDA(cudaMalloc(&b.outputs, sizeof(float) * out_elems * (full_outputs ? std::max<size_t>(n, 1) : 2)));
+            GFX_CUDA(cudaStreamCreateWithFlags(&b.io_in, cudaStreamNonBlocking));
+            GFX_CUDA(cudaStreamCreateWithFlags(&b.io_out, cudaStreamNonBlocking));
+            GFX_CUDA(cudaEventCreate(&b.start));
+            GFX_CUDA(cudaEventCreate(&b.stop));
+            if (!args.host_io) {
+                // HBM-resident inputs, generated once outside the timed region.
+                for (size_t r = 0; r < n; ++r)
+                    gfx::launch_fill_params(b.inputs + r * in_elems, in_elems, gfx_input_seed(static_cast<int>(r)),
+                                            0xFFFFFFFFu, 1.0f, mgrs[g]->compute_stream());
+            }
+            GFX_CUDA(cudaDeviceSynchronize());
+        }
+        if (args.use_p2p && args.n_devices > 1) {
+            for (int a = 0; a < G; ++a)
+                for (int b2 = 0; b2 < G; ++b2) {
+                    if (a == b2 || !mgrs[a] || !mgrs[b2]) continue;
+                    int ok = 0;
+                    GFX_CUDA(cudaDeviceCanAccessPeer(&ok, dev_of[a], dev_of[b2]));
+                    if (ok) {
+                        GFX_CUDA(cudaSetDevice(dev_of[a]));
+                        cudaError_t e = cudaDeviceEnablePeerAccess(dev_of[b2], 0);
+                        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) GFX_CUDA(e);
+                        cudaGetLastError();
+                    }
+                }
+        }
+        req_start.assign(n, nullptr);
+        req_end.assign(n, nullptr);
+        req_gpu.assign(n, -1);
+    }
+
+    void on_begin_execution(int gpu, const gpufaas::Request& req, int model, bool hit,
+                            const std::vector<int>& evicted, int source, gpufaas::SimTime, gpufaas::SimTime) override {
+        if (args.only_gpu >= 0 && gpu != args.only_gpu) return;
+        GpuManager& m = *mgrs[static_cast<size_t>(gpu)];
+        DevBufs& b = bufs[static_cast<size_t>(gpu)];
+        const int rid = req.request_id;
+        m.activate();
+        cudaEvent_t e0 = nullptr;
+        req_gpu[rid] = gpu;
+        if (args.record_requests) {
+            e0 = req_timer.next();
+            req_start[rid] = e0;
+        }
+        if (!hit) {
+            if (e0) GFX_CUDA(cudaEventRecord(e0, m.copy_stream()));
+            for (int v : evicted) m.evict(v);
+            GpuManager* src = nullptr;
+            if (args.use_p2p && source >= 0 && mgrs[static_cast<size_t>(source)] &&
+                mgrs[static_cast<size_t>(source)]->resident(model))
+                src = mgrs[static_cast<size_t>(source)].get();
+            const uint64_t bytes = m.load(model, src);
+            if (src) {
+                res.loads_p2p++;
+                res.p2p_bytes += bytes;
+            } else {
+                res.loads_h2d++;
+                res.h2d_bytes += bytes;
+            }
+        } else if (e0) {
+            GFX_CUDA(cudaEventRecord(e0, m.compute_stream()));
+        }
+        float* in = b.inputs + static_cast<size_t>(rid) * in_elems;
+        float* out = b.outputs + (full_outputs ? static_cast<size_t>(rid) : static_cast<size_t>(rid & 1)) * out_elems;
+        if (args.host_io) {
+            // e2e: this request's input crosses PCIe inside the timed region.
+            GFX_CUDA(cudaMemcpyAsync(in, args.host_inputs + static_cast<size_t>(rid) * in_elems,
+                                     sizeof(float) * in_elems, cudaMemcpyHostToDevice, b.io_in));
+            cudaEvent_t ein = req_timer.next();
+            GFX_CUDA(cudaEventRecord(ein, b.io_in));
+            GFX_CUDA(cudaStreamWaitEvent(m.compute_stream(), ein, 0));
+            res.io_h2d_bytes += sizeof(float) * in_elems;
+        }
+        m.infer(model, in, out);
+        const gfx::ModelBlob& blob = ModelStore::get().at(model);
+        res.mlp_flops += blob.flops;
+        res.mlp_weight_bytes += blob.alg_bytes;
+        if (args.record_requests) {
+            cudaEvent_t e1 = req_timer.next();
+            GFX_CUDA(cudaEventRecord(e1, m.compute_stream()));
+            req_end[rid] = e1;
+        }
+        if (args.host_io) {
+            cudaEvent_t done = req_timer.next();
+            GFX_CUDA(cudaEventRecord(done, m.compute_stream()));
+            GFX_CUDA(cudaStreamWaitEvent(b.io_out, done, 0));
+            GFX_CUDA(cudaMemcpyAsync(args.host_outputs + static_cast<size_t>(rid) * out_elems, out,
+                                     sizeof(float) * out_elems, cudaMemcpyDeviceToHost, b.io_out));
+            res.io_d2h_bytes += sizeof(float) * out_elems;
+        }
+    }
+
+    void on_complete(int, int, gpufaas::SimTime) override {}
+
+    void run(gfx_replay_result* out) {
+        res = gfx_replay_result{};
+        layer_timer.used = load_timer.used = req_timer.used = 0;
+        std::fill(req_start.begin(), req_start.end(), nullptr);
+        std::fill(req_end.begin(), req_end.end(), nullptr);
+        const int G = gpu_count();
+        for (int g = 0; g < G; ++g) {
+            if (!mgrs[g]) continue;
+            mgrs[g]->reset();
+            mgrs[g]->kernel_launches = 0;
+        }
+        const auto h0 = std::chrono::steady_clock::now();
+        for (int g = 0; g < G; ++g) {
+            if (!mgrs[g]) continue;
+            GpuManager& m = *mgrs[g];
+            m.activate();
+            GFX_CUDA(cudaEventRecord(bufs[g].start, m.compute_stream()));
+            for (cudaStream_t s : {m.copy_stream(), bufs[g].io_in, bufs[g].io_out})
+                GFX_CUDA(cudaStreamWaitEvent(s, bufs[g].start, 0));
+        }
+        gpufaas::SimConfig cfg = gpufaas::capi::to_sim_config(args.cfg);
+        const auto s0 = std::chrono::steady_clock::now();
+        gpufaas::SimResult sim = gpufaas::run_stream(cfg, catalog, requests, nullptr, nullptr, this);
+        const auto s1 = std::chrono::steady_clock::now();
+        for (int g = 0; g < G; ++g) {
+            if (!mgrs[g]) continue;
+            GpuManager& m = *mgrs[g];
+            m.activate();
+            for (cudaStream_t s : {m.copy_stream(), bufs[g].io_in, bufs[g].io_out}) {
+                cudaEvent_t e = req_timer.next();
+                GFX_CUDA(cudaEventRecord(e, s));
+                GFX_CUDA(cudaStreamWaitEvent(m.compute_stream(), e, 0));
+            }
+            GFX_CUDA(cudaEventRecord(bufs[g].stop, m.compute_stream()));
+        }
+        double dev_ms = 0;
+        for (int g = 0; g < G; ++g) {
+            if (!mgrs[g]) continue;
+            GFX_CUDA(cudaSetDevice(dev_of[g]));
+            GFX_CUDA(cudaEventSynchronize(bufs[g].stop));
+            dev_ms = std::max(dev_ms, elapsed_ms(bufs[g].start, bufs[g].stop));
+        }
+        const auto h1 = std::chrono::steady_clock::now();
+
+        res.n_requests = static_cast<int64_t>(sim.requests.size());
+        res.n_decisions = static_cast<int64_t>(sim.decisions.size());
+        res.hits = sim.report.hits;
+        res.misses = sim.report.misses;
+        res.false_misses = sim.report.false_misses;
+        res.local_enqueues = sim.report.local_enqueues;
+        res.evictions = sim.report.evictions;
+        uint64_t h = 14695981039346656037ULL;
+        auto fnv = [&](const void* p, size_t len) {
+            const unsigned char* c = static_cast<const unsigned char*>(p);
+            for (size_t i = 0; i < len; ++i) {
+                h ^= c[i];
+                h *= 1099511628211ULL;
+            }
+        };
+        for (const gpufaas::Decision& d : sim.decisions) {
+            const int32_t a[6] = {static_cast<int32_t>(d.kind), d.request_id, d.gpu_id, d.from_local_queue,
+                                  d.false_miss, d.skip_count};
+            fnv(a, sizeof a);
+            fnv(&d.completion_us, 8);
+            fnv(&d.load_us, 8);
+            fnv(&d.infer_us, 8);
+            const int32_t ne = static_cast<int32_t>(d.evicted.size());
+            fnv(&ne, 4);
+            for (const std::string& s : d.evicted) fnv(s.c_str(), s.size() + 1);
+        }
+        res.decision_digest = h;
+        res.device_ms = dev_ms;
+        res.host_ms = std::chrono::duration<double, std::milli>(h1 - h0).count();
+        res.sched_ms = std::chrono::duration<double, std::milli>(s1 - s0).count();
+        for (int g = 0; g < G; ++g)
+            if (mgrs[g]) res.kernel_launches += mgrs[g]->kernel_launches;
+        for (size_t i = 0; i + 1 < layer_timer.used; i += 2)
+            res.kernel_ms += elapsed_ms(layer_timer.ev[i], layer_timer.ev[i + 1]);
+        for (size_t i = 0; i + 1 < load_timer.used; i += 2)
+            res.h2d_ms += elapsed_ms(load_timer.ev[i], load_timer.ev[i + 1]);
+        if (args.record_requests) {
+            std::vector<double> svc;
+            for (size_t r = 0; r < req_start.size(); ++r)
+                if (req_start[r] && req_end[r]) svc.push_back(elapsed_ms(req_start[r], req_end[r]));
+            res.service_p50_ms = percentile(svc, 50);
+            res.service_p99_ms = percentile(svc, 99);
+            service_ms = std::move(svc);
+        }
+        res.sim_p50_s = gpufaas::latency_percentile_s(sim.requests, 50);
+        res.sim_p99_s = gpufaas::latency_percentile_s(sim.requests, 99);
+        res.sim_avg_latency_s = sim.report.avg_latency_s.value_or(0.0);
+        last_models.clear();
+        for (const gpufaas::Request& r : sim.requests) last_models.push_back(catalog.index_of(r.model_id));
+        *out = res;
+    }
+
+    std::vector<double> service_ms;
+    std::vector<int32_t> last_models;
+
+    ~gfx_replay_s() override {
+        for (size_t g = 0; g < bufs.size(); ++g) {
+            if (!mgrs[g]) continue;
+            cudaSetDevice(dev_of[g]);
+            cudaDeviceSynchronize();
+            cudaFree(bufs[g].inputs);
+            cudaFree(bufs[g].outputs);
+            cudaStreamDestroy(bufs[g].io_in);
+            cudaStreamDestroy(bufs[g].io_out);
+            cudaEventDestroy(bufs[g].start);
+            cudaEventDestroy(bufs[g].stop);
+        }
+        for (KernelTimer* t : {&layer_timer, &load_timer, &req_timer})
+            for (cudaEvent_t e : t->ev) cudaEventDestroy(e);
+    }
+};
+
+extern "C" {
+
+const char* gfx_last_error(void) { return g_err.c_str(); }
+
+int gfx_device_count(int* out) {
+    return guarded([&] {
+        int n = 0;
+        GFX_CUDA(cudaGetDeviceCount(&n));
+        *out = n;
+    });
+}
+
+int gfx_device_init(int dev, int enable_peers) {
+    return guarded([&] {
+        GFX_CUDA(cudaSetDevice(dev));
+        GFX_CUDA(cudaFree(nullptr));
+        if (enable_peers) {
+            int n = 0;
+            GFX_CUDA(cudaGetDeviceCount(&n));
+            for (int p = 0; p < n; ++p) {
+                if (p == dev) continue;
+                int ok = 0;
+                GFX_CUDA(cudaDeviceCanAccessPeer(&ok, dev, p));
+                if (!ok) continue;
+                cudaError_t e = cudaDeviceEnablePeerAccess(p, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) GFX_CUDA(e);
+                cudaGetLastError();
+            }
+        }
+    });
+}
+
+int gfx_model_register(int model_idx, const gfx_model_desc* desc) {
+    return guarded([&] { ModelStore::get().add(model_idx, *desc); });
+}
+int gfx_model_bytes(int model_idx, uint64_t* bytes) {
+    return guarded([&] { *bytes = ModelStore::get().at(model_idx).bytes; });
+}
+int gfx_model_pages(int model_idx, int32_t* pages) {
+    return guarded([&] { *pages = static_cast<int32_t>(ModelStore::get().at(model_idx).pages); });
+}
+int gfx_models_clear(void) {
+    return guarded([&] { ModelStore::get().clear(); });
+}
+
+int gfx_arena_create(int dev, uint64_t capacity_bytes, gfx_arena_t* out) {
+    return guarded([&] {
+        auto a = std::make_unique<gfx_arena_s>();
+        a->mgr = std::make_unique<GpuManager>(dev, capacity_bytes, 0);
+        *out = a.release();
+    });
+}
+int gfx_arena_destroy(gfx_arena_t a) {
+    return guarded([&] { delete a; });
+}
+int gfx_arena_reset(gfx_arena_t a) {
+    return guarded([&] { a->mgr->reset(); });
+}
+int gfx_arena_free_pages(gfx_arena_t a, int32_t* out) {
+    return guarded([&] { *out = static_cast<int32_t>(a->mgr->free_pages()); });
+}
+int gfx_arena_resident(gfx_arena_t a, int model_idx, int32_t* out) {
+    return guarded([&] { *out = a->mgr->resident(model_idx) ? 1 : 0; });
+}
+
+static void make_event(GpuManager& m, cudaStream_t s, gfx_event_t* done) {
+    if (!done) return;
+    auto e = std::make_unique<gfx_event_s>();
+    e->device = m.device();
+    GFX_CUDA(cudaEventCreateWithFlags(&e->ev, cudaEventDisableTiming));
+    GFX_CUDA(cudaEventRecord(e->ev, s));
+    *done = e.release();
+}
+
+int gfx_load_h2d(gfx_arena_t a, int model_idx, gfx_event_t* done) {
+    return guarded([&] {
+        a->mgr->load(model_idx, nullptr);
+        make_event(*a->mgr, a->mgr->copy_stream(), done);
+    });
+}
+int gfx_fetch_p2p(gfx_arena_t dst, gfx_arena_t src, int model_idx, gfx_event_t* done) {
+    return guarded([&] {
+        if (!src->mgr->resident(model_idx)) throw std::invalid_argument("peer does not hold the model");
+        dst->mgr->load(model_idx, src->mgr.get());
+        make_event(*dst->mgr, dst->mgr->copy_stream(), done);
+    });
+}
+int gfx_evict(gfx_arena_t a, int model_idx) {
+    return guarded([&] { a->mgr->evict(model_idx); });
+}
+int gfx_infer(gfx_arena_t a, int model_idx, const float* in, float* out, int batch, gfx_event_t* done) {
+    return guarded([&] {
+        if (batch != 32) throw std::invalid_argument("batch must be 32");
+        a->mgr->infer(model_idx, in, out);
+        make_event(*a->mgr, a->mgr->compute_stream(), done);
+    });
+}
+
+int gfx_event_query(gfx_event_t e) {
+    cudaSetDevice(e->device);
+    const cudaError_t r = cudaEventQuery(e->ev);
+    if (r == cudaSuccess) return 0;
+    if (r == cudaErrorNotReady) {
+        cudaGetLastError();
+        return 1;
+    }
+    g_err = cudaGetErrorString(r);
+    return -GFX_ERR_CUDA;
+}
+int gfx_event_sync(gfx_event_t e) {
+    return guarded([&] {
+        GFX_CUDA(cudaSetDevice(e->device));
+        GFX_CUDA(cudaEventSynchronize(e->ev));
+    });
+}
+int gfx_event_release(gfx_event_t e) {
+    return guarded([&] {
+        if (e) {
+            cudaEventDestroy(e->ev);
+            delete e;
+        }
+    });
+}
+
+int gfx_device_alloc(gfx_arena_t a, uint64_t bytes, void** out) {
+    return guarded([&] {
+        a->mgr->activate();
+        GFX_CUDA(cudaMalloc(out, bytes));
+    });
+}
+int gfx_device_free(gfx_arena_t a, void* p) {
+    return guarded([&] {
+        a->mgr->activate();
+        GFX_CUDA(cudaFree(p));
+    });
+}
+int gfx_memcpy_h2d(gfx_arena_t a, void* dst, const void* src, uint64_t bytes) {
+    return guarded([&] {
+        a->mgr->activate();
+        GFX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, a->mgr->compute_stream()));
+        GFX_CUDA(cudaStreamSynchronize(a->mgr->compute_stream()));
+    });
+}
+int gfx_memcpy_d2h(gfx_arena_t a, void* dst, const void* src, uint64_t bytes) {
+    return guarded([&] {
+        a->mgr->activate();
+        GFX_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, a->mgr->compute_stream()));
+        GFX_CUDA(cudaStreamSynchronize(a->mgr->compute_stream()));
+    });
+}
+int gfx_synchronize(gfx_arena_t a) {
+    return guarded([&] {
+        a->mgr->activate();
+        GFX_CUDA(cudaStreamSynchronize(a->mgr->copy_stream()));
+        GFX_CUDA(cudaStreamSynchronize(a->mgr->compute_stream()));
+    });
+}
+int gfx_fill_params(gfx_arena_t a, float* dst, uint64_t n, uint64_t seed, uint32_t tensor, float scale) {
+    return guarded([&] {
+        a->mgr->activate();
+        gfx::launch_fill_params(dst, n, seed, tensor, scale, a->mgr->compute_stream());
+        GFX_CUDA(cudaStreamSynchronize(a->mgr->compute_stream()));
+    });
+}
+int gfx_host_fill_params(float* dst, uint64_t n, uint64_t seed, uint32_t tensor, float scale) {
+    return guarded([&] {
+        const uint64_t stream = gfx::param_stream(seed, tensor);
+        const float scaled = gfx::param_scale(scale);
+        for (uint64_t i = 0; i < n; ++i) dst[i] = gfx::param_at(stream, i, scaled);
+    });
+}
+uint64_t gfx_input_seed(int request_id) { return 0xC0FFEE0000000000ULL + static_cast<uint64_t>(request_id); }
+
+int gfx_replay_create(const gfx_replay_args* args, gfx_replay_t* out) {
+    return guarded([&] {
+        auto r = std::make_unique<gfx_replay_s>();
+        r->args = *args;
+        r->catalog_csv = args->catalog_csv ? args->catalog_csv : "";
+        if (args->trace_csv) r->trace_csv = args->trace_csv;
+        r->args.catalog_csv = r->catalog_csv.c_str();
+        r->args.trace_csv = args->trace_csv ? r->trace_csv.c_str() : nullptr;
+        r->setup();
+        *out = r.release();
+    });
+}
+int gfx_replay_run(gfx_replay_t r, gfx_replay_result* out) {
+    return guarded([&] { r->run(out); });
+}
+int gfx_replay_outputs(gfx_replay_t r, float* host, uint64_t count) {
+    return guarded([&] {
+        if (!r->full_outputs) throw std::invalid_argument("replay was created without keep_outputs");
+        const size_t n = r->requests.size();
+        if (count < n * r->out_elems) throw std::invalid_argument("output buffer too small");
+        // Outputs live on the GPU that served each request.
+        std::vector<float> tmp(r->out_elems);
+        for (size_t g = 0; g < r->mgrs.size(); ++g) {
+            if (!r->mgrs[g]) continue;
+            GFX_CUDA(cudaSetDevice(r->dev_of[g]));
+            GFX_CUDA(cudaDeviceSynchronize());
+        }
+        // Route each request to the GPU whose manager executed it (last run).
+        for (size_t i = 0; i < n; ++i) {
+            const int g = r->req_gpu[i] >= 0 ? r->req_gpu[i] : (r->args.only_gpu >= 0 ? r->args.only_gpu : 0);
+            if (!r->mgrs[static_cast<size_t>(g)]) continue;
+            GFX_CUDA(cudaSetDevice(r->dev_of[static_cast<size_t>(g)]));
+            GFX_CUDA(cudaMemcpy(host + i * r->out_elems, r->bufs[static_cast<size_t>(g)].outputs + i * r->out_elems,
+                                sizeof(float) * r->out_elems, cudaMemcpyDeviceToHost));
+        }
+    });
+}
+int gfx_replay_requests(gfx_replay_t r, int32_t* model_idx, double* service_ms, int64_t n) {
+    return guarded([&] {
+        for (int64_t i = 0; i < n && static_cast<size_t>(i) < r->last_models.size(); ++i) {
+            if (model_idx) model_idx[i] = r->last_models[static_cast<size_t>(i)];
+            if (service_ms)
+                service_ms[i] = (r->req_start[static_cast<size_t>(i)] && r->req_end[static_cast<size_t>(i)])
+                                    ? elapsed_ms(r->req_start[static_cast<size_t>(i)], r->req_end[static_cast<size_t>(i)])
+                                    : -1.0;
+        }
+    });
+}
+int gfx_replay_destroy(gfx_replay_t r) {
+    return guarded([&] { delete r; });
+}
+int gfx_replay(const gfx_replay_args* args, gfx_replay_result* out) {
+    gfx_replay_t r = nullptr;
+    int rc = gfx_replay_create(args, &r);
+    if (rc) return rc;
+    rc = gfx_replay_run(r, out);
+    gfx_replay_destroy(r);
+    return rc;
+}
+
+}  // extern "C"

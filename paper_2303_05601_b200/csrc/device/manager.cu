@@ -1,0 +1,335 @@
+// GPU Manager implementation — see manager.cuh.
+#include "manager.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <thread>
+
+namespace gfx {
+
+namespace {
+constexpr int kMaxDim = 8192;  // widest layer the inference workspace supports
+constexpr int kBatch = 32;
+}  // namespace
+
+// ------------------------------------------------------------- model store
+
+ModelBlob::~ModelBlob() {
+    if (host) cudaFreeHost(host);
+}
+
+void mlp_layout(const gfx_model_desc& d, std::vector<uint64_t>& w_off, std::vector<uint64_t>& b_off,
+                uint64_t& bytes) {
+    w_off.clear();
+    b_off.clear();
+    uint64_t off = 0;
+    auto align = [](uint64_t v) { return (v + 255) & ~uint64_t{255}; };
+    for (int l = 0; l < d.n_layers; ++l) {
+        const uint64_t K = static_cast<uint64_t>(d.dims[l]);
+        const uint64_t N = static_cast<uint64_t>(d.dims[l + 1]);
+        w_off.push_back(off);
+        off = align(off + 4 * K * N);
+        b_off.push_back(off);
+        off = align(off + 4 * N);
+    }
+    bytes = off;
+}
+
+ModelStore& ModelStore::get() {
+    static ModelStore store;
+    return store;
+}
+
+void ModelStore::add(int idx, const gfx_model_desc& desc) {
+    if (idx < 0) throw std::invalid_argument("model index must be >= 0");
+    if (desc.family != GFX_MODEL_MLP) throw std::invalid_argument("unsupported model family");
+    if (desc.n_layers < 1 || desc.n_layers > GFX_MAX_LAYERS) throw std::invalid_argument("bad layer count");
+    if (desc.batch != kBatch) throw std::invalid_argument("batch must be 32");
+    for (int l = 0; l <= desc.n_layers; ++l)
+        if (desc.dims[l] <= 0 || desc.dims[l] > kMaxDim) throw std::invalid_argument("bad layer width");
+    for (int l = 0; l < desc.n_layers; ++l)
+        if (desc.dims[l] % 32 != 0 || desc.dims[l + 1] % 4 != 0)
+            throw std::invalid_argument("layer inputs must be multiples of 32, outputs of 4");
+
+    auto blob = std::make_unique<ModelBlob>();
+    blob->desc = desc;
+    mlp_layout(desc, blob->w_off, blob->b_off, blob->bytes);
+    blob->pages = static_cast<uint32_t>((blob->bytes + kPageBytes - 1) / kPageBytes);
+    if (blob->pages > GFX_MAX_PAGES) throw std::invalid_argument("model larger than the page-table limit");
+    GFX_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&blob->host), blob->bytes, cudaHostAllocDefault));
+    std::memset(blob->host, 0, blob->bytes);
+
+    // Parameters, generated in parallel on the host.
+    struct Job {
+        float* dst;
+        uint64_t n;
+        uint64_t stream;
+        float scaled;
+    };
+    std::vector<Job> jobs;
+    double flops = 0, wbytes = 0;
+    for (int l = 0; l < desc.n_layers; ++l) {
+        const uint64_t K = static_cast<uint64_t>(desc.dims[l]);
+        const uint64_t N = static_cast<uint64_t>(desc.dims[l + 1]);
+        const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(K)));
+        char* base = reinterpret_cast<char*>(blob->host);
+        jobs.push_back({reinterpret_cast<float*>(base + blob->w_off[l]), K * N,
+                        param_stream(desc.seed, static_cast<uint32_t>(2 * l)), param_scale(scale)});
+        jobs.push_back({reinterpret_cast<float*>(base + blob->b_off[l]), N,
+                        param_stream(desc.seed, static_cast<uint32_t>(2 * l + 1)), param_scale(scale)});
+        flops += 2.0 * kBatch * static_cast<double>(K) * static_cast<double>(N);
+        wbytes += 4.0 * static_cast<double>(K * N + N) + 4.0 * kBatch * static_cast<double>(K + N);
+    }
+    blob->flops = flops;
+    blob->alg_bytes = wbytes;
+    unsigned nthreads = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < nthreads; ++t)
+        pool.emplace_back([&, t] {
+            for (const Job& j : jobs) {
+                const uint64_t chunk = (j.n + nthreads - 1) / nthreads;
+                const uint64_t lo = std::min<uint64_t>(j.n, t * chunk), hi = std::min<uint64_t>(j.n, lo + chunk);
+                for (uint64_t i = lo; i < hi; ++i) j.dst[i] = param_at(j.stream, i, j.scaled);
+            }
+        });
+    for (auto& th : pool) th.join();
+
+    std::lock_guard<std::mutex> lk(mu_);
+    if (static_cast<size_t>(idx) >= blobs_.size()) blobs_.resize(static_cast<size_t>(idx) + 1);
+    blobs_[static_cast<size_t>(idx)] = std::move(blob);
+}
+
+const ModelBlob& ModelStore::at(int idx) const {
+    std::lock_guard<std::mutex> lk(mu_);
+    if (idx < 0 || static_cast<size_t>(idx) >= blobs_.size() || !blobs_[static_cast<size_t>(idx)])
+        throw std::invalid_argument("model " + std::to_string(idx) + " is not registered");
+    return *blobs_[static_cast<size_t>(idx)];
+}
+
+bool ModelStore::has(int idx) const {
+    std::lock_guard<std::mutex> lk(mu_);
+    return idx >= 0 && static_cast<size_t>(idx) < blobs_.size() && blobs_[static_cast<size_t>(idx)];
+}
+
+void ModelStore::clear() {
+    std::lock_guard<std::mutex> lk(mu_);
+    blobs_.clear();
+}
+
+// ------------------------------------------------------------- timer
+
+cudaEvent_t KernelTimer::next() {
+    if (used == ev.size()) {
+        cudaEvent_t e;
+        GFX_CUDA(cudaEventCreate(&e));
+        ev.push_back(e);
+    }
+    return ev[used++];
+}
+
+// ------------------------------------------------------------- manager
+
+GpuManager::GpuManager(int device, uint64_t capacity_bytes, int manager_id) : device_(device), id_(manager_id) {
+    if (capacity_bytes == 0 || capacity_bytes % kPageBytes != 0)
+        throw std::invalid_argument("arena capacity must be a positive multiple of 2 MiB");
+    activate();
+    npages_ = static_cast<uint32_t>(capacity_bytes / kPageBytes);
+    GFX_CUDA(cudaMalloc(&arena_, capacity_bytes));
+    for (uint32_t p = 0; p < npages_; ++p) free_.insert(p);
+    GFX_CUDA(cudaStreamCreateWithFlags(&compute_, cudaStreamNonBlocking));
+    GFX_CUDA(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
+    GFX_CUDA(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, device_));
+    max_dim_ = kMaxDim;
+    GFX_CUDA(cudaMalloc(&act_[0], sizeof(float) * kBatch * kMaxDim));
+    GFX_CUDA(cudaMalloc(&act_[1], sizeof(float) * kBatch * kMaxDim));
+    GFX_CUDA(cudaMalloc(&ws_, sizeof(float) * kMaxSplits * kBatch * kMaxDim));
+    const int ncnt = kMaxDim / 64 + 2;
+    GFX_CUDA(cudaMalloc(&counters_, sizeof(unsigned) * ncnt));
+    GFX_CUDA(cudaMalloc(&stats_, sizeof(float) * 2 * kBatch * ncnt));
+    GFX_CUDA(cudaMemset(counters_, 0, sizeof(unsigned) * ncnt));
+    GFX_CUDA(cudaDeviceSynchronize());
+}
+
+GpuManager::~GpuManager() {
+    cudaSetDevice(device_);
+    cudaStreamSynchronize(compute_);
+    cudaStreamSynchronize(copy_);
+    for (Slot& s : slots_) {
+        if (s.loaded) cudaEventDestroy(s.loaded);
+        if (s.last_use) cudaEventDestroy(s.last_use);
+    }
+    cudaFree(arena_);
+    cudaFree(act_[0]);
+    cudaFree(act_[1]);
+    cudaFree(ws_);
+    cudaFree(counters_);
+    cudaFree(stats_);
+    cudaStreamDestroy(compute_);
+    cudaStreamDestroy(copy_);
+}
+
+void GpuManager::activate() const { GFX_CUDA(cudaSetDevice(device_)); }
+
+GpuManager::Slot& GpuManager::slot(int model) {
+    if (model < 0) throw std::invalid_argument("negative model index");
+    if (static_cast<size_t>(model) >= slots_.size()) slots_.resize(static_cast<size_t>(model) + 1);
+    Slot& s = slots_[static_cast<size_t>(model)];
+    if (!s.loaded) {
+        GFX_CUDA(cudaEventCreateWithFlags(&s.loaded, cudaEventDisableTiming));
+        GFX_CUDA(cudaEventCreateWithFlags(&s.last_use, cudaEventDisableTiming));
+    }
+    return s;
+}
+
+bool GpuManager::resident(int model) const {
+    return model >= 0 && static_cast<size_t>(model) < slots_.size() && slots_[static_cast<size_t>(model)].live;
+}
+
+cudaEvent_t GpuManager::loaded_event(int model) const {
+    if (!resident(model)) throw std::logic_error("loaded_event of non-resident model");
+    return slots_[static_cast<size_t>(model)].loaded;
+}
+
+const std::vector<uint32_t>& GpuManager::pages_of(int model) const {
+    if (!resident(model)) throw std::logic_error("pages_of non-resident model");
+    return slots_[static_cast<size_t>(model)].pages;
+}
+
+void GpuManager::add_reader(int model, cudaEvent_t e) { slot(model).readers.push_back(e); }
+
+// ClusterState::evict_one (proj/src/cluster.cpp:117-129) on device: the pages
+// return to the pool at once (host bookkeeping), and the copy stream — the
+// only writer of arena pages — is ordered after every pending reader of them
+// (the model's last inference and any peer fetch out of them), so a later
+// load can never overwrite weights still in use.
+void GpuManager::evict(int model) {
+    Slot& s = slot(model);
+    if (!s.live) throw std::logic_error("evict of non-resident model " + std::to_string(model));
+    activate();
+    GFX_CUDA(cudaStreamWaitEvent(copy_, s.last_use, 0));
+    for (cudaEvent_t r : s.readers) GFX_CUDA(cudaStreamWaitEvent(copy_, r, 0));
+    s.readers.clear();
+    for (uint32_t p : s.pages) free_.insert(p);
+    s.pages.clear();
+    s.live = false;
+}
+
+// The load that replaces profile.load_time_us (proj/src/cluster.cpp:163-167).
+uint64_t GpuManager::load(int model, GpuManager* src) {
+    const ModelBlob& blob = ModelStore::get().at(model);
+    Slot& s = slot(model);
+    if (s.live) throw std::logic_error("load of resident model " + std::to_string(model));
+    if (free_.size() < blob.pages)
+        throw std::logic_error("arena out of pages: the control plane's capacity model and the arena disagree");
+    activate();
+    s.pages.clear();
+    for (uint32_t i = 0; i < blob.pages; ++i) {
+        s.pages.push_back(*free_.begin());
+        free_.erase(free_.begin());
+    }
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    if (load_timer) {
+        t0 = load_timer->next();
+        t1 = load_timer->next();
+        GFX_CUDA(cudaEventRecord(t0, copy_));
+    }
+    if (src == nullptr) {
+        // Pinned-host H2D, one copy per run of contiguous destination pages.
+        const char* host = reinterpret_cast<const char*>(blob.host);
+        uint32_t i = 0;
+        while (i < blob.pages) {
+            uint32_t j = i + 1;
+            while (j < blob.pages && s.pages[j] == s.pages[j - 1] + 1) ++j;
+            const uint64_t off = static_cast<uint64_t>(i) * kPageBytes;
+            const uint64_t len = std::min<uint64_t>(static_cast<uint64_t>(j - i) * kPageBytes, blob.bytes - off);
+            GFX_CUDA(cudaMemcpyAsync(arena_ + static_cast<uint64_t>(s.pages[i]) * kPageBytes, host + off, len,
+                                     cudaMemcpyHostToDevice, copy_));
+            i = j;
+        }
+    } else {
+        // NVLink peer fetch from the holder's arena (false miss): wait until
+        // the holder's copy is complete, copy runs contiguous on both sides,
+        // and register the fetch as a reader of the holder's pages.
+        const std::vector<uint32_t>& sp = src->pages_of(model);
+        GFX_CUDA(cudaStreamWaitEvent(copy_, src->loaded_event(model), 0));
+        uint32_t i = 0;
+        while (i < blob.pages) {
+            uint32_t j = i + 1;
+            while (j < blob.pages && s.pages[j] == s.pages[j - 1] + 1 && sp[j] == sp[j - 1] + 1) ++j;
+            const uint64_t off = static_cast<uint64_t>(i) * kPageBytes;
+            const uint64_t len = std::min<uint64_t>(static_cast<uint64_t>(j - i) * kPageBytes, blob.bytes - off);
+            GFX_CUDA(cudaMemcpyPeerAsync(arena_ + static_cast<uint64_t>(s.pages[i]) * kPageBytes, device_,
+                                         src->arena() + static_cast<uint64_t>(sp[i]) * kPageBytes, src->device(),
+                                         len, copy_));
+            i = j;
+        }
+    }
+    if (load_timer) GFX_CUDA(cudaEventRecord(t1, copy_));
+    GFX_CUDA(cudaEventRecord(s.loaded, copy_));
+    if (src) src->add_reader(model, s.loaded);
+    s.live = true;
+    // Inference of this model on the compute stream starts after the load.
+    GFX_CUDA(cudaStreamWaitEvent(compute_, s.loaded, 0));
+    return blob.bytes;
+}
+
+void GpuManager::build_page_table(const Slot& s, PageTable& pt) const {
+    pt.n = static_cast<uint32_t>(s.pages.size());
+    for (size_t i = 0; i < s.pages.size(); ++i) pt.page[i] = s.pages[i];
+}
+
+// The batched inference that replaces profile.infer_time_us
+// (proj/src/cluster.cpp:161,167): one K1 launch per layer on the compute stream.
+void GpuManager::infer(int model, const float* in, float* out) {
+    const ModelBlob& blob = ModelStore::get().at(model);
+    Slot& s = slot(model);
+    if (!s.live) throw std::logic_error("inference of non-resident model " + std::to_string(model));
+    activate();
+    MlpLayerArgs a{};
+    a.arena = arena_;
+    build_page_table(s, a.pt);
+    a.ws = ws_;
+    a.counters = counters_;
+    a.stats = stats_;
+    a.ldws = max_dim_;
+    const int L = blob.desc.n_layers;
+    const int C = blob.desc.dims[L];
+    const float* x = in;
+    for (int l = 0; l < L; ++l) {
+        a.K = blob.desc.dims[l];
+        a.N = blob.desc.dims[l + 1];
+        a.x = x;
+        const bool last = l + 1 == L;
+        a.y = last ? out : act_[l & 1];
+        a.probs = last ? out + static_cast<size_t>(kBatch) * C : nullptr;
+        a.relu = last ? 0 : 1;
+        a.w_off = blob.w_off[l];
+        a.b_off = blob.b_off[l];
+        a.ntiles = mlp_layer_tiles(a.N);
+        a.splits = mlp_layer_splits(a.K, a.N, sm_count_);
+        if (layer_timer) GFX_CUDA(cudaEventRecord(layer_timer->next(), compute_));
+        launch_mlp_layer(a, compute_);
+        if (layer_timer) GFX_CUDA(cudaEventRecord(layer_timer->next(), compute_));
+        ++kernel_launches;
+        x = a.y;
+    }
+    GFX_CUDA(cudaEventRecord(s.last_use, compute_));
+}
+
+void GpuManager::reset() {
+    activate();
+    GFX_CUDA(cudaStreamSynchronize(copy_));
+    GFX_CUDA(cudaStreamSynchronize(compute_));
+    for (Slot& s : slots_) {
+        for (uint32_t p : s.pages) free_.insert(p);
+        s.pages.clear();
+        s.readers.clear();
+        s.live = false;
+    }
+    GFX_CUDA(cudaMemset(counters_, 0, sizeof(unsigned) * (kMaxDim / 64 + 2)));
+    GFX_CUDA(cudaDeviceSynchronize());
+}
+
+}  // namespace gfx

@@ -1,0 +1,123 @@
+#pragma once
+// Per-B200 GPU Manager (the paper's GPU Manager, whose
+// cache bookkeeping the reference models in proj/src/cluster.cpp): owns a
+// pre-allocated HBM arena of 2 MiB pages, a copy stream for model loads
+// (pinned-host H2D or NVLink peer fetch) and a compute stream for batched
+// inference, and executes the cache operations the control plane decides.
+//
+// Arena layout: capacity / 2 MiB pages in one cudaMalloc. A model occupies
+// ceil(bytes / 2 MiB) pages anywhere in the arena (page table passed by value
+// to every kernel), so the reference's sum-of-sizes capacity model
+// (proj/src/cluster.cpp:107,133-147) is exact: any model set whose page
+// counts fit the budget fits physically — no fragmentation, no compaction.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <mutex>
+#include <set>
+#include <vector>
+
+#include "common.cuh"
+#include "gpufaas_b200.h"
+#include "mlp_ffma.cuh"
+
+namespace gfx {
+
+// One model of the pinned host model store.
+struct ModelBlob {
+    gfx_model_desc desc{};
+    uint64_t bytes = 0;
+    uint32_t pages = 0;
+    std::vector<uint64_t> w_off, b_off;  // per layer, offsets in the blob
+    float* host = nullptr;               // pinned (cudaHostAlloc)
+    double flops = 0;                    // per inference (2 * batch * sum K*N)
+    double alg_bytes = 0;                // per inference: weights + biases + in/out activations
+    ~ModelBlob();
+};
+
+class ModelStore {
+public:
+    static ModelStore& get();
+    void add(int idx, const gfx_model_desc& desc);
+    const ModelBlob& at(int idx) const;
+    bool has(int idx) const;
+    void clear();
+    int max_dim() const;
+
+private:
+    mutable std::mutex mu_;
+    std::vector<std::unique_ptr<ModelBlob>> blobs_;
+};
+
+// Blob layout of an MLP: per layer W [N x K] then b [N], fp32,
+// each aligned to 256 B.
+void mlp_layout(const gfx_model_desc& d, std::vector<uint64_t>& w_off, std::vector<uint64_t>& b_off,
+                uint64_t& bytes);
+
+struct KernelTimer {  // optional per-launch CUDA-event timing
+    std::vector<cudaEvent_t> ev;
+    size_t used = 0;
+    cudaEvent_t next();
+};
+
+class GpuManager {
+public:
+    GpuManager(int device, uint64_t capacity_bytes, int manager_id);
+    ~GpuManager();
+    GpuManager(const GpuManager&) = delete;
+    GpuManager& operator=(const GpuManager&) = delete;
+
+    int device() const { return device_; }
+    uint32_t total_pages() const { return npages_; }
+    uint32_t free_pages() const { return static_cast<uint32_t>(free_.size()); }
+    bool resident(int model) const;
+
+    // Cache operations (asynchronous; host bookkeeping is immediate).
+    void evict(int model);
+    // Returns bytes copied. src == nullptr -> pinned host store.
+    uint64_t load(int model, GpuManager* src);
+    void infer(int model, const float* in, float* out);
+    void reset();  // synchronise and drop every resident model
+
+    cudaStream_t compute_stream() const { return compute_; }
+    cudaStream_t copy_stream() const { return copy_; }
+    cudaEvent_t loaded_event(int model) const;
+    void add_reader(int model, cudaEvent_t e);  // peer fetch in flight from our pages
+    const std::vector<uint32_t>& pages_of(int model) const;
+    char* arena() const { return arena_; }
+    void activate() const;  // cudaSetDevice
+
+    // Instrumentation (all optional).
+    KernelTimer* layer_timer = nullptr;   // records around every layer launch
+    KernelTimer* load_timer = nullptr;    // records around every model load
+    int64_t kernel_launches = 0;
+
+private:
+    struct Slot {
+        bool live = false;
+        std::vector<uint32_t> pages;
+        cudaEvent_t loaded = nullptr;       // copy stream, after the load
+        cudaEvent_t last_use = nullptr;     // compute stream, after the last inference
+        std::vector<cudaEvent_t> readers;   // peer fetches out of our pages
+    };
+    Slot& slot(int model);
+    void build_page_table(const Slot& s, PageTable& pt) const;
+
+    int device_;
+    int id_;
+    uint32_t npages_ = 0;
+    char* arena_ = nullptr;
+    std::set<uint32_t> free_;  // lowest-first allocation keeps page runs contiguous
+    std::vector<Slot> slots_;
+    cudaStream_t compute_ = nullptr, copy_ = nullptr;
+    int sm_count_ = 148;
+    // inference workspace
+    float* act_[2] = {nullptr, nullptr};
+    float* ws_ = nullptr;
+    unsigned* counters_ = nullptr;
+    float* stats_ = nullptr;
+    int max_dim_ = 0;
+};
+
+}  // namespace gfx

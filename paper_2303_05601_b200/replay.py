@@ -1,0 +1,100 @@
+"""Trace replay through the product C-ABI (gfx_replay_*)."""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _ffi
+
+POLICIES = {"lb": 0, "lalb": 1, "lalbo3": 2}
+
+
+def sim_config(gpus=1, capacity_mb=204.0, policy="lalbo3", o3_limit=25, working_set=15, rpm=325,
+               minutes=6, seed=1, syn_functions=60, syn_minutes=6, syn_draws=3000, syn_zipf=0.7063,
+               syn_seed=91) -> _ffi.SimConfig:
+    """Reference SimConfig (proj/include/gpufaas/engine.hpp:20-32) with the C2 arena."""
+    c = _ffi.SimConfig()
+    c.gpu_count = gpus
+    c.policy = POLICIES[policy] if isinstance(policy, str) else int(policy)
+    c.o3_limit = o3_limit
+    c.working_set = working_set
+    c.per_minute_total = rpm
+    c.duration_minutes = minutes
+    c.use_synthetic_trace = 1
+    c.syn_function_count = syn_functions
+    c.syn_minutes = syn_minutes
+    c.syn_draws_per_minute = syn_draws
+    c.syn_zipf_exponent = syn_zipf
+    c.syn_seed = syn_seed
+    c.capacity_mb = capacity_mb
+    c.seed = seed
+    return c
+
+
+@dataclass
+class ReplayResult:
+    raw: dict
+
+    def __getattr__(self, k):
+        try:
+            return self.raw[k]
+        except KeyError as e:
+            raise AttributeError(k) from e
+
+
+class Replay:
+    """One replay context (GPU managers, device buffers, events) reused across runs."""
+
+    def __init__(self, catalog_csv: str, cfg: _ffi.SimConfig, n_devices=1, first_device=0, only_gpu=-1,
+                 use_p2p=False, host_io=False, record_kernels=False, record_requests=False,
+                 keep_outputs=False, host_inputs: np.ndarray | None = None,
+                 host_outputs: np.ndarray | None = None):
+        self._cat = catalog_csv.encode()
+        a = _ffi.ReplayArgs()
+        a.catalog_csv = self._cat
+        a.trace_csv = None
+        a.cfg = cfg
+        a.n_devices = n_devices
+        a.first_device = first_device
+        a.only_gpu = only_gpu
+        a.use_p2p = int(use_p2p)
+        a.host_io = int(host_io)
+        a.record_kernels = int(record_kernels)
+        a.record_requests = int(record_requests)
+        a.keep_outputs = int(keep_outputs)
+        self._in = host_inputs
+        self._out = host_outputs
+        a.host_inputs = host_inputs.ctypes.data if host_inputs is not None else None
+        a.host_outputs = host_outputs.ctypes.data if host_outputs is not None else None
+        self.args = a
+        self.h = C.c_void_p()
+        _ffi.check(_ffi.gfx_replay_create(C.byref(a), C.byref(self.h)))
+
+    def run(self) -> ReplayResult:
+        r = _ffi.ReplayResultC()
+        _ffi.check(_ffi.gfx_replay_run(self.h, C.byref(r)))
+        return ReplayResult({k: getattr(r, k) for k, _ in r._fields_})
+
+    def outputs(self, n_requests: int, classes: int = 1000) -> np.ndarray:
+        out = np.zeros((n_requests, 2, 32, classes), dtype=np.float32)
+        _ffi.check(_ffi.gfx_replay_outputs(self.h, out.ctypes.data, out.size))
+        return out
+
+    def request_info(self, n_requests: int):
+        mi = np.zeros(n_requests, np.int32)
+        svc = np.zeros(n_requests, np.float64)
+        _ffi.check(_ffi.gfx_replay_requests(self.h, mi.ctypes.data, svc.ctypes.data, n_requests))
+        return mi, svc
+
+    def close(self):
+        if self.h:
+            _ffi.check(_ffi.gfx_replay_destroy(self.h))
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
