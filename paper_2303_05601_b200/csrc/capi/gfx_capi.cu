@@ -160,9 +160,8 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
             GFX_CUDA(cudaEventCreate(&b.stop));
             if (!args.host_io) {
                 // HBM-resident inputs, generated once outside the timed region.
-                for (size_t r = 0; r < n; ++r)
-                    gfx::launch_fill_params(b.inputs + r * in_elems, in_elems, gfx_input_seed(static_cast<int>(r)),
-                                            0xFFFFFFFFu, 1.0f, mgrs[g]->compute_stream());
+                gfx::launch_fill_params(b.inputs, in_elems, gfx_input_seed(0), 0xFFFFFFFFu, 1.0f,
+                                        mgrs[g]->compute_stream(), n);
             }
             GFX_CUDA(cudaDeviceSynchronize());
         }

@@ -25,16 +25,19 @@ void mlp_layout(const gfx_model_desc& d, std::vector<uint64_t>& w_off, std::vect
     w_off.clear();
     b_off.clear();
     uint64_t off = 0;
-    auto align = [](uint64_t v) { return (v + 255) & ~uint64_t{255}; };
+    auto align = [](uint64_t v, uint64_t a) { return (v + a - 1) & ~(a - 1); };
     for (int l = 0; l < d.n_layers; ++l) {
         const uint64_t K = static_cast<uint64_t>(d.dims[l]);
         const uint64_t N = static_cast<uint64_t>(d.dims[l + 1]);
+        const uint64_t Npad = align(N, kWTileRows);
+        off = align(off, 16384);  // tiles never straddle a 2 MiB page
         w_off.push_back(off);
-        off = align(off + 4 * K * N);
+        off += 4 * K * Npad;
+        off = align(off, 256);
         b_off.push_back(off);
-        off = align(off + 4 * N);
+        off += 4 * N;
     }
-    bytes = off;
+    bytes = align(off, 256);
 }
 
 ModelStore& ModelStore::get() {
@@ -64,7 +67,8 @@ void ModelStore::add(int idx, const gfx_model_desc& desc) {
     // Parameters, generated in parallel on the host.
     struct Job {
         float* dst;
-        uint64_t n;
+        uint64_t n;        // values
+        uint64_t K;        // > 0: weight matrix [n / K x K] written as swizzled tiles
         uint64_t stream;
         float scaled;
     };
@@ -75,9 +79,9 @@ void ModelStore::add(int idx, const gfx_model_desc& desc) {
         const uint64_t N = static_cast<uint64_t>(desc.dims[l + 1]);
         const float scale = static_cast<float>(1.0 / std::sqrt(static_cast<double>(K)));
         char* base = reinterpret_cast<char*>(blob->host);
-        jobs.push_back({reinterpret_cast<float*>(base + blob->w_off[l]), K * N,
+        jobs.push_back({reinterpret_cast<float*>(base + blob->w_off[l]), K * N, K,
                         param_stream(desc.seed, static_cast<uint32_t>(2 * l)), param_scale(scale)});
-        jobs.push_back({reinterpret_cast<float*>(base + blob->b_off[l]), N,
+        jobs.push_back({reinterpret_cast<float*>(base + blob->b_off[l]), N, 0,
                         param_stream(desc.seed, static_cast<uint32_t>(2 * l + 1)), param_scale(scale)});
         flops += 2.0 * kBatch * static_cast<double>(K) * static_cast<double>(N);
         wbytes += 4.0 * static_cast<double>(K * N + N) + 4.0 * kBatch * static_cast<double>(K + N);
@@ -91,7 +95,14 @@ void ModelStore::add(int idx, const gfx_model_desc& desc) {
             for (const Job& j : jobs) {
                 const uint64_t chunk = (j.n + nthreads - 1) / nthreads;
                 const uint64_t lo = std::min<uint64_t>(j.n, t * chunk), hi = std::min<uint64_t>(j.n, lo + chunk);
-                for (uint64_t i = lo; i < hi; ++i) j.dst[i] = param_at(j.stream, i, j.scaled);
+                if (j.K == 0) {
+                    for (uint64_t i = lo; i < hi; ++i) j.dst[i] = param_at(j.stream, i, j.scaled);
+                } else {
+                    char* dst = reinterpret_cast<char*>(j.dst);
+                    for (uint64_t i = lo; i < hi; ++i)  // logical W[n][k] = stream[n*K + k]
+                        *reinterpret_cast<float*>(dst + wtile_offset(i / j.K, i % j.K, j.K)) =
+                            param_at(j.stream, i, j.scaled);
+                }
             }
         });
     for (auto& th : pool) th.join();

@@ -20,7 +20,7 @@
 
 #include "common.cuh"
 #include "gpufaas_b200.h"
-#include "mlp_ffma.cuh"
+#include "mlp.cuh"
 
 namespace gfx {
 
@@ -50,8 +50,8 @@ private:
     std::vector<std::unique_ptr<ModelBlob>> blobs_;
 };
 
-// Blob layout of an MLP: per layer W [N x K] then b [N], fp32,
-// each aligned to 256 B.
+// Blob layout of an MLP: per layer the weight tiles (16 KB,
+// 16 KB-aligned, N padded to 128 rows) then b [N] fp32 (256 B-aligned).
 void mlp_layout(const gfx_model_desc& d, std::vector<uint64_t>& w_off, std::vector<uint64_t>& b_off,
                 uint64_t& bytes);
 

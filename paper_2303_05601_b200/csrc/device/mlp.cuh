@@ -11,11 +11,11 @@ namespace gfx {
 constexpr int kMaxSplits = 32;
 
 struct MlpLayerArgs {
-    const float* x;        // [32 x K] activations, row-major, device
+    const float* x;        // [32 x K] activations, row-major, device (read through a TMA tensor map)
     float* y;              // [32 x N] output rows
     float* probs;          // last layer: [32 x N] softmax rows; else nullptr
     const char* arena;     // arena base
-    uint64_t w_off;        // model-blob offset of W [N x K]
+    uint64_t w_off;        // model-blob offset of W: ceil(N/128) x (K/32) swizzled 16 KB tiles
     uint64_t b_off;        // model-blob offset of b [N]
     int K, N;
     int splits, ntiles;
@@ -31,6 +31,17 @@ int mlp_layer_splits(int K, int N, int sm_count);
 int mlp_layer_tiles(int N);
 size_t mlp_layer_smem();
 void launch_mlp_layer(const MlpLayerArgs& a, cudaStream_t stream);
-void launch_fill_params(float* dst, uint64_t n, uint64_t seed, uint32_t tensor, float scale, cudaStream_t s);
+// Fills `count` consecutive tensors of n values, tensor t from seed + t.
+void launch_fill_params(float* dst, uint64_t n, uint64_t seed, uint32_t tensor, float scale, cudaStream_t s,
+                        uint64_t count = 1);
+
+// Weight tiles of the blob: 128 x 32 fp32, K-major SWIZZLE_128B image (16 KB).
+constexpr int kWTileRows = 128;
+constexpr int kWTileK = 32;
+__host__ __device__ inline uint64_t wtile_offset(uint64_t n, uint64_t k, uint64_t K) {
+    const uint64_t mt = n / kWTileRows, r = n % kWTileRows, kt = k / kWTileK, kk = k % kWTileK;
+    const uint64_t tile = mt * (K / kWTileK) + kt;
+    return tile * (kWTileRows * kWTileK * 4) + r * 128 + (((kk >> 2) ^ (r & 7)) << 4) + (kk & 3) * 4;
+}
 
 }  // namespace gfx

@@ -1,0 +1,429 @@
+// K1: fp32 linear layer of the MLP model family at batch 32 on the 5th-gen
+// tensor cores (tcgen05, kind::tf32) with 3xTF32 error compensation, weights
+// streamed by TMA straight out of the paged HBM arena.
+//
+//   Y[32 x N] = act(X[32 x K] . W^T + b);  computed as D^T[N x 32] = W . X^T
+//   ("swap AB": the weight rows fill the 128-row MMA M side, the 32 batch rows
+//   are the MMA N side), act = ReLU on hidden layers; the last layer also
+//   produces softmax(Y) rows.
+//
+// Precision: fp32 inputs are split v = hi + lo with hi = v with the low 13
+// mantissa bits cleared (exactly representable in TF32) and lo = v - hi
+// (exact). D += W_lo.X_hi + W_hi.X_lo + W_hi.X_hi, FP32 accumulation in TMEM:
+// ~fp32 accuracy (the dropped W_lo.X_lo term is < 2^-20 relative), which the
+// north-star fp32 tolerance (1e-5) requires — plain TF32 would not meet it.
+//
+// Bound: batch 32 gives 16 flop per weight byte; three TF32 MMAs per product
+// still leave the tensor pipe far from its limit, so the kernel is bound by
+// streaming fp32 weights from HBM.
+//
+// Structure, one CTA per (128-feature tile, K split), 1 CTA per SM:
+//   warp 0      TMA producer: per 32-wide K step one 1-D bulk copy of the
+//               16 KB pre-swizzled weight tile (the model blob stores W as
+//               SWIZZLE_128B K-major 128x32 tiles, so a tile never straddles
+//               a 2 MiB arena page) + one 2-D tensor copy of the 32x32 X tile;
+//   warps 2-5   split each landed stage into hi/lo planes in place
+//               (elementwise, so the swizzled layout is preserved), then
+//               fence.proxy.async and arrive;
+//   warp 1      one elected thread issues 12 tcgen05.mma (4 K slices x 3
+//               products) per stage into a 128x32 fp32 TMEM accumulator and
+//               commits the stage back to the producer; accumulators are
+//               double-buffered per chunk of 4 K tiles;
+//   warps 2-5   drain each finished chunk (tcgen05.ld of their 32-lane TMEM
+//               quarter) into fp32 registers while the next chunk runs, then
+//               the epilogue: split-K
+//               partials through a global workspace reduced by the last CTA of
+//               the feature tile in fixed split order (deterministic), bias +
+//               ReLU, and on the last layer a two-level softmax.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <mutex>
+#include <stdexcept>
+
+#include "common.cuh"
+#include "mlp.cuh"
+#include "sm100.cuh"
+
+namespace gfx {
+
+namespace {
+
+using namespace gfx::sm100;
+
+constexpr int kRows = 32;        // batch rows per request = MMA N
+constexpr int kTileM = 128;      // output features per CTA = MMA M
+constexpr int kTileK = 32;       // fp32 K per stage (= one 128-byte swizzle row)
+constexpr int kStages = 4;
+constexpr int kThreads = 192;    // 6 warps
+constexpr uint32_t kWBytes = kTileM * kTileK * 4;  // 16 KB
+constexpr uint32_t kXBytes = kRows * kTileK * 4;   // 4 KB
+constexpr uint32_t kStageBytes = 2 * kWBytes + 2 * kXBytes;
+constexpr uint32_t kTmemCols = 64;  // two 32-column accumulators (double-buffered chunks)
+constexpr int kChunk = 4;           // K tiles accumulated in TMEM before draining to fp32 registers
+constexpr int kDrainDelay = 2;      // drain a chunk after converting this many stages of the next
+
+struct StageView {
+    uint8_t* w_hi;
+    uint8_t* w_lo;
+    uint8_t* x_hi;
+    uint8_t* x_lo;
+};
+__device__ __forceinline__ StageView stage(uint8_t* base, int s) {
+    uint8_t* p = base + static_cast<size_t>(s) * kStageBytes;
+    return {p, p + kWBytes, p + 2 * kWBytes, p + 2 * kWBytes + kXBytes};
+}
+
+__device__ __forceinline__ const char* translate(const char* arena, const uint32_t* pt, uint64_t v) {
+    return arena + (static_cast<uint64_t>(pt[v >> kPageShift]) << kPageShift) + (v & kPageMask);
+}
+
+// v = hi + lo, hi = v rounded to the nearest TF32 value (exact in TF32),
+// lo = v - hi exact in fp32, |lo| <= 2^-11 |v|.
+__device__ __forceinline__ void split_tf32(float4& v, float4& lo) {
+    float* a = reinterpret_cast<float*>(&v);
+    float* b = reinterpret_cast<float*>(&lo);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const float hi = __uint_as_float((__float_as_uint(a[i]) + 0x1000u) & 0xFFFFE000u);
+        b[i] = a[i] - hi;
+        a[i] = hi;
+    }
+}
+
+__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
+
+__global__ void __launch_bounds__(kThreads, 1)
+    mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ MlpLayerArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
+    __shared__ __align__(8) uint64_t full_bar[kStages], conv_bar[kStages], empty_bar[kStages];
+    __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
+    __shared__ uint32_t tmem_base_s;
+    __shared__ uint32_t pt[GFX_MAX_PAGES];
+    __shared__ int last_flag;
+    __shared__ float red_m[4][kRows], red_s[4][kRows];
+    __shared__ float rowstat[kRows][2];
+
+    const int tid = threadIdx.x;
+    const int warp = tid >> 5;
+    const int lane = tid & 31;
+    const int tile = blockIdx.x;
+    const int split = blockIdx.y;
+    const int K = a.K;
+    const int N = a.N;
+    const int kt_total = K / kTileK;
+    const int kt_begin = static_cast<int>((static_cast<long long>(kt_total) * split) / a.splits);
+    const int kt_end = static_cast<int>((static_cast<long long>(kt_total) * (split + 1)) / a.splits);
+    const int nkt = kt_end - kt_begin;
+
+    for (int i = tid; i < static_cast<int>(a.pt.n); i += kThreads) pt[i] = a.pt.page[i];
+    if (tid == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&conv_bar[s], 128);
+            mbar_init(&empty_bar[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull_bar[b], 1);
+            mbar_init(&tempty_bar[b], 128);
+        }
+        mbar_fence_init();
+        tma_prefetch_desc(&tmap_x);
+    }
+    if (warp == 1) tmem_alloc<kTmemCols>(&tmem_base_s);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_base_s;
+
+    if (warp == 0) {
+        // ---------------- TMA producer ----------------
+        if (lane == 0) {
+            for (int it = 0; it < nkt; ++it) {
+                const int s = it % kStages;
+                if (it >= kStages) mbar_wait(&empty_bar[s], ((it / kStages) & 1) ^ 1);
+                const StageView st = stage(smem, s);
+                const int kt = kt_begin + it;
+                mbar_arrive_expect_tx(&full_bar[s], kWBytes + kXBytes);
+                const uint64_t v = a.w_off + (static_cast<uint64_t>(tile) * kt_total + kt) * kWBytes;
+                tma_bulk_g2s(st.w_hi, translate(a.arena, pt, v), kWBytes, &full_bar[s]);
+                tma_tile2d_g2s(st.x_hi, &tmap_x, kt * kTileK, 0, &full_bar[s]);
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer ----------------
+        if (lane == 0) {
+            constexpr uint32_t idesc = umma_idesc<kTileM, kRows, 2>();  // TF32 x TF32 -> F32
+            for (int it = 0; it < nkt; ++it) {
+                const int s = it % kStages;
+                const int chunk = it / kChunk;
+                const uint32_t acc_tmem = tmem + static_cast<uint32_t>((chunk & 1) * 32);
+                // Chunk c reuses accumulator buffer c&1: wait until chunk c-2 was drained.
+                if (it % kChunk == 0 && chunk >= 2) mbar_wait(&tempty_bar[chunk & 1], ((chunk >> 1) & 1) ^ 1);
+                mbar_wait(&conv_bar[s], (it / kStages) & 1);
+                tc_fence_after();
+                const StageView st = stage(smem, s);
+#pragma unroll
+                for (int kk = 0; kk < kTileK / 8; ++kk) {
+                    const uint32_t off = kk * 32;  // 8 fp32 = 32 bytes of the swizzled row
+                    const uint64_t ah = umma_desc_sw128(st.w_hi, off), al = umma_desc_sw128(st.w_lo, off);
+                    const uint64_t bh = umma_desc_sw128(st.x_hi, off), bl = umma_desc_sw128(st.x_lo, off);
+                    umma_tf32(acc_tmem, al, bh, idesc, ((it % kChunk) | kk) ? 1u : 0u);  // small terms first
+                    umma_tf32(acc_tmem, ah, bl, idesc, 1u);
+                    umma_tf32(acc_tmem, ah, bh, idesc, 1u);
+                }
+                umma_commit(&empty_bar[s]);  // stage smem free once these MMAs retire
+                if (it % kChunk == kChunk - 1 || it == nkt - 1) umma_commit(&tfull_bar[chunk & 1]);
+            }
+        }
+    } else {
+        // ---------------- hi/lo split, then epilogue ----------------
+        const int ct = tid - 64;  // 0..127
+        const int q = warp & 3;   // this warp's TMEM lane quarter
+        const int f = tile * kTileM + q * 32 + lane;
+        const int nchunks = (nkt + kChunk - 1) / kChunk;
+        // Accumulator: TMEM lane = feature row of the tile, column = batch row.
+        // Each chunk of kChunk K tiles is accumulated by the tensor core, then
+        // drained and summed here in fp32 (round-to-nearest) while the next
+        // chunk accumulates in the other buffer — short tensor-core
+        // accumulation chains keep the fp32 tolerance at any K.
+        float acc[kRows];
+#pragma unroll
+        for (int b = 0; b < kRows; ++b) acc[b] = 0.f;
+        int drained = 0;
+        auto drain = [&](int c) {
+            mbar_wait(&tfull_bar[c & 1], (c >> 1) & 1);
+            tc_fence_after();
+            float part[kRows];
+            tmem_ld_32x32b_x32(tmem + static_cast<uint32_t>((c & 1) * 32) + (static_cast<uint32_t>(q * 32) << 16), part);
+#pragma unroll
+            for (int b = 0; b < kRows; ++b) acc[b] += part[b];
+            tc_fence_before();
+            mbar_arrive(&tempty_bar[c & 1]);
+        };
+        for (int it = 0; it < nkt; ++it) {
+            const int s = it % kStages;
+            mbar_wait(&full_bar[s], (it / kStages) & 1);
+            const StageView st = stage(smem, s);
+            float4* wh = reinterpret_cast<float4*>(st.w_hi);
+            float4* wl = reinterpret_cast<float4*>(st.w_lo);
+#pragma unroll
+            for (int j = 0; j < static_cast<int>(kWBytes / 16 / 128); ++j) {
+                float4 v = wh[ct + 128 * j], lo;
+                split_tf32(v, lo);
+                wh[ct + 128 * j] = v;
+                wl[ct + 128 * j] = lo;
+            }
+            float4* xh = reinterpret_cast<float4*>(st.x_hi);
+            float4* xl = reinterpret_cast<float4*>(st.x_lo);
+#pragma unroll
+            for (int j = 0; j < static_cast<int>(kXBytes / 16 / 128); ++j) {
+                float4 v = xh[ct + 128 * j], lo;
+                split_tf32(v, lo);
+                xh[ct + 128 * j] = v;
+                xl[ct + 128 * j] = lo;
+            }
+            fence_proxy_async_smem();
+            mbar_arrive(&conv_bar[s]);
+            while (drained < nchunks && min(nkt, (drained + 1) * kChunk) - 1 + kDrainDelay <= it) drain(drained++);
+        }
+        while (drained < nchunks) drain(drained++);
+
+        bool finisher = true;
+        if (a.splits > 1) {
+            float* ws = a.ws + static_cast<size_t>(split) * kRows * a.ldws;
+#pragma unroll
+            for (int b = 0; b < kRows; ++b) ws[static_cast<size_t>(b) * a.ldws + f] = acc[b];
+            __threadfence();
+            epi_sync();
+            if (ct == 0) last_flag = atomicAdd(&a.counters[tile], 1u) == static_cast<unsigned>(a.splits - 1);
+            epi_sync();
+            finisher = last_flag;
+            if (finisher) {
+                __threadfence();
+#pragma unroll
+                for (int b = 0; b < kRows; ++b) acc[b] = 0.f;
+                for (int sp = 0; sp < a.splits; ++sp) {  // fixed order: deterministic
+                    const float* w = a.ws + static_cast<size_t>(sp) * kRows * a.ldws;
+#pragma unroll
+                    for (int b = 0; b < kRows; ++b) acc[b] += __ldcg(&w[static_cast<size_t>(b) * a.ldws + f]);
+                }
+                if (ct == 0) a.counters[tile] = 0;
+            }
+        }
+        if (finisher) {
+            const bool valid = f < N;
+            const float bias = valid ? *reinterpret_cast<const float*>(translate(a.arena, pt, a.b_off + 4ull * f)) : 0.f;
+#pragma unroll
+            for (int b = 0; b < kRows; ++b) {
+                float v = acc[b] + bias;
+                if (a.relu) v = fmaxf(v, 0.f);
+                acc[b] = v;
+                if (valid) a.y[static_cast<size_t>(b) * N + f] = v;
+            }
+            if (a.probs != nullptr) {
+                // Softmax level 1: per-row (max, sum exp) over this tile's 128 features.
+#pragma unroll
+                for (int b = 0; b < kRows; ++b) {
+                    float m = valid ? acc[b] : -INFINITY;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+                    if (lane == 0) red_m[q][b] = m;
+                }
+                epi_sync();
+#pragma unroll
+                for (int b = 0; b < kRows; ++b) {
+                    const float m = fmaxf(fmaxf(red_m[0][b], red_m[1][b]), fmaxf(red_m[2][b], red_m[3][b]));
+                    float e = valid ? expf(acc[b] - m) : 0.f;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+                    if (lane == 0) red_s[q][b] = e;
+                }
+                epi_sync();
+                if (ct < kRows) {
+                    const int b = ct;
+                    const float m = fmaxf(fmaxf(red_m[0][b], red_m[1][b]), fmaxf(red_m[2][b], red_m[3][b]));
+                    const float e = (red_s[0][b] + red_s[1][b]) + (red_s[2][b] + red_s[3][b]);
+                    float* st = a.stats + (static_cast<size_t>(tile) * kRows + b) * 2;
+                    st[0] = m;
+                    st[1] = e;
+                }
+                __threadfence();
+                epi_sync();
+                if (ct == 0) last_flag = atomicAdd(&a.counters[a.ntiles], 1u) == static_cast<unsigned>(a.ntiles - 1);
+                epi_sync();
+                if (last_flag) {
+                    // Softmax level 2 (last tile): combine tiles in order, write every probability.
+                    __threadfence();
+                    if (ct < kRows) {
+                        float m = -INFINITY;
+                        for (int t = 0; t < a.ntiles; ++t)
+                            m = fmaxf(m, __ldcg(a.stats + (static_cast<size_t>(t) * kRows + ct) * 2));
+                        float ssum = 0.f;
+                        for (int t = 0; t < a.ntiles; ++t) {
+                            const float* st = a.stats + (static_cast<size_t>(t) * kRows + ct) * 2;
+                            ssum += __ldcg(st + 1) * expf(__ldcg(st) - m);
+                        }
+                        rowstat[ct][0] = m;
+                        rowstat[ct][1] = 1.0f / ssum;
+                    }
+                    epi_sync();
+                    const int total = kRows * N;
+                    for (int i = ct; i < total; i += 4 * 128) {
+                        float v[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int j = i + u * 128;
+                            v[u] = j < total ? __ldcg(a.y + j) : 0.f;
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int j = i + u * 128;
+                            if (j < total) {
+                                const int row = j / N;
+                                a.probs[j] = expf(v[u] - rowstat[row][0]) * rowstat[row][1];
+                            }
+                        }
+                    }
+                    if (ct == 0) a.counters[a.ntiles] = 0;
+                }
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 1) tmem_dealloc<kTmemCols>(tmem);
+}
+
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        GFX_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (q != cudaDriverEntryPointSuccess || p == nullptr)
+            throw CudaError("cuTensorMapEncodeTiled entry point unavailable");
+        fn = reinterpret_cast<EncodeTiledFn>(p);
+    });
+    return fn;
+}
+
+}  // namespace
+
+bool encode_tensor_map_2d(CUtensorMap* map, CUtensorMapDataType dtype, uint32_t elem_bytes, const void* base,
+                          uint64_t inner, uint64_t outer, uint64_t row_stride_bytes, uint32_t box_inner,
+                          uint32_t box_outer, CUtensorMapSwizzle swizzle) {
+    (void)elem_bytes;
+    const cuuint64_t dims[2] = {inner, outer};
+    const cuuint64_t strides[1] = {row_stride_bytes};
+    const cuuint32_t box[2] = {box_inner, box_outer};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = encode_fn()(map, dtype, 2, const_cast<void*>(base), dims, strides, box, estr,
+                                   CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+int mlp_layer_splits(int K, int N, int sm_count) {
+    const int tiles = mlp_layer_tiles(N);
+    const int kt = K / kTileK;
+    int s = sm_count / tiles;  // one wave, one CTA per SM
+    if (s > kt) s = kt;
+    if (s > kMaxSplits) s = kMaxSplits;
+    return s < 1 ? 1 : s;
+}
+
+int mlp_layer_tiles(int N) { return (N + kTileM - 1) / kTileM; }
+
+size_t mlp_layer_smem() { return static_cast<size_t>(kStageBytes) * kStages + 1024; }
+
+void launch_mlp_layer(const MlpLayerArgs& a, cudaStream_t stream) {
+    if (a.K % kTileK != 0) throw std::runtime_error("mlp layer: K must be a multiple of 32");
+    CUtensorMap tmx;
+    if (!encode_tensor_map_2d(&tmx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, a.x, static_cast<uint64_t>(a.K), kRows,
+                              static_cast<uint64_t>(a.K) * 4, kTileK, kRows, CU_TENSOR_MAP_SWIZZLE_128B))
+        throw CudaError("cuTensorMapEncodeTiled failed for the activation tile map");
+    static bool attr = false;
+    const size_t smem = mlp_layer_smem();
+    if (!attr) {
+        GFX_CUDA(cudaFuncSetAttribute(mlp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+        attr = true;
+    }
+    dim3 grid(static_cast<unsigned>(a.ntiles), static_cast<unsigned>(a.splits));
+    mlp_tc_kernel<<<grid, kThreads, smem, stream>>>(tmx, a);
+    GFX_CUDA(cudaGetLastError());
+}
+
+// Request inputs / test tensors straight from the parameter stream; one
+// launch fills `count` consecutive tensors with seeds seed0, seed0+1, ...
+__global__ void fill_params_kernel(float* dst, uint64_t n, uint64_t count, uint64_t seed0, uint32_t tensor,
+                                   float scaled) {
+    const uint64_t total = n * count;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t t = i / n;
+        dst[i] = param_at(param_stream(seed0 + t, tensor), i - t * n, scaled);
+    }
+}
+
+void launch_fill_params(float* dst, uint64_t n, uint64_t seed, uint32_t tensor, float scale, cudaStream_t s,
+                        uint64_t count) {
+    const uint64_t total = n * count;
+    unsigned blocks = static_cast<unsigned>((total + 255) / 256);
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    if (blocks == 0) blocks = 1;
+    fill_params_kernel<<<blocks, 256, 0, s>>>(dst, n, count, seed, tensor, param_scale(scale));
+    GFX_CUDA(cudaGetLastError());
+}
+
+}  // namespace gfx

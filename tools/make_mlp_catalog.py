@@ -21,12 +21,14 @@ PAGE = 2 << 20
 
 
 def mlp_bytes(dims):
+    """Mirrors mlp_layout in csrc/device/manager.cu: per layer 16 KB-aligned
+    weight tiles (rows padded to 128) then the 256 B-aligned bias."""
+    align = lambda v, a: (v + a - 1) // a * a  # noqa: E731
     off = 0
-    align = lambda v: (v + 255) & ~255  # noqa: E731  (mirrors mlp_layout in manager.cu)
     for k, n in zip(dims[:-1], dims[1:]):
-        off = align(off + 4 * k * n)
-        off = align(off + 4 * n)
-    return off
+        off = align(off, 16384) + 4 * k * align(n, 128)
+        off = align(off, 256) + 4 * n
+    return align(off, 256)
 
 
 def mlp_flops(dims, batch=32):
