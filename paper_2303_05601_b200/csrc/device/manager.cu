@@ -314,7 +314,7 @@ void GpuManager::infer(int model, const float* in, float* out) {
         a.x = x;
         const bool last = l + 1 == L;
         a.y = last ? out : act_[l & 1];
-        a.probs = last ? out + static_cast<size_t>(kBatch) * C : nullptr;
+        a.probs = nullptr;  // softmax runs as its own row-parallel kernel
         a.relu = last ? 0 : 1;
         a.w_off = blob.w_off[l];
         a.b_off = blob.b_off[l];
@@ -326,6 +326,8 @@ void GpuManager::infer(int model, const float* in, float* out) {
         ++kernel_launches;
         x = a.y;
     }
+    launch_softmax_rows(out, out + static_cast<size_t>(kBatch) * C, kBatch, C, compute_);
+    ++kernel_launches;
     GFX_CUDA(cudaEventRecord(s.last_use, compute_));
 }
 

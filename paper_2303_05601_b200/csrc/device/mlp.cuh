@@ -31,6 +31,7 @@ int mlp_layer_splits(int K, int N, int sm_count);
 int mlp_layer_tiles(int N);
 size_t mlp_layer_smem();
 void launch_mlp_layer(const MlpLayerArgs& a, cudaStream_t stream);
+void launch_softmax_rows(const float* logits, float* probs, int rows, int C, cudaStream_t s);
 // Fills `count` consecutive tensors of n values, tensor t from seed + t.
 void launch_fill_params(float* dst, uint64_t n, uint64_t seed, uint32_t tensor, float scale, cudaStream_t s,
                         uint64_t count = 1);

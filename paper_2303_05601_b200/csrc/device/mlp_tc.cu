@@ -18,13 +18,15 @@
 // streaming fp32 weights from HBM.
 //
 // Structure, one CTA per (128-feature tile, K split), 1 CTA per SM:
-//   warp 0      TMA producer: per 32-wide K step one 1-D bulk copy of the
-//               16 KB pre-swizzled weight tile (the model blob stores W as
-//               SWIZZLE_128B K-major 128x32 tiles, so a tile never straddles
-//               a 2 MiB arena page) + one 2-D tensor copy of the 32x32 X tile;
-//   warps 2-5   split each landed stage into hi/lo planes in place
-//               (elementwise, so the swizzled layout is preserved), then
-//               fence.proxy.async and arrive;
+//   warp 0      TMA producer into a 6-deep landing ring (120 KB in flight per
+//               SM covers HBM latency): per 32-wide K step one 1-D bulk copy
+//               of the 16 KB pre-swizzled weight tile (the model blob stores W
+//               as SWIZZLE_128B K-major 128x32 tiles, so a tile never
+//               straddles a 2 MiB arena page) + one 2-D tensor-map copy of the
+//               32x32 activation tile;
+//   warps 2-5   split each landed tile into hi/lo planes of a 2-deep operand
+//               ring (elementwise, so the swizzled layout is preserved),
+//               release the landing slot, fence.proxy.async and arrive;
 //   warp 1      one elected thread issues 12 tcgen05.mma (4 K slices x 3
 //               products) per stage into a 128x32 fp32 TMEM accumulator and
 //               commits the stage back to the producer; accumulators are
@@ -34,7 +36,7 @@
 //               the epilogue: split-K
 //               partials through a global workspace reduced by the last CTA of
 //               the feature tile in fixed split order (deterministic), bias +
-//               ReLU, and on the last layer a two-level softmax.
+//               ReLU. The classifier softmax is a separate row-parallel kernel.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -55,23 +57,33 @@ using namespace gfx::sm100;
 constexpr int kRows = 32;        // batch rows per request = MMA N
 constexpr int kTileM = 128;      // output features per CTA = MMA M
 constexpr int kTileK = 32;       // fp32 K per stage (= one 128-byte swizzle row)
-constexpr int kStages = 4;
+constexpr int kLand = 6;         // TMA landing ring: raw fp32 tiles in flight from HBM
+constexpr int kOps = 2;          // converted (hi/lo) operand ring read by the tensor core
 constexpr int kThreads = 192;    // 6 warps
 constexpr uint32_t kWBytes = kTileM * kTileK * 4;  // 16 KB
 constexpr uint32_t kXBytes = kRows * kTileK * 4;   // 4 KB
-constexpr uint32_t kStageBytes = 2 * kWBytes + 2 * kXBytes;
+constexpr uint32_t kLandBytes = kWBytes + kXBytes;           // 20 KB, 1024-aligned
+constexpr uint32_t kOpBytes = 2 * kWBytes + 2 * kXBytes;     // 40 KB
 constexpr uint32_t kTmemCols = 64;  // two 32-column accumulators (double-buffered chunks)
 constexpr int kChunk = 4;           // K tiles accumulated in TMEM before draining to fp32 registers
 constexpr int kDrainDelay = 2;      // drain a chunk after converting this many stages of the next
 
-struct StageView {
+struct Landing {
+    uint8_t* w;
+    uint8_t* x;
+};
+__device__ __forceinline__ Landing landing(uint8_t* base, int s) {
+    uint8_t* p = base + static_cast<size_t>(s) * kLandBytes;
+    return {p, p + kWBytes};
+}
+struct Operands {
     uint8_t* w_hi;
     uint8_t* w_lo;
     uint8_t* x_hi;
     uint8_t* x_lo;
 };
-__device__ __forceinline__ StageView stage(uint8_t* base, int s) {
-    uint8_t* p = base + static_cast<size_t>(s) * kStageBytes;
+__device__ __forceinline__ Operands operands(uint8_t* base, int s) {
+    uint8_t* p = base + static_cast<size_t>(kLand) * kLandBytes + static_cast<size_t>(s) * kOpBytes;
     return {p, p + kWBytes, p + 2 * kWBytes, p + 2 * kWBytes + kXBytes};
 }
 
@@ -81,14 +93,14 @@ __device__ __forceinline__ const char* translate(const char* arena, const uint32
 
 // v = hi + lo, hi = v rounded to the nearest TF32 value (exact in TF32),
 // lo = v - hi exact in fp32, |lo| <= 2^-11 |v|.
-__device__ __forceinline__ void split_tf32(float4& v, float4& lo) {
-    float* a = reinterpret_cast<float*>(&v);
+__device__ __forceinline__ void split_tf32(const float4& v, float4& hi, float4& lo) {
+    const float* a = reinterpret_cast<const float*>(&v);
+    float* h = reinterpret_cast<float*>(&hi);
     float* b = reinterpret_cast<float*>(&lo);
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-        const float hi = __uint_as_float((__float_as_uint(a[i]) + 0x1000u) & 0xFFFFE000u);
-        b[i] = a[i] - hi;
-        a[i] = hi;
+        h[i] = __uint_as_float((__float_as_uint(a[i]) + 0x1000u) & 0xFFFFE000u);
+        b[i] = a[i] - h[i];
     }
 }
 
@@ -98,7 +110,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ MlpLayerArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
-    __shared__ __align__(8) uint64_t full_bar[kStages], conv_bar[kStages], empty_bar[kStages];
+    __shared__ __align__(8) uint64_t land_full[kLand], land_empty[kLand], op_full[kOps], op_empty[kOps];
     __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
     __shared__ uint32_t tmem_base_s;
     __shared__ uint32_t pt[GFX_MAX_PAGES];
@@ -120,10 +132,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     for (int i = tid; i < static_cast<int>(a.pt.n); i += kThreads) pt[i] = a.pt.page[i];
     if (tid == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full_bar[s], 1);
-            mbar_init(&conv_bar[s], 128);
-            mbar_init(&empty_bar[s], 1);
+        for (int s = 0; s < kLand; ++s) {
+            mbar_init(&land_full[s], 1);
+            mbar_init(&land_empty[s], 128);
+        }
+        for (int s = 0; s < kOps; ++s) {
+            mbar_init(&op_full[s], 128);
+            mbar_init(&op_empty[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull_bar[b], 1);
@@ -142,14 +157,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         // ---------------- TMA producer ----------------
         if (lane == 0) {
             for (int it = 0; it < nkt; ++it) {
-                const int s = it % kStages;
-                if (it >= kStages) mbar_wait(&empty_bar[s], ((it / kStages) & 1) ^ 1);
-                const StageView st = stage(smem, s);
+                const int s = it % kLand;
+                if (it >= kLand) mbar_wait(&land_empty[s], ((it / kLand) & 1) ^ 1);
+                const Landing ld = landing(smem, s);
                 const int kt = kt_begin + it;
-                mbar_arrive_expect_tx(&full_bar[s], kWBytes + kXBytes);
+                mbar_arrive_expect_tx(&land_full[s], kLandBytes);
                 const uint64_t v = a.w_off + (static_cast<uint64_t>(tile) * kt_total + kt) * kWBytes;
-                tma_bulk_g2s(st.w_hi, translate(a.arena, pt, v), kWBytes, &full_bar[s]);
-                tma_tile2d_g2s(st.x_hi, &tmap_x, kt * kTileK, 0, &full_bar[s]);
+                tma_bulk_g2s(ld.w, translate(a.arena, pt, v), kWBytes, &land_full[s]);
+                tma_tile2d_g2s(ld.x, &tmap_x, kt * kTileK, 0, &land_full[s]);
             }
         }
     } else if (warp == 1) {
@@ -157,14 +172,14 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) {
             constexpr uint32_t idesc = umma_idesc<kTileM, kRows, 2>();  // TF32 x TF32 -> F32
             for (int it = 0; it < nkt; ++it) {
-                const int s = it % kStages;
+                const int s = it % kOps;
                 const int chunk = it / kChunk;
                 const uint32_t acc_tmem = tmem + static_cast<uint32_t>((chunk & 1) * 32);
                 // Chunk c reuses accumulator buffer c&1: wait until chunk c-2 was drained.
                 if (it % kChunk == 0 && chunk >= 2) mbar_wait(&tempty_bar[chunk & 1], ((chunk >> 1) & 1) ^ 1);
-                mbar_wait(&conv_bar[s], (it / kStages) & 1);
+                mbar_wait(&op_full[s], (it / kOps) & 1);
                 tc_fence_after();
-                const StageView st = stage(smem, s);
+                const Operands st = operands(smem, s);
 #pragma unroll
                 for (int kk = 0; kk < kTileK / 8; ++kk) {
                     const uint32_t off = kk * 32;  // 8 fp32 = 32 bytes of the swizzled row
@@ -174,7 +189,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     umma_tf32(acc_tmem, ah, bl, idesc, 1u);
                     umma_tf32(acc_tmem, ah, bh, idesc, 1u);
                 }
-                umma_commit(&empty_bar[s]);  // stage smem free once these MMAs retire
+                umma_commit(&op_empty[s]);  // operand buffer free once these MMAs retire
                 if (it % kChunk == kChunk - 1 || it == nkt - 1) umma_commit(&tfull_bar[chunk & 1]);
             }
         }
@@ -204,29 +219,36 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_arrive(&tempty_bar[c & 1]);
         };
         for (int it = 0; it < nkt; ++it) {
-            const int s = it % kStages;
-            mbar_wait(&full_bar[s], (it / kStages) & 1);
-            const StageView st = stage(smem, s);
-            float4* wh = reinterpret_cast<float4*>(st.w_hi);
-            float4* wl = reinterpret_cast<float4*>(st.w_lo);
+            const int s = it % kLand;
+            const int o = it % kOps;
+            mbar_wait(&land_full[s], (it / kLand) & 1);
+            if (it >= kOps) mbar_wait(&op_empty[o], ((it / kOps) & 1) ^ 1);
+            const Landing ld = landing(smem, s);
+            const Operands op = operands(smem, o);
+            const float4* w = reinterpret_cast<const float4*>(ld.w);
+            const float4* x = reinterpret_cast<const float4*>(ld.x);
+            float4 wv[kWBytes / 16 / 128], xv[kXBytes / 16 / 128];
+#pragma unroll
+            for (int j = 0; j < static_cast<int>(kWBytes / 16 / 128); ++j) wv[j] = w[ct + 128 * j];
+#pragma unroll
+            for (int j = 0; j < static_cast<int>(kXBytes / 16 / 128); ++j) xv[j] = x[ct + 128 * j];
+            mbar_arrive(&land_empty[s]);  // landing slot back to the TMA producer
 #pragma unroll
             for (int j = 0; j < static_cast<int>(kWBytes / 16 / 128); ++j) {
-                float4 v = wh[ct + 128 * j], lo;
-                split_tf32(v, lo);
-                wh[ct + 128 * j] = v;
-                wl[ct + 128 * j] = lo;
+                float4 hi, lo;
+                split_tf32(wv[j], hi, lo);
+                reinterpret_cast<float4*>(op.w_hi)[ct + 128 * j] = hi;
+                reinterpret_cast<float4*>(op.w_lo)[ct + 128 * j] = lo;
             }
-            float4* xh = reinterpret_cast<float4*>(st.x_hi);
-            float4* xl = reinterpret_cast<float4*>(st.x_lo);
 #pragma unroll
             for (int j = 0; j < static_cast<int>(kXBytes / 16 / 128); ++j) {
-                float4 v = xh[ct + 128 * j], lo;
-                split_tf32(v, lo);
-                xh[ct + 128 * j] = v;
-                xl[ct + 128 * j] = lo;
+                float4 hi, lo;
+                split_tf32(xv[j], hi, lo);
+                reinterpret_cast<float4*>(op.x_hi)[ct + 128 * j] = hi;
+                reinterpret_cast<float4*>(op.x_lo)[ct + 128 * j] = lo;
             }
             fence_proxy_async_smem();
-            mbar_arrive(&conv_bar[s]);
+            mbar_arrive(&op_full[o]);
             while (drained < nchunks && min(nkt, (drained + 1) * kChunk) - 1 + kDrainDelay <= it) drain(drained++);
         }
         while (drained < nchunks) drain(drained++);
@@ -262,73 +284,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (a.relu) v = fmaxf(v, 0.f);
                 acc[b] = v;
                 if (valid) a.y[static_cast<size_t>(b) * N + f] = v;
-            }
-            if (a.probs != nullptr) {
-                // Softmax level 1: per-row (max, sum exp) over this tile's 128 features.
-#pragma unroll
-                for (int b = 0; b < kRows; ++b) {
-                    float m = valid ? acc[b] : -INFINITY;
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-                    if (lane == 0) red_m[q][b] = m;
-                }
-                epi_sync();
-#pragma unroll
-                for (int b = 0; b < kRows; ++b) {
-                    const float m = fmaxf(fmaxf(red_m[0][b], red_m[1][b]), fmaxf(red_m[2][b], red_m[3][b]));
-                    float e = valid ? expf(acc[b] - m) : 0.f;
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-                    if (lane == 0) red_s[q][b] = e;
-                }
-                epi_sync();
-                if (ct < kRows) {
-                    const int b = ct;
-                    const float m = fmaxf(fmaxf(red_m[0][b], red_m[1][b]), fmaxf(red_m[2][b], red_m[3][b]));
-                    const float e = (red_s[0][b] + red_s[1][b]) + (red_s[2][b] + red_s[3][b]);
-                    float* st = a.stats + (static_cast<size_t>(tile) * kRows + b) * 2;
-                    st[0] = m;
-                    st[1] = e;
-                }
-                __threadfence();
-                epi_sync();
-                if (ct == 0) last_flag = atomicAdd(&a.counters[a.ntiles], 1u) == static_cast<unsigned>(a.ntiles - 1);
-                epi_sync();
-                if (last_flag) {
-                    // Softmax level 2 (last tile): combine tiles in order, write every probability.
-                    __threadfence();
-                    if (ct < kRows) {
-                        float m = -INFINITY;
-                        for (int t = 0; t < a.ntiles; ++t)
-                            m = fmaxf(m, __ldcg(a.stats + (static_cast<size_t>(t) * kRows + ct) * 2));
-                        float ssum = 0.f;
-                        for (int t = 0; t < a.ntiles; ++t) {
-                            const float* st = a.stats + (static_cast<size_t>(t) * kRows + ct) * 2;
-                            ssum += __ldcg(st + 1) * expf(__ldcg(st) - m);
-                        }
-                        rowstat[ct][0] = m;
-                        rowstat[ct][1] = 1.0f / ssum;
-                    }
-                    epi_sync();
-                    const int total = kRows * N;
-                    for (int i = ct; i < total; i += 4 * 128) {
-                        float v[4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const int j = i + u * 128;
-                            v[u] = j < total ? __ldcg(a.y + j) : 0.f;
-                        }
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const int j = i + u * 128;
-                            if (j < total) {
-                                const int row = j / N;
-                                a.probs[j] = expf(v[u] - rowstat[row][0]) * rowstat[row][1];
-                            }
-                        }
-                    }
-                    if (ct == 0) a.counters[a.ntiles] = 0;
-                }
             }
         }
     }
@@ -384,7 +339,7 @@ int mlp_layer_splits(int K, int N, int sm_count) {
 
 int mlp_layer_tiles(int N) { return (N + kTileM - 1) / kTileM; }
 
-size_t mlp_layer_smem() { return static_cast<size_t>(kStageBytes) * kStages + 1024; }
+size_t mlp_layer_smem() { return static_cast<size_t>(kLandBytes) * kLand + static_cast<size_t>(kOpBytes) * kOps + 1024; }
 
 void launch_mlp_layer(const MlpLayerArgs& a, cudaStream_t stream) {
     if (a.K % kTileK != 0) throw std::runtime_error("mlp layer: K must be a multiple of 32");
@@ -401,6 +356,60 @@ void launch_mlp_layer(const MlpLayerArgs& a, cudaStream_t stream) {
     }
     dim3 grid(static_cast<unsigned>(a.ntiles), static_cast<unsigned>(a.splits));
     mlp_tc_kernel<<<grid, kThreads, smem, stream>>>(tmx, a);
+    GFX_CUDA(cudaGetLastError());
+}
+
+// Row softmax of the classifier logits: one CTA per batch row, 256 threads,
+// block-wide max / sum through warp shuffles (K4, HBM/L2-latency bound).
+__global__ void __launch_bounds__(256) softmax_rows_kernel(const float* __restrict__ logits,
+                                                           float* __restrict__ probs, int C) {
+    __shared__ float red[8];
+    const int row = blockIdx.x;
+    const float* in = logits + static_cast<size_t>(row) * C;
+    float* out = probs + static_cast<size_t>(row) * C;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr int kPer = 8;  // C <= 2048
+    float v[kPer];
+    float m = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+        const int c = threadIdx.x + i * 256;
+        v[i] = c < C ? in[c] : -INFINITY;
+        m = fmaxf(m, v[i]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) red[warp] = m;
+    __syncthreads();
+    m = red[0];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) m = fmaxf(m, red[w]);
+    __syncthreads();
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+        const int c = threadIdx.x + i * 256;
+        v[i] = c < C ? expf(v[i] - m) : 0.f;
+        s += v[i];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) red[warp] = s;
+    __syncthreads();
+    float tot = 0.f;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) tot += red[w];
+    const float inv = 1.0f / tot;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+        const int c = threadIdx.x + i * 256;
+        if (c < C) out[c] = v[i] * inv;
+    }
+}
+
+void launch_softmax_rows(const float* logits, float* probs, int rows, int C, cudaStream_t s) {
+    if (C > 2048) throw std::runtime_error("softmax: at most 2048 classes");
+    softmax_rows_kernel<<<rows, 256, 0, s>>>(logits, probs, C);
     GFX_CUDA(cudaGetLastError());
 }
 

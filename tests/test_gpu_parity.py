@@ -123,10 +123,11 @@ def test_every_model_shape(gfx, olib):
 
 def test_cache_ops_errors_and_page_accounting(gfx):
     a = C.c_void_p()
-    gfx.check(gfx._ffi.gfx_arena_create(0, 100 << 20, C.byref(a)))  # 50 pages
+    pages21 = gfx.load_model_specs("mlp_c2")[21].pages  # vgg19, the largest model
+    gfx.check(gfx._ffi.gfx_arena_create(0, pages21 << 21, C.byref(a)))  # exactly its pages
     try:
         free = C.c_int32()
-        gfx.check(gfx._ffi.gfx_load_h2d(a, 21, None))  # vgg19: 50 pages
+        gfx.check(gfx._ffi.gfx_load_h2d(a, 21, None))
         gfx.check(gfx._ffi.gfx_arena_free_pages(a, C.byref(free)))
         assert free.value == 0
         rc = gfx._ffi.gfx_load_h2d(a, 0, None)  # no room: the control plane would have evicted
@@ -135,7 +136,7 @@ def test_cache_ops_errors_and_page_accounting(gfx):
         assert gfx._ffi.gfx_evict(a, 3) == 2
         gfx.check(gfx._ffi.gfx_evict(a, 21))
         gfx.check(gfx._ffi.gfx_arena_free_pages(a, C.byref(free)))
-        assert free.value == 50
+        assert free.value == pages21
         ev = C.c_void_p()
         gfx.check(gfx._ffi.gfx_load_h2d(a, 0, C.byref(ev)))
         gfx.check(gfx._ffi.gfx_event_sync(ev))

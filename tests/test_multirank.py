@@ -1,0 +1,70 @@
+"""Multi-GPU host logic on CPU (gloo, world_size 2): one process per GPU, each
+running the same deterministic control plane (bench.py --gpus N) and executing
+only its own GPU's decisions. Checks that every rank derives the identical
+decision stream and that the per-rank shards partition the requests exactly —
+no request lost, none executed twice, no collective on the data path."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import simabi
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, cat, q):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        lib = simabi.load_product()
+        cfg = simabi.make_config(gpus=world, capacity_mb=204.0, policy="lalbo3", rpm=325 * world, minutes=3)
+        res = lib.run(cat, cfg)
+        mine = res.ints[:, 2] == rank
+        dispatched = res.ints[mine & (res.ints[:, 0] != 2), 1]
+        # All ranks must agree on the schedule bit for bit.
+        dg = torch.tensor([res.decision_digest & 0x7FFFFFFFFFFFFFFF], dtype=torch.int64)
+        all_dg = [torch.zeros_like(dg) for _ in range(world)]
+        dist.all_gather(all_dg, dg)
+        # Shards: request ids dispatched on this rank's GPU.
+        n = torch.tensor([len(dispatched)], dtype=torch.int64)
+        sizes = [torch.zeros_like(n) for _ in range(world)]
+        dist.all_gather(sizes, n)
+        buf = torch.full((int(max(s.item() for s in sizes)),), -1, dtype=torch.int64)
+        buf[: len(dispatched)] = torch.from_numpy(dispatched.astype(np.int64))
+        shards = [torch.zeros_like(buf) for _ in range(world)]
+        dist.all_gather(shards, buf)
+        if rank == 0:
+            ids = np.concatenate([s.numpy()[s.numpy() >= 0] for s in shards])
+            q.put((sorted({int(d.item()) for d in all_dg}), ids.tolist(), len(res.arrival),
+                   [int(s.item()) for s in sizes]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2])
+def test_ranks_share_one_schedule_and_partition_requests(mlp_catalog, world):
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mlp_catalog, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    digests, ids, n, sizes = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert len(digests) == 1, "ranks derived different schedules"
+    assert sorted(ids) == list(range(n)), "shards must partition the request stream"
+    assert all(s > 0 for s in sizes)
