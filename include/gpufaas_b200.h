@@ -157,7 +157,7 @@ typedef struct {
     int32_t only_gpu;            /* >= 0: execute only this GPU's decisions (one rank per GPU) */
     int32_t use_p2p;             /* false misses fetch from the peer holder over NVLink */
     int32_t host_io;             /* 1: inputs from pinned host, outputs back to host (e2e) */
-    int32_t record_kernels;      /* per-launch CUDA-event timing of the inference kernels */
+    int32_t record_kernels;      /* CUDA-event timing of every inference (its L+1 kernels, PDL-chained) */
     int32_t record_requests;     /* per-request service-time events */
     int32_t keep_outputs;        /* keep every request's output (parity checks) */
     const float* host_inputs;    /* host_io: [n_requests][batch*dims0] pinned, else NULL */
@@ -178,7 +178,7 @@ typedef struct {
     double device_ms;            /* CUDA-event time of the whole replay (max over devices) */
     double host_ms;              /* wall time of the call */
     double sched_ms;             /* host time spent in the control plane */
-    double kernel_ms;            /* sum of inference-kernel event times (record_kernels) */
+    double kernel_ms;            /* sum over inferences of their kernel-chain event time (record_kernels) */
     double h2d_ms;               /* sum of model-load event times */
     double service_p50_ms, service_p99_ms; /* per-request device service time (record_requests) */
     double sim_p50_s, sim_p99_s, sim_avg_latency_s; /* virtual-time latency from the schedule */

@@ -320,14 +320,16 @@ void GpuManager::infer(int model, const float* in, float* out) {
         a.b_off = blob.b_off[l];
         a.ntiles = mlp_layer_tiles(a.N);
         a.splits = mlp_layer_splits(a.K, a.N, sm_count_);
-        if (layer_timer) GFX_CUDA(cudaEventRecord(layer_timer->next(), compute_));
-        launch_mlp_layer(a, compute_);
-        if (layer_timer) GFX_CUDA(cudaEventRecord(layer_timer->next(), compute_));
+        if (l == 0 && layer_timer) GFX_CUDA(cudaEventRecord(layer_timer->next(), compute_));
+        // Layers 1.. and the softmax are programmatic dependents of the kernel
+        // before them: their prologue and weight prefetch overlap its tail.
+        launch_mlp_layer(a, compute_, /*pdl=*/l > 0);
         ++kernel_launches;
         x = a.y;
     }
     launch_softmax_rows(out, out + static_cast<size_t>(kBatch) * C, kBatch, C, compute_);
     ++kernel_launches;
+    if (layer_timer) GFX_CUDA(cudaEventRecord(layer_timer->next(), compute_));  // one pair per inference
     GFX_CUDA(cudaEventRecord(s.last_use, compute_));
 }
 

@@ -21,7 +21,7 @@ struct MlpLayerArgs {
     int splits, ntiles;
     int relu;
     int ldws;              // leading dimension of the split-K workspace
-    float* ws;             // [splits][32][ldws]
+    float* ws;             // split-K partials [tiles][splits][32][128]
     unsigned* counters;    // [ntiles + 1], zero between launches
     float* stats;          // last layer: [ntiles][32][2] per-tile softmax partials
     PageTable pt;
@@ -30,7 +30,9 @@ struct MlpLayerArgs {
 int mlp_layer_splits(int K, int N, int sm_count);
 int mlp_layer_tiles(int N);
 size_t mlp_layer_smem();
-void launch_mlp_layer(const MlpLayerArgs& a, cudaStream_t stream);
+// pdl: launch as a programmatic dependent of the previous kernel in the stream
+// (only when that previous operation is a kernel, not an event wait).
+void launch_mlp_layer(const MlpLayerArgs& a, cudaStream_t stream, bool pdl);
 void launch_softmax_rows(const float* logits, float* probs, int rows, int C, cudaStream_t s);
 // Fills `count` consecutive tensors of n values, tensor t from seed + t.
 void launch_fill_params(float* dst, uint64_t n, uint64_t seed, uint32_t tensor, float scale, cudaStream_t s,

@@ -105,6 +105,13 @@ __device__ __forceinline__ void split_tf32(const float4& v, float4& hi, float4& 
 }
 
 __device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
+// Programmatic dependent launch: wait for the previous kernel of the stream
+// (no-op without the launch attribute) / let the next one start its prologue.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+}
 
 __global__ void __launch_bounds__(kThreads, 1)
     mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ MlpLayerArgs a) {
@@ -156,9 +163,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == 0) {
         // ---------------- TMA producer ----------------
         if (lane == 0) {
-            for (int it = 0; it < nkt; ++it) {
+            // Weights do not depend on the previous layer: stream the first
+            // landing slots' weight tiles before waiting for it (PDL overlap).
+            const int pre = nkt < kLand ? nkt : kLand;
+            for (int it = 0; it < pre; ++it) {
+                const Landing ld = landing(smem, it);
+                mbar_arrive_expect_tx(&land_full[it], kLandBytes);
+                const uint64_t v = a.w_off + (static_cast<uint64_t>(tile) * kt_total + kt_begin + it) * kWBytes;
+                tma_bulk_g2s(ld.w, translate(a.arena, pt, v), kWBytes, &land_full[it]);
+            }
+            pdl_wait();
+            for (int it = 0; it < pre; ++it)
+                tma_tile2d_g2s(landing(smem, it).x, &tmap_x, (kt_begin + it) * kTileK, 0, &land_full[it]);
+            for (int it = pre; it < nkt; ++it) {
                 const int s = it % kLand;
-                if (it >= kLand) mbar_wait(&land_empty[s], ((it / kLand) & 1) ^ 1);
+                mbar_wait(&land_empty[s], ((it / kLand) & 1) ^ 1);
                 const Landing ld = landing(smem, s);
                 const int kt = kt_begin + it;
                 mbar_arrive_expect_tx(&land_full[s], kLandBytes);
@@ -253,11 +272,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         while (drained < nchunks) drain(drained++);
 
+        pdl_trigger();  // main loop done: the next layer may start its prologue
+        pdl_wait();     // workspace / counters / output belong to us only after the previous layer
         bool finisher = true;
         if (a.splits > 1) {
-            float* ws = a.ws + static_cast<size_t>(split) * kRows * a.ldws;
+            // Partials: ws[tile][split][32 rows][128 features], contiguous 16 KB blocks.
+            const int fl = q * 32 + lane;
+            float* blk = a.ws + (static_cast<size_t>(tile) * a.splits + split) * (kRows * kTileM);
 #pragma unroll
-            for (int b = 0; b < kRows; ++b) ws[static_cast<size_t>(b) * a.ldws + f] = acc[b];
+            for (int b = 0; b < kRows; ++b) blk[b * kTileM + fl] = acc[b];
             __threadfence();
             epi_sync();
             if (ct == 0) last_flag = atomicAdd(&a.counters[tile], 1u) == static_cast<unsigned>(a.splits - 1);
@@ -265,18 +288,31 @@ __global__ void __launch_bounds__(kThreads, 1)
             finisher = last_flag;
             if (finisher) {
                 __threadfence();
+                // Gather all partials of the tile into the (now idle) landing ring in
+                // one round of cp.async, then sum in fixed split order (deterministic).
+                float* red = reinterpret_cast<float*>(smem);
+                const float* src = a.ws + static_cast<size_t>(tile) * a.splits * (kRows * kTileM);
+                constexpr int kGroup = (kLand * kLandBytes) / (kRows * kTileM * 4);  // partials per round
 #pragma unroll
                 for (int b = 0; b < kRows; ++b) acc[b] = 0.f;
-                for (int sp = 0; sp < a.splits; ++sp) {  // fixed order: deterministic
-                    const float* w = a.ws + static_cast<size_t>(sp) * kRows * a.ldws;
+                for (int g0 = 0; g0 < a.splits; g0 += kGroup) {
+                    const int ng = a.splits - g0 < kGroup ? a.splits - g0 : kGroup;
+                    const int chunks = ng * kRows * kTileM / 4;  // 16-byte chunks
+                    for (int c = ct; c < chunks; c += 128)
+                        cp_async16(red + 4 * c, src + static_cast<size_t>(g0) * kRows * kTileM + 4 * c);
+                    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+                    epi_sync();
+                    for (int sp = 0; sp < ng; ++sp) {
 #pragma unroll
-                    for (int b = 0; b < kRows; ++b) acc[b] += __ldcg(&w[static_cast<size_t>(b) * a.ldws + f]);
+                        for (int b = 0; b < kRows; ++b) acc[b] += red[(sp * kRows + b) * kTileM + fl];
+                    }
+                    epi_sync();
                 }
                 if (ct == 0) a.counters[tile] = 0;
             }
         }
         if (finisher) {
-            const bool valid = f < N;
+            const bool valid = f < N;  // rows >= N are the zero padding of the last weight tile
             const float bias = valid ? *reinterpret_cast<const float*>(translate(a.arena, pt, a.b_off + 4ull * f)) : 0.f;
 #pragma unroll
             for (int b = 0; b < kRows; ++b) {
@@ -341,22 +377,30 @@ int mlp_layer_tiles(int N) { return (N + kTileM - 1) / kTileM; }
 
 size_t mlp_layer_smem() { return static_cast<size_t>(kLandBytes) * kLand + static_cast<size_t>(kOpBytes) * kOps + 1024; }
 
-void launch_mlp_layer(const MlpLayerArgs& a, cudaStream_t stream) {
+void launch_mlp_layer(const MlpLayerArgs& a, cudaStream_t stream, bool pdl) {
     if (a.K % kTileK != 0) throw std::runtime_error("mlp layer: K must be a multiple of 32");
     CUtensorMap tmx;
     if (!encode_tensor_map_2d(&tmx, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, a.x, static_cast<uint64_t>(a.K), kRows,
                               static_cast<uint64_t>(a.K) * 4, kTileK, kRows, CU_TENSOR_MAP_SWIZZLE_128B))
         throw CudaError("cuTensorMapEncodeTiled failed for the activation tile map");
-    static bool attr = false;
+    static bool attr_set = false;
     const size_t smem = mlp_layer_smem();
-    if (!attr) {
+    if (!attr_set) {
         GFX_CUDA(cudaFuncSetAttribute(mlp_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(smem)));
-        attr = true;
+        attr_set = true;
     }
-    dim3 grid(static_cast<unsigned>(a.ntiles), static_cast<unsigned>(a.splits));
-    mlp_tc_kernel<<<grid, kThreads, smem, stream>>>(tmx, a);
-    GFX_CUDA(cudaGetLastError());
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(a.ntiles), static_cast<unsigned>(a.splits));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    GFX_CUDA(cudaLaunchKernelEx(&cfg, mlp_tc_kernel, tmx, a));
 }
 
 // Row softmax of the classifier logits: one CTA per batch row, 256 threads,
@@ -364,6 +408,7 @@ void launch_mlp_layer(const MlpLayerArgs& a, cudaStream_t stream) {
 __global__ void __launch_bounds__(256) softmax_rows_kernel(const float* __restrict__ logits,
                                                            float* __restrict__ probs, int C) {
     __shared__ float red[8];
+    pdl_wait();
     const int row = blockIdx.x;
     const float* in = logits + static_cast<size_t>(row) * C;
     float* out = probs + static_cast<size_t>(row) * C;
@@ -409,8 +454,16 @@ __global__ void __launch_bounds__(256) softmax_rows_kernel(const float* __restri
 
 void launch_softmax_rows(const float* logits, float* probs, int rows, int C, cudaStream_t s) {
     if (C > 2048) throw std::runtime_error("softmax: at most 2048 classes");
-    softmax_rows_kernel<<<rows, 256, 0, s>>>(logits, probs, C);
-    GFX_CUDA(cudaGetLastError());
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(rows));
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    GFX_CUDA(cudaLaunchKernelEx(&cfg, softmax_rows_kernel, logits, probs, C));
 }
 
 // Request inputs / test tensors straight from the parameter stream; one
