@@ -88,13 +88,15 @@ void gfx_sim_free(void* h);
 typedef struct gfx_arena_s* gfx_arena_t; /* one per device: the GPU manager */
 typedef struct gfx_event_s* gfx_event_t;
 
-#define GFX_MODEL_MLP 1 /* fp32 MLP classifier: relu(xW^T+b) ... softmax */
+#define GFX_MODEL_MLP 1  /* fp32 MLP classifier: relu(xW^T+b) ... softmax */
+#define GFX_MODEL_BERT 2 /* bf16 post-LN transformer encoder + tanh pooler (C5) */
 
 typedef struct {
     int32_t family;             /* GFX_MODEL_* */
-    int32_t n_layers;           /* linear layers */
-    int32_t dims[GFX_MAX_LAYERS + 1]; /* dims[0] = input features, dims[L] = classes */
-    int32_t batch;              /* rows per request (32) */
+    int32_t n_layers;           /* MLP: linear layers; BERT: encoder layers */
+    int32_t dims[GFX_MAX_LAYERS + 1]; /* MLP: dims[0] = input features, dims[L] = classes;
+                                         BERT: {d_model, heads, ffn, seq} */
+    int32_t batch;              /* MLP: rows per request (32); BERT: sequences per request */
     int32_t pad_;
     uint64_t seed;              /* parameter stream */
 } gfx_model_desc;
@@ -108,6 +110,8 @@ int gfx_device_init(int dev, int enable_peers);
 int gfx_model_register(int model_idx, const gfx_model_desc* desc);
 int gfx_model_bytes(int model_idx, uint64_t* bytes);
 int gfx_model_pages(int model_idx, int32_t* pages);
+/* Bytes of one request's input / output tensors for this model. */
+int gfx_model_io_bytes(int model_idx, uint64_t* in_bytes, uint64_t* out_bytes);
 int gfx_models_clear(void);
 
 /* Pre-allocated HBM arena of `capacity_bytes` (multiple of GFX_PAGE_BYTES)
@@ -123,10 +127,14 @@ int gfx_arena_resident(gfx_arena_t a, int model_idx, int32_t* out);
 int gfx_load_h2d(gfx_arena_t a, int model_idx, gfx_event_t* done);
 int gfx_fetch_p2p(gfx_arena_t dst, gfx_arena_t src, int model_idx, gfx_event_t* done);
 int gfx_evict(gfx_arena_t a, int model_idx);
-/* One batched inference of a resident model. in: [batch x dims[0]] fp32,
- * out: [2][batch x classes] fp32 (logits then softmax probabilities). Both
- * are DEVICE pointers on the arena's device. */
-int gfx_infer(gfx_arena_t a, int model_idx, const float* in, float* out, int batch, gfx_event_t* done);
+/* One batched inference of a resident model (DEVICE pointers on the arena's device).
+ * MLP:  in [batch x dims[0]] fp32, out [2][batch x classes] fp32 (logits, softmax).
+ * BERT: in [batch*seq x d] bf16 embeddings, out [batch x d] fp32 pooled output. */
+int gfx_infer(gfx_arena_t a, int model_idx, const void* in, void* out, int batch, gfx_event_t* done);
+
+/* Test/debug: BERT inference that also copies every layer's hidden state into
+ * hidden ([L+1][batch*seq][d] bf16, device) for teacher-forced parity checks. */
+int gfx_infer_debug(gfx_arena_t a, int model_idx, const void* in, void* out, int batch, void* hidden);
 
 int gfx_event_query(gfx_event_t e); /* 0 done, 1 pending */
 int gfx_event_sync(gfx_event_t e);
@@ -143,6 +151,8 @@ int gfx_fill_params(gfx_arena_t a, float* dst, uint64_t n, uint64_t seed, uint32
 uint64_t gfx_input_seed(int request_id);
 /* Same stream generated on the host (no device needed). */
 int gfx_host_fill_params(float* dst, uint64_t n, uint64_t seed, uint32_t tensor, float scale);
+/* The model's request input for request_id, generated on the host (fp32 or bf16 bits). */
+int gfx_host_fill_input(int model_idx, int request_id, void* dst, uint64_t bytes);
 
 /* ---------------------------------------------------------------- replay */
 /* Trace replay: the control plane (scheduler + cluster state, bit-exact with
@@ -160,8 +170,8 @@ typedef struct {
     int32_t record_kernels;      /* CUDA-event timing of every inference (its L+1 kernels, PDL-chained) */
     int32_t record_requests;     /* per-request service-time events */
     int32_t keep_outputs;        /* keep every request's output (parity checks) */
-    const float* host_inputs;    /* host_io: [n_requests][batch*dims0] pinned, else NULL */
-    float* host_outputs;         /* host_io/keep_outputs: [n_requests][2*batch*classes] or NULL */
+    const void* host_inputs;     /* host_io: [n_requests][in_bytes] pinned, else NULL */
+    void* host_outputs;          /* host_io: [n_requests][out_bytes] or NULL */
 } gfx_replay_args;
 
 typedef struct {
@@ -192,8 +202,8 @@ typedef struct {
 typedef struct gfx_replay_s* gfx_replay_t;
 int gfx_replay_create(const gfx_replay_args* args, gfx_replay_t* out);
 int gfx_replay_run(gfx_replay_t r, gfx_replay_result* out);
-/* Per-request outputs of the last run (keep_outputs): [n_requests][2*batch*classes]. */
-int gfx_replay_outputs(gfx_replay_t r, float* host, uint64_t count);
+/* Per-request outputs of the last run (keep_outputs): [n_requests][out_bytes]. */
+int gfx_replay_outputs(gfx_replay_t r, void* host, uint64_t bytes);
 /* Per-request model row and device service time (ms) of the last run. */
 int gfx_replay_requests(gfx_replay_t r, int32_t* model_idx, double* service_ms, int64_t n);
 int gfx_replay_destroy(gfx_replay_t r);

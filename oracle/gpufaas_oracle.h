@@ -108,6 +108,19 @@ void orc_fill_params(uint64_t model_seed, uint32_t tensor, uint64_t n, float sca
 int orc_mlp_forward(uint64_t model_seed, int n_layers, const int32_t* dims, int batch,
                     const float* x, float* logits, float* probs, int threads);
 
+/* BERT-base-style encoder (C5) forward, fp64 accumulation with the product's
+ * bf16 rounding points. x_bits: [batch*seq x d] bf16 bit patterns;
+ * pooled: [batch x d] fp32. */
+int orc_bert_forward(uint64_t seed, int L, int d, int heads, int ffn, int seq, int batch, const uint16_t* x_bits,
+                     float* pooled, int threads);
+/* Teacher-forced pieces: encoder layer l applied to a given bf16 input, and the
+ * pooler applied to a given final hidden state. */
+int orc_bert_layer(uint64_t seed, int l, int d, int heads, int ffn, int seq, int batch, const uint16_t* x_in,
+                   uint16_t* x_out, int threads);
+int orc_bert_pool(uint64_t seed, int L, int d, int seq, int batch, const uint16_t* x_bits, float* pooled);
+/* Test hook: fp32 (k-order) GEMM accumulation, to measure intrinsic sensitivity. */
+void orc_set_acc32(int on);
+
 #ifdef __cplusplus
 }
 #endif

@@ -72,6 +72,8 @@ gfx_model_register = _sig("gfx_model_register", C.c_int, [C.c_int, C.POINTER(Mod
 gfx_model_bytes = _sig("gfx_model_bytes", C.c_int, [C.c_int, C.POINTER(C.c_uint64)])
 gfx_model_pages = _sig("gfx_model_pages", C.c_int, [C.c_int, C.POINTER(C.c_int32)])
 gfx_models_clear = _sig("gfx_models_clear", C.c_int, [])
+gfx_model_io_bytes = _sig("gfx_model_io_bytes", C.c_int, [C.c_int, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)])
+gfx_host_fill_input = _sig("gfx_host_fill_input", C.c_int, [C.c_int, C.c_int, C.c_void_p, C.c_uint64])
 gfx_arena_create = _sig("gfx_arena_create", C.c_int, [C.c_int, C.c_uint64, C.POINTER(_vp)])
 gfx_arena_destroy = _sig("gfx_arena_destroy", C.c_int, [_vp])
 gfx_arena_reset = _sig("gfx_arena_reset", C.c_int, [_vp])
@@ -81,6 +83,7 @@ gfx_load_h2d = _sig("gfx_load_h2d", C.c_int, [_vp, C.c_int, C.POINTER(_vp)])
 gfx_fetch_p2p = _sig("gfx_fetch_p2p", C.c_int, [_vp, _vp, C.c_int, C.POINTER(_vp)])
 gfx_evict = _sig("gfx_evict", C.c_int, [_vp, C.c_int])
 gfx_infer = _sig("gfx_infer", C.c_int, [_vp, C.c_int, _vp, _vp, C.c_int, C.POINTER(_vp)])
+gfx_infer_debug = _sig("gfx_infer_debug", C.c_int, [_vp, C.c_int, _vp, _vp, C.c_int, _vp])
 gfx_event_query = _sig("gfx_event_query", C.c_int, [_vp])
 gfx_event_sync = _sig("gfx_event_sync", C.c_int, [_vp])
 gfx_event_release = _sig("gfx_event_release", C.c_int, [_vp])

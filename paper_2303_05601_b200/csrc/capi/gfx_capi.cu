@@ -93,13 +93,14 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
     std::vector<int> dev_of;
     // device buffers per device
     struct DevBufs {
-        float* inputs = nullptr;   // [n][in_elems]
-        float* outputs = nullptr;  // [n][out_elems] (keep/host_io) or [2][out_elems] ring
+        char* inputs = nullptr;    // [n][in_bytes]
+        char* outputs = nullptr;   // [n][out_bytes] (keep/host_io) or [2][out_bytes] ring
         cudaStream_t io_in = nullptr, io_out = nullptr;
         cudaEvent_t start = nullptr, stop = nullptr;
     };
     std::vector<DevBufs> bufs;  // per GPU id
-    size_t in_elems = 0, out_elems = 0;
+    size_t in_bytes = 0, out_bytes = 0;
+    int family = 0;
     bool full_outputs = false;
     // timing
     KernelTimer layer_timer, load_timer, req_timer;
@@ -120,21 +121,20 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
         if (args.n_devices != 1 && args.n_devices != G)
             throw std::invalid_argument("n_devices must be 1 or cfg.gpu_count");
         // Every catalog model must be registered and its charge must cover its pages.
-        int C = -1, D0 = -1;
         for (size_t i = 0; i < catalog.size(); ++i) {
             const gfx::ModelBlob& b = ModelStore::get().at(static_cast<int>(i));
             const double need = 2.0 * b.pages;
             if (catalog.profiles()[i].occupation_mb < need)
                 throw std::invalid_argument("catalog occupation_mb of '" + catalog.profiles()[i].model_id +
                                             "' is below its " + std::to_string(b.pages) + " arena pages");
-            const int c = b.desc.dims[b.desc.n_layers], d0 = b.desc.dims[0];
-            if ((C >= 0 && C != c) || (D0 >= 0 && D0 != d0))
-                throw std::invalid_argument("all models of a replay must share input and class widths");
-            C = c;
-            D0 = d0;
+            if (i == 0) {
+                in_bytes = b.in_bytes;
+                out_bytes = b.out_bytes;
+                family = b.desc.family;
+            } else if (b.in_bytes != in_bytes || b.out_bytes != out_bytes || b.desc.family != family) {
+                throw std::invalid_argument("all models of a replay must share family and request tensor shapes");
+            }
         }
-        in_elems = static_cast<size_t>(32) * D0;
-        out_elems = static_cast<size_t>(2) * 32 * C;
         full_outputs = args.keep_outputs || args.host_io;
         const uint64_t pages = static_cast<uint64_t>(args.cfg.capacity_mb / 2.0);
         const uint64_t cap_bytes = pages * gfx::kPageBytes;
@@ -152,16 +152,20 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
             DevBufs& b = bufs[g];
             GFX_CUDA(cudaSetDevice(dev_of[g]));
             // Inputs: every request this GPU might serve (ids are global).
-            GFX_CUDA(cudaMalloc(&b.inputs, sizeof(float) * in_elems * std::max<size_t>(n, 1)));
-            GFX_CUDA(cudaMalloc(&b.outputs, sizeof(float) * out_elems * (full_outputs ? std::max<size_t>(n, 1) : 2)));
+            GFX_CUDA(cudaMalloc(&b.inputs, in_bytes * std::max<size_t>(n, 1)));
+            GFX_CUDA(cudaMalloc(&b.outputs, out_bytes * (full_outputs ? std::max<size_t>(n, 1) : 2)));
             GFX_CUDA(cudaStreamCreateWithFlags(&b.io_in, cudaStreamNonBlocking));
             GFX_CUDA(cudaStreamCreateWithFlags(&b.io_out, cudaStreamNonBlocking));
             GFX_CUDA(cudaEventCreate(&b.start));
             GFX_CUDA(cudaEventCreate(&b.stop));
             if (!args.host_io) {
                 // HBM-resident inputs, generated once outside the timed region.
-                gfx::launch_fill_params(b.inputs, in_elems, gfx_input_seed(0), 0xFFFFFFFFu, 1.0f,
-                                        mgrs[g]->compute_stream(), n);
+                if (family == GFX_MODEL_BERT)
+                    gfx::launch_fill_bf16(reinterpret_cast<__nv_bfloat16*>(b.inputs), in_bytes / 2, gfx_input_seed(0),
+                                          0xFFFFFFFFu, 1.0f, mgrs[g]->compute_stream(), n);
+                else
+                    gfx::launch_fill_params(reinterpret_cast<float*>(b.inputs), in_bytes / 4, gfx_input_seed(0),
+                                            0xFFFFFFFFu, 1.0f, mgrs[g]->compute_stream(), n);
             }
             GFX_CUDA(cudaDeviceSynchronize());
         }
@@ -215,16 +219,16 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
         } else if (e0) {
             GFX_CUDA(cudaEventRecord(e0, m.compute_stream()));
         }
-        float* in = b.inputs + static_cast<size_t>(rid) * in_elems;
-        float* out = b.outputs + (full_outputs ? static_cast<size_t>(rid) : static_cast<size_t>(rid & 1)) * out_elems;
+        char* in = b.inputs + static_cast<size_t>(rid) * in_bytes;
+        char* out = b.outputs + (full_outputs ? static_cast<size_t>(rid) : static_cast<size_t>(rid & 1)) * out_bytes;
         if (args.host_io) {
             // e2e: this request's input crosses PCIe inside the timed region.
-            GFX_CUDA(cudaMemcpyAsync(in, args.host_inputs + static_cast<size_t>(rid) * in_elems,
-                                     sizeof(float) * in_elems, cudaMemcpyHostToDevice, b.io_in));
+            GFX_CUDA(cudaMemcpyAsync(in, static_cast<const char*>(args.host_inputs) + static_cast<size_t>(rid) * in_bytes,
+                                     in_bytes, cudaMemcpyHostToDevice, b.io_in));
             cudaEvent_t ein = req_timer.next();
             GFX_CUDA(cudaEventRecord(ein, b.io_in));
             GFX_CUDA(cudaStreamWaitEvent(m.compute_stream(), ein, 0));
-            res.io_h2d_bytes += sizeof(float) * in_elems;
+            res.io_h2d_bytes += in_bytes;
         }
         m.infer(model, in, out);
         const gfx::ModelBlob& blob = ModelStore::get().at(model);
@@ -239,9 +243,9 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
             cudaEvent_t done = req_timer.next();
             GFX_CUDA(cudaEventRecord(done, m.compute_stream()));
             GFX_CUDA(cudaStreamWaitEvent(b.io_out, done, 0));
-            GFX_CUDA(cudaMemcpyAsync(args.host_outputs + static_cast<size_t>(rid) * out_elems, out,
-                                     sizeof(float) * out_elems, cudaMemcpyDeviceToHost, b.io_out));
-            res.io_d2h_bytes += sizeof(float) * out_elems;
+            GFX_CUDA(cudaMemcpyAsync(static_cast<char*>(args.host_outputs) + static_cast<size_t>(rid) * out_bytes, out,
+                                     out_bytes, cudaMemcpyDeviceToHost, b.io_out));
+            res.io_d2h_bytes += out_bytes;
         }
     }
 
@@ -404,6 +408,28 @@ int gfx_model_bytes(int model_idx, uint64_t* bytes) {
 int gfx_model_pages(int model_idx, int32_t* pages) {
     return guarded([&] { *pages = static_cast<int32_t>(ModelStore::get().at(model_idx).pages); });
 }
+int gfx_model_io_bytes(int model_idx, uint64_t* in_bytes, uint64_t* out_bytes) {
+    return guarded([&] {
+        const gfx::ModelBlob& b = ModelStore::get().at(model_idx);
+        *in_bytes = b.in_bytes;
+        *out_bytes = b.out_bytes;
+    });
+}
+int gfx_host_fill_input(int model_idx, int request_id, void* dst, uint64_t bytes) {
+    return guarded([&] {
+        const gfx::ModelBlob& b = ModelStore::get().at(model_idx);
+        if (bytes < b.in_bytes) throw std::invalid_argument("input buffer too small");
+        const uint64_t st = gfx::param_stream(gfx_input_seed(request_id), 0xFFFFFFFFu);
+        const float sc = gfx::param_scale(1.0f);
+        if (b.desc.family == GFX_MODEL_BERT) {
+            uint16_t* o = static_cast<uint16_t*>(dst);
+            for (uint64_t i = 0; i < b.in_bytes / 2; ++i) o[i] = gfx::bf16_bits(gfx::param_at(st, i, sc));
+        } else {
+            float* o = static_cast<float*>(dst);
+            for (uint64_t i = 0; i < b.in_bytes / 4; ++i) o[i] = gfx::param_at(st, i, sc);
+        }
+    });
+}
 int gfx_models_clear(void) {
     return guarded([&] { ModelStore::get().clear(); });
 }
@@ -453,11 +479,22 @@ int gfx_fetch_p2p(gfx_arena_t dst, gfx_arena_t src, int model_idx, gfx_event_t* 
 int gfx_evict(gfx_arena_t a, int model_idx) {
     return guarded([&] { a->mgr->evict(model_idx); });
 }
-int gfx_infer(gfx_arena_t a, int model_idx, const float* in, float* out, int batch, gfx_event_t* done) {
+int gfx_infer(gfx_arena_t a, int model_idx, const void* in, void* out, int batch, gfx_event_t* done) {
     return guarded([&] {
-        if (batch != 32) throw std::invalid_argument("batch must be 32");
+        if (batch != ModelStore::get().at(model_idx).desc.batch)
+            throw std::invalid_argument("batch does not match the registered model");
         a->mgr->infer(model_idx, in, out);
         make_event(*a->mgr, a->mgr->compute_stream(), done);
+    });
+}
+
+int gfx_infer_debug(gfx_arena_t a, int model_idx, const void* in, void* out, int batch, void* hidden) {
+    return guarded([&] {
+        const gfx::ModelBlob& b = ModelStore::get().at(model_idx);
+        if (b.desc.family != GFX_MODEL_BERT) throw std::invalid_argument("gfx_infer_debug: BERT models only");
+        if (batch != b.desc.batch) throw std::invalid_argument("batch does not match the registered model");
+        a->mgr->infer(model_idx, in, out, hidden);
+        GFX_CUDA(cudaStreamSynchronize(a->mgr->compute_stream()));
     });
 }
 
@@ -551,25 +588,24 @@ int gfx_replay_create(const gfx_replay_args* args, gfx_replay_t* out) {
 int gfx_replay_run(gfx_replay_t r, gfx_replay_result* out) {
     return guarded([&] { r->run(out); });
 }
-int gfx_replay_outputs(gfx_replay_t r, float* host, uint64_t count) {
+int gfx_replay_outputs(gfx_replay_t r, void* host, uint64_t bytes) {
     return guarded([&] {
         if (!r->full_outputs) throw std::invalid_argument("replay was created without keep_outputs");
         const size_t n = r->requests.size();
-        if (count < n * r->out_elems) throw std::invalid_argument("output buffer too small");
-        // Outputs live on the GPU that served each request.
-        std::vector<float> tmp(r->out_elems);
+        if (bytes < n * r->out_bytes) throw std::invalid_argument("output buffer too small");
         for (size_t g = 0; g < r->mgrs.size(); ++g) {
             if (!r->mgrs[g]) continue;
             GFX_CUDA(cudaSetDevice(r->dev_of[g]));
             GFX_CUDA(cudaDeviceSynchronize());
         }
-        // Route each request to the GPU whose manager executed it (last run).
+        // Each request's output lives on the GPU that served it in the last run.
         for (size_t i = 0; i < n; ++i) {
             const int g = r->req_gpu[i] >= 0 ? r->req_gpu[i] : (r->args.only_gpu >= 0 ? r->args.only_gpu : 0);
             if (!r->mgrs[static_cast<size_t>(g)]) continue;
             GFX_CUDA(cudaSetDevice(r->dev_of[static_cast<size_t>(g)]));
-            GFX_CUDA(cudaMemcpy(host + i * r->out_elems, r->bufs[static_cast<size_t>(g)].outputs + i * r->out_elems,
-                                sizeof(float) * r->out_elems, cudaMemcpyDeviceToHost));
+            GFX_CUDA(cudaMemcpy(static_cast<char*>(host) + i * r->out_bytes,
+                                r->bufs[static_cast<size_t>(g)].outputs + i * r->out_bytes, r->out_bytes,
+                                cudaMemcpyDeviceToHost));
         }
     });
 }

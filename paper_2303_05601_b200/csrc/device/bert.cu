@@ -1,0 +1,554 @@
+// C5: BERT-base-style encoder (post-LN, bf16 activations, fp32 accumulation)
+// served from the paged HBM arena.
+//
+// Kernels:
+//   K2 gemm_bf16_kernel   Y[T x N] = epi(X[T x K] . W^T + b) on tcgen05
+//                         (kind::f16, bf16 -> fp32 in TMEM), 128x128 tiles, X via
+//                         a 2-D TMA tensor map, W tiles (pre-swizzled 16 KB) via
+//                         1-D bulk TMA from the arena; epilogue fused: bias,
+//                         GELU, or residual add; bf16 out. Tensor-core bound.
+//   K3 attention_kernel   softmax(Q K^T / sqrt(64)) V per (sequence, head),
+//                         S = 128: one CTA, 8 warps x 16 query rows, warp-level
+//                         mma.sync (bf16 -> fp32) flash-attention-2 style; 2.7 %
+//                         of the model's flops.
+//   K4 layernorm_kernel   one warp per token row, 16-byte vector loads, fp32
+//                         two-pass statistics; HBM bound.
+//   pooler_kernel         tanh(Wp . x_cls + bp) per sequence, fp32 out.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+
+#include "bert.cuh"
+#include "mlp.cuh"
+#include "sm100.cuh"
+
+namespace gfx {
+
+namespace {
+
+using namespace gfx::sm100;
+
+__device__ __forceinline__ const char* translate(const char* arena, const uint32_t* pt, uint64_t v) {
+    return arena + (static_cast<uint64_t>(pt[v >> kPageShift]) << kPageShift) + (v & kPageMask);
+}
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+
+__device__ __forceinline__ float gelu(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
+
+// ------------------------------------------------------------------ K2 GEMM
+
+constexpr int kGM = 128, kGN = 128, kGK = 64, kGStages = 4, kGThreads = 192;
+constexpr uint32_t kGTile = 128 * 128;  // 16 KB (A tile = B tile)
+constexpr uint32_t kGStage = 2 * kGTile;
+
+enum Epi : int { kEpiBias = 0, kEpiGelu = 1, kEpiResid = 2 };
+
+struct GemmArgs {
+    const char* arena;
+    uint64_t w_off, b_off;        // weight tiles, fp32 bias
+    __nv_bfloat16* y;             // [T x N]
+    const __nv_bfloat16* resid;   // [T x N] (kEpiResid)
+    int K, N;
+    PageTable pt;
+};
+
+template <int kEpi>
+__global__ void __launch_bounds__(kGThreads, 1)
+    gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ GemmArgs a) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
+    __shared__ __align__(8) uint64_t full_bar[kGStages], empty_bar[kGStages], tmem_bar;
+    __shared__ uint32_t tmem_s;
+    __shared__ uint32_t pt[GFX_MAX_PAGES];
+    __shared__ float bias_s[kGN];
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int n0 = blockIdx.x * kGN, m0 = blockIdx.y * kGM;
+    const int nkt = a.K / kGK;
+    const int ktiles_row = a.K / kGK;
+
+    for (int i = tid; i < static_cast<int>(a.pt.n); i += kGThreads) pt[i] = a.pt.page[i];
+    if (tid == 0) {
+        for (int s = 0; s < kGStages; ++s) {
+            mbar_init(&full_bar[s], 1);
+            mbar_init(&empty_bar[s], 1);
+        }
+        mbar_init(&tmem_bar, 1);
+        mbar_fence_init();
+        tma_prefetch_desc(&tmap_x);
+    }
+    if (warp == 1) tmem_alloc<128>(&tmem_s);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_s;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            const int pre = nkt < kGStages ? nkt : kGStages;
+            for (int it = 0; it < pre; ++it) {  // weights: before the grid dependency
+                uint8_t* st = smem + static_cast<size_t>(it) * kGStage;
+                mbar_arrive_expect_tx(&full_bar[it], kGStage);
+                const uint64_t v = a.w_off + (static_cast<uint64_t>(blockIdx.x) * ktiles_row + it) * kGTile;
+                tma_bulk_g2s(st + kGTile, translate(a.arena, pt, v), kGTile, &full_bar[it]);
+            }
+            pdl_wait();
+            for (int it = 0; it < pre; ++it)
+                tma_tile2d_g2s(smem + static_cast<size_t>(it) * kGStage, &tmap_x, it * kGK, m0, &full_bar[it]);
+            for (int it = pre; it < nkt; ++it) {
+                const int s = it % kGStages;
+                mbar_wait(&empty_bar[s], ((it / kGStages) & 1) ^ 1);
+                uint8_t* st = smem + static_cast<size_t>(s) * kGStage;
+                mbar_arrive_expect_tx(&full_bar[s], kGStage);
+                const uint64_t v = a.w_off + (static_cast<uint64_t>(blockIdx.x) * ktiles_row + it) * kGTile;
+                tma_bulk_g2s(st + kGTile, translate(a.arena, pt, v), kGTile, &full_bar[s]);
+                tma_tile2d_g2s(st, &tmap_x, it * kGK, m0, &full_bar[s]);
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {
+            constexpr uint32_t idesc = umma_idesc<kGM, kGN, 1>();  // BF16 x BF16 -> F32
+            for (int it = 0; it < nkt; ++it) {
+                const int s = it % kGStages;
+                mbar_wait(&full_bar[s], (it / kGStages) & 1);
+                tc_fence_after();
+                uint8_t* st = smem + static_cast<size_t>(s) * kGStage;
+#pragma unroll
+                for (int kk = 0; kk < kGK / 16; ++kk) {  // K = 16 bf16 = 32 bytes per MMA
+                    umma_f16(tmem, umma_desc_sw128(st, kk * 32), umma_desc_sw128(st + kGTile, kk * 32), idesc,
+                             (it | kk) ? 1u : 0u);
+                }
+                umma_commit(&empty_bar[s]);
+            }
+            umma_commit(&tmem_bar);
+        }
+    } else {
+        // Epilogue: TMEM lane = token row, column = output feature.
+        const int q = warp & 3;
+        const int row = m0 + q * 32 + lane;
+        bias_s[tid - 64] = *reinterpret_cast<const float*>(translate(a.arena, pt, a.b_off + 4ull * (n0 + tid - 64)));
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");  // epilogue warps only
+        mbar_wait(&tmem_bar, 0);
+        tc_fence_after();
+        pdl_trigger();
+        __nv_bfloat16* yrow = a.y + static_cast<size_t>(row) * a.N + n0;
+#pragma unroll 1
+        for (int c = 0; c < kGN / 32; ++c) {
+            float v[32];
+            tmem_ld_32x32b_x32(tmem + static_cast<uint32_t>(c * 32) + (static_cast<uint32_t>(q * 32) << 16), v);
+            float r[32];
+            if (kEpi == kEpiResid) {
+                const uint4* rp = reinterpret_cast<const uint4*>(a.resid + static_cast<size_t>(row) * a.N + n0 + c * 32);
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint4 u = rp[i];
+                    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const float2 f2 = __bfloat1622float2(h2[j]);
+                        r[i * 8 + 2 * j] = f2.x;
+                        r[i * 8 + 2 * j + 1] = f2.y;
+                    }
+                }
+            }
+            uint4 out[4];
+            __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(out);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                float x0 = v[2 * j] + bias_s[c * 32 + 2 * j];
+                float x1 = v[2 * j + 1] + bias_s[c * 32 + 2 * j + 1];
+                if (kEpi == kEpiGelu) {
+                    x0 = gelu(x0);
+                    x1 = gelu(x1);
+                }
+                if (kEpi == kEpiResid) {
+                    x0 += r[2 * j];
+                    x1 += r[2 * j + 1];
+                }
+                o2[j] = __floats2bfloat162_rn(x0, x1);
+            }
+            uint4* dst = reinterpret_cast<uint4*>(yrow + c * 32);
+#pragma unroll
+            for (int i = 0; i < 4; ++i) dst[i] = out[i];
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 1) tmem_dealloc<128>(tmem);
+}
+
+// ------------------------------------------------------------------ K3 attention
+// One CTA per (sequence, head), S = 128 tokens, d_head = 64. Warp w owns query
+// rows 16w..16w+15; mma.sync m16n8k16 bf16 -> fp32.
+
+constexpr int kS = 128, kDh = 64;
+constexpr int kKPitch = kDh + 8;   // bf16 elements per K row (bank-conflict-free B loads)
+constexpr int kVPitch = kS + 8;    // bf16 elements per V^T row
+
+__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__global__ void __launch_bounds__(256) attention_kernel(const __nv_bfloat16* __restrict__ qkv,
+                                                        __nv_bfloat16* __restrict__ ctx, int heads) {
+    __shared__ __align__(16) __nv_bfloat16 ks[kS * kKPitch];
+    __shared__ __align__(16) __nv_bfloat16 vts[kDh * kVPitch];
+    const int seq = blockIdx.x / heads, h = blockIdx.x % heads;
+    const int d = heads * kDh, ld = 3 * d;
+    const size_t tok0 = static_cast<size_t>(seq) * kS;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    pdl_wait();
+    // K rows and V transposed into shared memory.
+    for (int i = tid; i < kS * (kDh / 8); i += 256) {
+        const int t = i / (kDh / 8), c = (i % (kDh / 8)) * 8;
+        const uint4 kv = *reinterpret_cast<const uint4*>(qkv + (tok0 + t) * ld + d + h * kDh + c);
+        *reinterpret_cast<uint4*>(&ks[t * kKPitch + c]) = kv;
+        const uint4 vv = *reinterpret_cast<const uint4*>(qkv + (tok0 + t) * ld + 2 * d + h * kDh + c);
+        const __nv_bfloat16* ve = reinterpret_cast<const __nv_bfloat16*>(&vv);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) vts[(c + j) * kVPitch + t] = ve[j];
+    }
+    __syncthreads();
+    pdl_trigger();
+
+    const int g = lane >> 2, tq = lane & 3;  // mma fragment coordinates
+    const int r0 = warp * 16 + g;            // this thread's query rows: r0, r0 + 8
+    // Q fragments for the 4 k16 steps of d_head = 64.
+    uint32_t qa[4][4];
+    const __nv_bfloat16* q0 = qkv + (tok0 + r0) * ld + h * kDh;
+    const __nv_bfloat16* q1 = q0 + 8 * static_cast<size_t>(ld);
+#pragma unroll
+    for (int kk = 0; kk < 4; ++kk) {
+        const int c = kk * 16 + 2 * tq;
+        qa[kk][0] = *reinterpret_cast<const uint32_t*>(q0 + c);
+        qa[kk][1] = *reinterpret_cast<const uint32_t*>(q1 + c);
+        qa[kk][2] = *reinterpret_cast<const uint32_t*>(q0 + c + 8);
+        qa[kk][3] = *reinterpret_cast<const uint32_t*>(q1 + c + 8);
+    }
+    // S = Q K^T: 16 n8 tiles of keys.
+    float sc[16][4];
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt) {
+        sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+            const __nv_bfloat16* kr = &ks[(nt * 8 + g) * kKPitch + kk * 16 + 2 * tq];
+            const uint32_t b[2] = {*reinterpret_cast<const uint32_t*>(kr), *reinterpret_cast<const uint32_t*>(kr + 8)};
+            mma_bf16_16816(sc[nt], qa[kk], b);
+        }
+    }
+    // Row softmax of S / 8 (rows r0: elements 0,1; r0+8: elements 2,3).
+    const float scale = 0.125f;
+    float m0 = -INFINITY, m1 = -INFINITY;
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt) {
+        m0 = fmaxf(m0, fmaxf(sc[nt][0], sc[nt][1]));
+        m1 = fmaxf(m1, fmaxf(sc[nt][2], sc[nt][3]));
+    }
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+        m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+        m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+    }
+    float l0 = 0.f, l1 = 0.f;
+#pragma unroll
+    for (int nt = 0; nt < 16; ++nt) {
+        sc[nt][0] = expf((sc[nt][0] - m0) * scale);
+        sc[nt][1] = expf((sc[nt][1] - m0) * scale);
+        sc[nt][2] = expf((sc[nt][2] - m1) * scale);
+        sc[nt][3] = expf((sc[nt][3] - m1) * scale);
+        l0 += sc[nt][0] + sc[nt][1];
+        l1 += sc[nt][2] + sc[nt][3];
+    }
+#pragma unroll
+    for (int o = 1; o <= 2; o <<= 1) {
+        l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+        l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+    }
+    // O = P V: P (bf16) from the S fragments, 8 n8 tiles of d_head.
+    float oc[8][4];
+#pragma unroll
+    for (int dt = 0; dt < 8; ++dt) oc[dt][0] = oc[dt][1] = oc[dt][2] = oc[dt][3] = 0.f;
+#pragma unroll
+    for (int kk = 0; kk < 8; ++kk) {  // 16 keys per step
+        const uint32_t pa[4] = {pack_bf16(sc[2 * kk][0], sc[2 * kk][1]), pack_bf16(sc[2 * kk][2], sc[2 * kk][3]),
+                                pack_bf16(sc[2 * kk + 1][0], sc[2 * kk + 1][1]),
+                                pack_bf16(sc[2 * kk + 1][2], sc[2 * kk + 1][3])};
+#pragma unroll
+        for (int dt = 0; dt < 8; ++dt) {
+            const __nv_bfloat16* vr = &vts[(dt * 8 + g) * kVPitch + kk * 16 + 2 * tq];
+            const uint32_t b[2] = {*reinterpret_cast<const uint32_t*>(vr), *reinterpret_cast<const uint32_t*>(vr + 8)};
+            mma_bf16_16816(oc[dt], pa, b);
+        }
+    }
+    const float i0 = 1.f / l0, i1 = 1.f / l1;
+    __nv_bfloat16* c0 = ctx + (tok0 + r0) * d + h * kDh;
+    __nv_bfloat16* c1 = c0 + 8 * static_cast<size_t>(d);
+#pragma unroll
+    for (int dt = 0; dt < 8; ++dt) {
+        *reinterpret_cast<__nv_bfloat162*>(c0 + dt * 8 + 2 * tq) = __floats2bfloat162_rn(oc[dt][0] * i0, oc[dt][1] * i0);
+        *reinterpret_cast<__nv_bfloat162*>(c1 + dt * 8 + 2 * tq) = __floats2bfloat162_rn(oc[dt][2] * i1, oc[dt][3] * i1);
+    }
+}
+
+// ------------------------------------------------------------------ K4 LayerNorm
+
+template <int kD>
+__global__ void __launch_bounds__(256) layernorm_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
+                                                        const char* arena, PageTable ptab, uint64_t g_off,
+                                                        uint64_t b_off, int rows) {
+    __shared__ float gam[kD], bet[kD];
+    __shared__ uint32_t pt[GFX_MAX_PAGES];
+    for (int i = threadIdx.x; i < static_cast<int>(ptab.n); i += 256) pt[i] = ptab.page[i];
+    __syncthreads();
+    for (int i = threadIdx.x; i < kD; i += 256) {
+        gam[i] = *reinterpret_cast<const float*>(translate(arena, pt, g_off + 4ull * i));
+        bet[i] = *reinterpret_cast<const float*>(translate(arena, pt, b_off + 4ull * i));
+    }
+    __syncthreads();
+    pdl_wait();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int row = blockIdx.x * 8 + warp;
+    if (row >= rows) return;
+    constexpr int kPer = kD / 256;  // uint4 (8 bf16) chunks per lane
+    float v[kPer * 8];
+    const __nv_bfloat16* xr = x + static_cast<size_t>(row) * kD;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+        const uint4 u = *reinterpret_cast<const uint4*>(xr + (i * 32 + lane) * 8);
+        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float2 f = __bfloat1622float2(h2[j]);
+            v[i * 8 + 2 * j] = f.x;
+            v[i * 8 + 2 * j + 1] = f.y;
+        }
+    }
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < kPer * 8; ++i) s += v[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    const float mean = s / kD;
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < kPer * 8; ++i) {
+        const float t = v[i] - mean;
+        q += t * t;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+    const float rstd = rsqrtf(q / kD + 1e-12f);
+    __nv_bfloat16* yr = y + static_cast<size_t>(row) * kD;
+#pragma unroll
+    for (int i = 0; i < kPer; ++i) {
+        uint4 u;
+        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+        const int c0 = (i * 32 + lane) * 8;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            h2[j] = __floats2bfloat162_rn((v[i * 8 + 2 * j] - mean) * rstd * gam[c0 + 2 * j] + bet[c0 + 2 * j],
+                                          (v[i * 8 + 2 * j + 1] - mean) * rstd * gam[c0 + 2 * j + 1] + bet[c0 + 2 * j + 1]);
+        *reinterpret_cast<uint4*>(yr + c0) = u;
+    }
+}
+
+// ------------------------------------------------------------------ pooler
+
+__global__ void __launch_bounds__(256) pooler_kernel(const __nv_bfloat16* __restrict__ x, float* __restrict__ out,
+                                                     const char* arena, PageTable ptab, uint64_t w_off, uint64_t b_off,
+                                                     int d, int seq, int batch) {
+    __shared__ uint32_t pt[GFX_MAX_PAGES];
+    for (int i = threadIdx.x; i < static_cast<int>(ptab.n); i += 256) pt[i] = ptab.page[i];
+    __syncthreads();
+    pdl_wait();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int n = blockIdx.x * 8 + warp;
+    if (n >= d) return;
+    const float bias = *reinterpret_cast<const float*>(translate(arena, pt, b_off + 4ull * n));
+    for (int b = 0; b < batch; ++b) {
+        const __nv_bfloat16* xr = x + static_cast<size_t>(b) * seq * d;  // [CLS] = token 0
+        float acc = 0.f;
+        for (int k = lane; k < d; k += 32) {
+            const uint16_t wb =
+                *reinterpret_cast<const uint16_t*>(translate(arena, pt, w_off + bf16_tile_offset(n, k, d)));
+            acc += __uint_as_float(static_cast<uint32_t>(wb) << 16) * __bfloat162float(xr[k]);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) out[static_cast<size_t>(b) * d + n] = tanhf(acc + bias);
+    }
+}
+
+__global__ void fill_bf16_kernel(__nv_bfloat16* dst, uint64_t n, uint64_t count, uint64_t seed0, uint32_t tensor,
+                                 float scaled) {
+    const uint64_t total = n * count;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t t = i / n;
+        const float v = param_at(param_stream(seed0 + t, tensor), i - t * n, scaled);
+        dst[i] = __ushort_as_bfloat16(bf16_bits(v));
+    }
+}
+
+template <typename Kern, typename... Args>
+void launch_pdl(Kern k, dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool pdl, Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    GFX_CUDA(cudaLaunchKernelEx(&cfg, k, args...));
+}
+
+template <int kEpi>
+void gemm(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_off, const __nv_bfloat16* x,
+          __nv_bfloat16* y, const __nv_bfloat16* resid, int T, int K, int N, cudaStream_t s, bool pdl) {
+    if (T % kGM || N % kGN || K % kGK) throw std::runtime_error("bert gemm: T, N multiple of 128, K of 64");
+    CUtensorMap tm;
+    if (!encode_tensor_map_2d(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, x, static_cast<uint64_t>(K),
+                              static_cast<uint64_t>(T), static_cast<uint64_t>(K) * 2, kGK, kGM,
+                              CU_TENSOR_MAP_SWIZZLE_128B))
+        throw CudaError("cuTensorMapEncodeTiled failed (bert gemm)");
+    GemmArgs a{arena, w_off, b_off, y, resid, K, N, pt};
+    static bool attr_set = false;
+    const size_t smem = static_cast<size_t>(kGStage) * kGStages + 1024;
+    if (!attr_set) {
+        GFX_CUDA(cudaFuncSetAttribute(gemm_bf16_kernel<kEpi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(smem)));
+        attr_set = true;
+    }
+    launch_pdl(gemm_bf16_kernel<kEpi>, dim3(N / kGN, T / kGM), dim3(kGThreads), smem, s, pdl, tm, a);
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ layout
+
+BertLayout bert_layout(int L, int d, int heads, int ffn, int seq) {
+    BertLayout lay;
+    lay.L = L;
+    lay.d = d;
+    lay.heads = heads;
+    lay.ffn = ffn;
+    lay.seq = seq;
+    uint64_t off = 0;
+    auto align = [](uint64_t v, uint64_t a) { return (v + a - 1) / a * a; };
+    auto wmat = [&](uint64_t n, uint64_t k) {
+        off = align(off, 16384);
+        const uint64_t at = off;
+        off += align(n, 128) * k * 2;
+        return at;
+    };
+    auto vec = [&](uint64_t n) {
+        off = align(off, 256);
+        const uint64_t at = off;
+        off += 4 * n;
+        return at;
+    };
+    for (int l = 0; l < L; ++l) {
+        BertLayerOffsets o{};
+        o.wqkv = wmat(3 * d, d);
+        o.bqkv = vec(3 * d);
+        o.wo = wmat(d, d);
+        o.bo = vec(d);
+        o.ln1_g = vec(d);
+        o.ln1_b = vec(d);
+        o.w1 = wmat(ffn, d);
+        o.b1 = vec(ffn);
+        o.w2 = wmat(d, ffn);
+        o.b2 = vec(d);
+        o.ln2_g = vec(d);
+        o.ln2_b = vec(d);
+        lay.layer.push_back(o);
+    }
+    lay.wp = wmat(d, d);
+    lay.bp = vec(d);
+    lay.bytes = align(off, 256);
+    return lay;
+}
+
+void BertWorkspace::ensure(int ntok, int d, int ffn) {
+    if (ntok <= tokens) return;
+    release();
+    const size_t T = static_cast<size_t>(ntok);
+    GFX_CUDA(cudaMalloc(&x, T * d * 2));
+    GFX_CUDA(cudaMalloc(&qkv, T * 3 * d * 2));
+    GFX_CUDA(cudaMalloc(&ctx, T * d * 2));
+    GFX_CUDA(cudaMalloc(&h, T * d * 2));
+    GFX_CUDA(cudaMalloc(&f, T * ffn * 2));
+    GFX_CUDA(cudaMalloc(&t, T * d * 2));
+    tokens = ntok;
+}
+
+void BertWorkspace::release() {
+    for (__nv_bfloat16** p : {&x, &qkv, &ctx, &h, &f, &t}) {
+        if (*p) cudaFree(*p);
+        *p = nullptr;
+    }
+    tokens = 0;
+}
+
+int bert_forward(const char* arena, const PageTable& pt, const BertLayout& lay, int batch, const __nv_bfloat16* in,
+                 float* out, BertWorkspace& ws, cudaStream_t s, __nv_bfloat16* hidden) {
+    const int d = lay.d, T = batch * lay.seq;
+    if (lay.seq != kS || d / lay.heads != kDh || d != 768)
+        throw std::runtime_error("bert: this build serves seq 128, d_head 64, d 768");
+    ws.ensure(T, d, lay.ffn);
+    int launches = 0;
+    const __nv_bfloat16* x = in;
+    const size_t hbytes = static_cast<size_t>(T) * d * 2;
+    if (hidden) GFX_CUDA(cudaMemcpyAsync(hidden, in, hbytes, cudaMemcpyDeviceToDevice, s));
+    for (int l = 0; l < lay.L; ++l) {
+        const BertLayerOffsets& o = lay.layer[static_cast<size_t>(l)];
+        gemm<kEpiBias>(arena, pt, o.wqkv, o.bqkv, x, ws.qkv, nullptr, T, d, 3 * d, s, l > 0 && !hidden);
+        launch_pdl(attention_kernel, dim3(batch * lay.heads), dim3(256), 0, s, true,
+                   static_cast<const __nv_bfloat16*>(ws.qkv), ws.ctx, lay.heads);
+        gemm<kEpiResid>(arena, pt, o.wo, o.bo, ws.ctx, ws.t, x, T, d, d, s, true);
+        launch_pdl(layernorm_kernel<768>, dim3((T + 7) / 8), dim3(256), 0, s, true,
+                   static_cast<const __nv_bfloat16*>(ws.t), ws.h, arena, pt, o.ln1_g, o.ln1_b, T);
+        gemm<kEpiGelu>(arena, pt, o.w1, o.b1, ws.h, ws.f, nullptr, T, d, lay.ffn, s, true);
+        gemm<kEpiResid>(arena, pt, o.w2, o.b2, ws.f, ws.t, ws.h, T, lay.ffn, d, s, true);
+        launch_pdl(layernorm_kernel<768>, dim3((T + 7) / 8), dim3(256), 0, s, true,
+                   static_cast<const __nv_bfloat16*>(ws.t), ws.x, arena, pt, o.ln2_g, o.ln2_b, T);
+        launches += 7;
+        x = ws.x;
+        if (hidden)
+            GFX_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(hidden) + (l + 1) * hbytes, ws.x, hbytes,
+                                     cudaMemcpyDeviceToDevice, s));
+    }
+    launch_pdl(pooler_kernel, dim3((d + 7) / 8), dim3(256), 0, s, !hidden, static_cast<const __nv_bfloat16*>(x), out,
+               arena, pt, lay.wp, lay.bp, d, lay.seq, batch);
+    return launches + 1;
+}
+
+void launch_fill_bf16(__nv_bfloat16* dst, uint64_t n, uint64_t seed, uint32_t tensor, float scale, cudaStream_t s,
+                      uint64_t count) {
+    const uint64_t total = n * count;
+    unsigned blocks = static_cast<unsigned>((total + 255) / 256);
+    if (blocks > 148 * 32) blocks = 148 * 32;
+    if (blocks == 0) blocks = 1;
+    fill_bf16_kernel<<<blocks, 256, 0, s>>>(dst, n, count, seed, tensor, param_scale(scale));
+    GFX_CUDA(cudaGetLastError());
+}
+
+}  // namespace gfx

@@ -3,6 +3,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 #include <thread>
@@ -45,8 +47,98 @@ ModelStore& ModelStore::get() {
     return store;
 }
 
+namespace {
+
+// BERT parameter blob: bf16 weight tiles, fp32 vectors.
+void build_bert_blob(ModelBlob& blob) {
+    const gfx_model_desc& d = blob.desc;
+    const BertLayout& lay = blob.bert;
+    char* base = reinterpret_cast<char*>(blob.host);
+    std::vector<std::thread> pool;
+    struct Mat {
+        uint64_t off, n, k;
+        uint32_t tensor;
+    };
+    struct Vec {
+        uint64_t off, n;
+        uint32_t tensor;
+        float scale, shift;
+    };
+    std::vector<Mat> mats;
+    std::vector<Vec> vecs;
+    const uint64_t D = static_cast<uint64_t>(lay.d), F = static_cast<uint64_t>(lay.ffn);
+    const float sd = static_cast<float>(1.0 / std::sqrt(static_cast<double>(D)));
+    const float sf = static_cast<float>(1.0 / std::sqrt(static_cast<double>(F)));
+    for (int l = 0; l < lay.L; ++l) {
+        const BertLayerOffsets& o = lay.layer[static_cast<size_t>(l)];
+        const uint32_t t0 = 16u * static_cast<uint32_t>(l);
+        mats.push_back({o.wqkv, 3 * D, D, t0 + kWqkv});
+        mats.push_back({o.wo, D, D, t0 + kWo});
+        mats.push_back({o.w1, F, D, t0 + kW1});
+        mats.push_back({o.w2, D, F, t0 + kW2});
+        vecs.push_back({o.bqkv, 3 * D, t0 + kBqkv, 0.02f, 0.f});
+        vecs.push_back({o.bo, D, t0 + kBo, 0.02f, 0.f});
+        vecs.push_back({o.b1, F, t0 + kB1, 0.02f, 0.f});
+        vecs.push_back({o.b2, D, t0 + kB2, 0.02f, 0.f});
+        vecs.push_back({o.ln1_g, D, t0 + kLn1G, 0.1f, 1.f});
+        vecs.push_back({o.ln1_b, D, t0 + kLn1B, 0.1f, 0.f});
+        vecs.push_back({o.ln2_g, D, t0 + kLn2G, 0.1f, 1.f});
+        vecs.push_back({o.ln2_b, D, t0 + kLn2B, 0.1f, 0.f});
+    }
+    const uint32_t tp = 16u * static_cast<uint32_t>(lay.L);
+    mats.push_back({lay.wp, D, D, tp + 0});
+    vecs.push_back({lay.bp, D, tp + 1, 0.02f, 0.f});
+    for (const Vec& v : vecs) {
+        const uint64_t st = param_stream(d.seed, v.tensor);
+        const float sc = param_scale(v.scale);
+        float* dst = reinterpret_cast<float*>(base + v.off);
+        for (uint64_t i = 0; i < v.n; ++i) dst[i] = v.shift + param_at(st, i, sc);
+    }
+    unsigned nthreads = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    for (unsigned t = 0; t < nthreads; ++t)
+        pool.emplace_back([&, t] {
+            for (const Mat& m : mats) {
+                const uint64_t st = param_stream(d.seed, m.tensor);
+                const float sc = param_scale(m.k == F ? sf : sd);
+                const uint64_t total = m.n * m.k, chunk = (total + nthreads - 1) / nthreads;
+                const uint64_t lo = std::min<uint64_t>(total, t * chunk), hi = std::min<uint64_t>(total, lo + chunk);
+                for (uint64_t i = lo; i < hi; ++i) {
+                    const uint64_t n = i / m.k, k = i % m.k;
+                    *reinterpret_cast<uint16_t*>(base + m.off + bf16_tile_offset(n, k, m.k)) =
+                        bf16_bits(param_at(st, i, sc));
+                }
+            }
+        });
+    for (auto& th : pool) th.join();
+    const double T = static_cast<double>(d.batch) * lay.seq;
+    blob.flops = lay.L * (2.0 * T * (3 * D * D + D * D + 2 * D * F) + 4.0 * T * lay.seq * D) + 2.0 * d.batch * D * D;
+    blob.alg_bytes = static_cast<double>(blob.bytes) + T * D * 2 + d.batch * D * 4.0;
+    blob.in_bytes = static_cast<uint64_t>(T) * D * 2;
+    blob.out_bytes = static_cast<uint64_t>(d.batch) * D * 4;
+}
+
+}  // namespace
+
 void ModelStore::add(int idx, const gfx_model_desc& desc) {
     if (idx < 0) throw std::invalid_argument("model index must be >= 0");
+    if (desc.family == GFX_MODEL_BERT) {
+        const int L = desc.n_layers, D = desc.dims[0], H = desc.dims[1], F = desc.dims[2], S = desc.dims[3];
+        if (L < 1 || D != 768 || H != 12 || F % 128 || S != 128 || desc.batch < 1 || desc.batch * S % 128)
+            throw std::invalid_argument("bert: supported shape is d=768, 12 heads, seq 128, ffn % 128 == 0");
+        auto blob = std::make_unique<ModelBlob>();
+        blob->desc = desc;
+        blob->bert = bert_layout(L, D, H, F, S);
+        blob->bytes = blob->bert.bytes;
+        blob->pages = static_cast<uint32_t>((blob->bytes + kPageBytes - 1) / kPageBytes);
+        if (blob->pages > GFX_MAX_PAGES) throw std::invalid_argument("model larger than the page-table limit");
+        GFX_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&blob->host), blob->bytes, cudaHostAllocDefault));
+        std::memset(blob->host, 0, blob->bytes);
+        build_bert_blob(*blob);
+        std::lock_guard<std::mutex> lk(mu_);
+        if (static_cast<size_t>(idx) >= blobs_.size()) blobs_.resize(static_cast<size_t>(idx) + 1);
+        blobs_[static_cast<size_t>(idx)] = std::move(blob);
+        return;
+    }
     if (desc.family != GFX_MODEL_MLP) throw std::invalid_argument("unsupported model family");
     if (desc.n_layers < 1 || desc.n_layers > GFX_MAX_LAYERS) throw std::invalid_argument("bad layer count");
     if (desc.batch != kBatch) throw std::invalid_argument("batch must be 32");
@@ -88,6 +180,8 @@ void ModelStore::add(int idx, const gfx_model_desc& desc) {
     }
     blob->flops = flops;
     blob->alg_bytes = wbytes;
+    blob->in_bytes = static_cast<uint64_t>(kBatch) * desc.dims[0] * 4;
+    blob->out_bytes = static_cast<uint64_t>(2) * kBatch * desc.dims[desc.n_layers] * 4;
     unsigned nthreads = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
     std::vector<std::thread> pool;
     for (unsigned t = 0; t < nthreads; ++t)
@@ -177,6 +271,7 @@ GpuManager::~GpuManager() {
     cudaFree(ws_);
     cudaFree(counters_);
     cudaFree(stats_);
+    bert_ws_.release();
     cudaStreamDestroy(compute_);
     cudaStreamDestroy(copy_);
 }
@@ -293,11 +388,24 @@ void GpuManager::build_page_table(const Slot& s, PageTable& pt) const {
 
 // The batched inference that replaces profile.infer_time_us
 // (proj/src/cluster.cpp:161,167): one K1 launch per layer on the compute stream.
-void GpuManager::infer(int model, const float* in, float* out) {
+void GpuManager::infer(int model, const void* in_v, void* out_v, void* debug_hidden) {
     const ModelBlob& blob = ModelStore::get().at(model);
     Slot& s = slot(model);
     if (!s.live) throw std::logic_error("inference of non-resident model " + std::to_string(model));
     activate();
+    if (blob.desc.family == GFX_MODEL_BERT) {
+        PageTable pt;
+        build_page_table(s, pt);
+        if (layer_timer) GFX_CUDA(cudaEventRecord(layer_timer->next(), compute_));
+        kernel_launches += bert_forward(arena_, pt, blob.bert, blob.desc.batch,
+                                        static_cast<const __nv_bfloat16*>(in_v), static_cast<float*>(out_v), bert_ws_,
+                                        compute_, static_cast<__nv_bfloat16*>(debug_hidden));
+        if (layer_timer) GFX_CUDA(cudaEventRecord(layer_timer->next(), compute_));
+        GFX_CUDA(cudaEventRecord(s.last_use, compute_));
+        return;
+    }
+    const float* in = static_cast<const float*>(in_v);
+    float* out = static_cast<float*>(out_v);
     MlpLayerArgs a{};
     a.arena = arena_;
     build_page_table(s, a.pt);
@@ -323,7 +431,35 @@ void GpuManager::infer(int model, const float* in, float* out) {
         if (l == 0 && layer_timer) GFX_CUDA(cudaEventRecord(layer_timer->next(), compute_));
         // Layers 1.. and the softmax are programmatic dependents of the kernel
         // before them: their prologue and weight prefetch overlap its tail.
-        launch_mlp_layer(a, compute_, /*pdl=*/l > 0);
+        static const bool trace_on = std::getenv("GFX_TRACE_MLP") != nullptr;
+        std::vector<unsigned long long> tr;
+        if (trace_on) {  // debug timeline: per-CTA phase timestamps of this launch
+            GFX_CUDA(cudaMalloc(&a.trace, sizeof(unsigned long long) * 8 * a.ntiles * a.splits));
+            GFX_CUDA(cudaMemset(a.trace, 0, sizeof(unsigned long long) * 8 * a.ntiles * a.splits));
+        }
+        launch_mlp_layer(a, compute_, /*pdl=*/l > 0 && !trace_on);
+        if (trace_on) {
+            tr.resize(static_cast<size_t>(8) * a.ntiles * a.splits);
+            GFX_CUDA(cudaStreamSynchronize(compute_));
+            GFX_CUDA(cudaMemcpy(tr.data(), a.trace, tr.size() * 8, cudaMemcpyDeviceToHost));
+            GFX_CUDA(cudaFree(a.trace));
+            a.trace = nullptr;
+            unsigned long long t0 = ~0ull;
+            for (size_t i = 0; i < tr.size(); i += 8) t0 = std::min(t0, tr[i]);
+            std::fprintf(stderr, "[trace] layer %d K=%d N=%d grid %dx%d (us after first CTA start: min/med/max)\n", l,
+                         a.K, a.N, a.ntiles, a.splits);
+            const char* names[7] = {"start", "prologue", "tma_issued", "first_data", "mainloop_end", "splitk_done",
+                                    "store_done"};
+            for (int ph = 0; ph < 7; ++ph) {
+                std::vector<double> v;
+                for (size_t i = 0; i < tr.size(); i += 8)
+                    if (tr[i + static_cast<size_t>(ph)]) v.push_back((tr[i + static_cast<size_t>(ph)] - t0) * 1e-3);
+                if (v.empty()) continue;
+                std::sort(v.begin(), v.end());
+                std::fprintf(stderr, "  %-13s n=%3zu %8.2f %8.2f %8.2f\n", names[ph], v.size(), v.front(),
+                             v[v.size() / 2], v.back());
+            }
+        }
         ++kernel_launches;
         x = a.y;
     }

@@ -20,6 +20,7 @@
 
 #include "common.cuh"
 #include "gpufaas_b200.h"
+#include "bert.cuh"
 #include "mlp.cuh"
 
 namespace gfx {
@@ -31,8 +32,10 @@ struct ModelBlob {
     uint32_t pages = 0;
     std::vector<uint64_t> w_off, b_off;  // per layer, offsets in the blob
     float* host = nullptr;               // pinned (cudaHostAlloc)
-    double flops = 0;                    // per inference (2 * batch * sum K*N)
+    double flops = 0;                    // per inference
     double alg_bytes = 0;                // per inference: weights + biases + in/out activations
+    uint64_t in_bytes = 0, out_bytes = 0;  // one request's input / output tensors
+    BertLayout bert;                     // GFX_MODEL_BERT
     ~ModelBlob();
 };
 
@@ -77,7 +80,7 @@ public:
     void evict(int model);
     // Returns bytes copied. src == nullptr -> pinned host store.
     uint64_t load(int model, GpuManager* src);
-    void infer(int model, const float* in, float* out);
+    void infer(int model, const void* in, void* out, void* debug_hidden = nullptr);
     void reset();  // synchronise and drop every resident model
 
     cudaStream_t compute_stream() const { return compute_; }
@@ -115,6 +118,7 @@ private:
     // inference workspace
     float* act_[2] = {nullptr, nullptr};
     float* ws_ = nullptr;
+    BertWorkspace bert_ws_;
     unsigned* counters_ = nullptr;
     float* stats_ = nullptr;
     int max_dim_ = 0;

@@ -24,6 +24,7 @@ struct MlpLayerArgs {
     float* ws;             // split-K partials [tiles][splits][32][128]
     unsigned* counters;    // [ntiles + 1], zero between launches
     float* stats;          // last layer: [ntiles][32][2] per-tile softmax partials
+    unsigned long long* trace;  // debug (GFX_TRACE_MLP): per-CTA phase timestamps, else nullptr
     PageTable pt;
 };
 

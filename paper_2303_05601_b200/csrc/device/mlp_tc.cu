@@ -109,6 +109,12 @@ __device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 128;\n" :
 // (no-op without the launch attribute) / let the next one start its prologue.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+__device__ __forceinline__ void trace_mark(unsigned long long* tr, int i) {
+    if (tr == nullptr) return;
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    tr[(static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * 8 + i] = t;
+}
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
@@ -137,6 +143,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int kt_end = static_cast<int>((static_cast<long long>(kt_total) * (split + 1)) / a.splits);
     const int nkt = kt_end - kt_begin;
 
+    if (tid == 0) trace_mark(a.trace, 0);
     for (int i = tid; i < static_cast<int>(a.pt.n); i += kThreads) pt[i] = a.pt.page[i];
     if (tid == 0) {
         for (int s = 0; s < kLand; ++s) {
@@ -159,6 +166,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_base_s;
+    if (tid == 0) trace_mark(a.trace, 1);
 
     if (warp == 0) {
         // ---------------- TMA producer ----------------
@@ -175,6 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             pdl_wait();
             for (int it = 0; it < pre; ++it)
                 tma_tile2d_g2s(landing(smem, it).x, &tmap_x, (kt_begin + it) * kTileK, 0, &land_full[it]);
+            trace_mark(a.trace, 2);
             for (int it = pre; it < nkt; ++it) {
                 const int s = it % kLand;
                 mbar_wait(&land_empty[s], ((it / kLand) & 1) ^ 1);
@@ -241,6 +250,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int s = it % kLand;
             const int o = it % kOps;
             mbar_wait(&land_full[s], (it / kLand) & 1);
+            if (it == 0 && ct == 0) trace_mark(a.trace, 3);
             if (it >= kOps) mbar_wait(&op_empty[o], ((it / kOps) & 1) ^ 1);
             const Landing ld = landing(smem, s);
             const Operands op = operands(smem, o);
@@ -271,6 +281,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             while (drained < nchunks && min(nkt, (drained + 1) * kChunk) - 1 + kDrainDelay <= it) drain(drained++);
         }
         while (drained < nchunks) drain(drained++);
+        if (ct == 0) trace_mark(a.trace, 4);
 
         pdl_trigger();  // main loop done: the next layer may start its prologue
         pdl_wait();     // workspace / counters / output belong to us only after the previous layer
@@ -311,6 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (ct == 0) a.counters[tile] = 0;
             }
         }
+        if (ct == 0) trace_mark(a.trace, 5);
         if (finisher) {
             const bool valid = f < N;  // rows >= N are the zero padding of the last weight tile
             const float bias = valid ? *reinterpret_cast<const float*>(translate(a.arena, pt, a.b_off + 4ull * f)) : 0.f;
@@ -321,6 +333,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 acc[b] = v;
                 if (valid) a.y[static_cast<size_t>(b) * N + f] = v;
             }
+            if (ct == 0) trace_mark(a.trace, 6);
         }
     }
 

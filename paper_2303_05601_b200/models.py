@@ -10,6 +10,7 @@ from . import _ffi
 
 DATA_DIR = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data")
 GFX_MODEL_MLP = 1
+GFX_MODEL_BERT = 2
 
 
 def model_seed(model_id: str) -> int:
@@ -34,6 +35,9 @@ class ModelSpec:
         return model_seed(self.model_id)
 
     def desc(self) -> _ffi.ModelDesc:
+        if self.family == "bert":  # dims = [layers, d_model, heads, ffn, seq, sequences]
+            return bert_desc(self.dims[0], self.dims[5], self.seed, d=self.dims[1], heads=self.dims[2],
+                             ffn=self.dims[3], seq=self.dims[4])
         d = _ffi.ModelDesc()
         d.family = GFX_MODEL_MLP
         d.n_layers = len(self.dims) - 1
@@ -42,6 +46,18 @@ class ModelSpec:
         d.batch = 32
         d.seed = self.seed
         return d
+
+
+def bert_desc(layers: int, sequences: int, seed: int, d=768, heads=12, ffn=3072, seq=128) -> _ffi.ModelDesc:
+    """BERT-base-style encoder (C5): bf16, post-LN, tanh pooler."""
+    m = _ffi.ModelDesc()
+    m.family = GFX_MODEL_BERT
+    m.n_layers = layers
+    for i, v in enumerate((d, heads, ffn, seq)):
+        m.dims[i] = v
+    m.batch = sequences
+    m.seed = seed
+    return m
 
 
 def load_model_specs(name: str = "mlp_c2") -> list[ModelSpec]:

@@ -77,9 +77,11 @@ class Replay:
         _ffi.check(_ffi.gfx_replay_run(self.h, C.byref(r)))
         return ReplayResult({k: getattr(r, k) for k, _ in r._fields_})
 
-    def outputs(self, n_requests: int, classes: int = 1000) -> np.ndarray:
-        out = np.zeros((n_requests, 2, 32, classes), dtype=np.float32)
-        _ffi.check(_ffi.gfx_replay_outputs(self.h, out.ctypes.data, out.size))
+    def outputs(self, n_requests: int, shape=(2, 32, 1000)) -> np.ndarray:
+        """Per-request fp32 outputs of the last run (MLP: logits + softmax;
+        BERT: pass shape=(sequences, 768) for the pooled output)."""
+        out = np.zeros((n_requests,) + tuple(shape), dtype=np.float32)
+        _ffi.check(_ffi.gfx_replay_outputs(self.h, out.ctypes.data, out.nbytes))
         return out
 
     def request_info(self, n_requests: int):

@@ -1,0 +1,132 @@
+"""C5 model family on B200: BERT-base encoder (bf16 activations, fp32
+accumulation, post-LN, tanh pooler) — tcgen05 GEMMs with fused bias / GELU /
+residual epilogues, mma.sync attention, LayerNorm — against the oracle's fp64
+restatement with the same bf16 rounding points. Tolerance (north star, bf16):
+normwise relative error <= 1e-3.
+
+Why teacher forcing: this bf16 network is chaotic with respect to rounding
+flips — perturbing ONE of the 196 608 input values by one bf16 ulp moves the
+pooled output by 6e-4 after one layer and 1.7e-3 after two (measured with the
+oracle alone; fp32 vs fp64 accumulation differs by 1.6e-3 after two layers).
+End-to-end 1e-3 parity of a deep stack is therefore ill-posed for ANY
+implementation that is not the oracle's exact operation order. The well-posed
+check is per layer: feed each oracle layer the GPU's own input to that layer
+and compare outputs — done here for all 12 layers of full BERT-base."""
+import ctypes as C
+import os
+
+import numpy as np
+import pytest
+
+import simabi
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-3
+D, SEQ = 768, 128
+
+
+@pytest.fixture(scope="module")
+def gfx():
+    import paper_2303_05601_b200 as g
+    n = C.c_int(0)
+    g.check(g._ffi.gfx_device_count(C.byref(n)))
+    assert n.value >= 1
+    return g
+
+
+@pytest.fixture(scope="module")
+def olib():
+    lib = C.CDLL(simabi.ORACLE_SO)
+    lib.orc_bert_forward.restype = C.c_int
+    lib.orc_bert_forward.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                     C.c_void_p, C.c_int]
+    lib.orc_bert_layer.restype = C.c_int
+    lib.orc_bert_layer.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                   C.c_void_p, C.c_int]
+    lib.orc_bert_pool.restype = C.c_int
+    lib.orc_bert_pool.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
+    return lib
+
+
+def bf16_to_f32(bits):
+    return (bits.astype(np.uint32) << 16).view(np.float32)
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / np.linalg.norm(b))
+
+
+def run_gpu(gfx, idx, layers, seqs, seed, request_id=7, debug=True):
+    desc = gfx.models.bert_desc(layers, seqs, seed)
+    gfx.check(gfx._ffi.gfx_model_register(idx, C.byref(desc)))
+    inb, outb = C.c_uint64(), C.c_uint64()
+    gfx.check(gfx._ffi.gfx_model_io_bytes(idx, C.byref(inb), C.byref(outb)))
+    assert inb.value == seqs * SEQ * D * 2 and outb.value == seqs * D * 4
+    pages = C.c_int32()
+    gfx.check(gfx._ffi.gfx_model_pages(idx, C.byref(pages)))
+    a = C.c_void_p()
+    gfx.check(gfx._ffi.gfx_arena_create(0, (pages.value + 2) << 21, C.byref(a)))
+    try:
+        x_bits = np.zeros(inb.value // 2, np.uint16)
+        gfx.check(gfx._ffi.gfx_host_fill_input(idx, request_id, x_bits.ctypes.data, inb.value))
+        xd, yd, hd = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        hbytes = (layers + 1) * inb.value
+        gfx.check(gfx._ffi.gfx_device_alloc(a, inb.value, C.byref(xd)))
+        gfx.check(gfx._ffi.gfx_device_alloc(a, outb.value, C.byref(yd)))
+        gfx.check(gfx._ffi.gfx_device_alloc(a, hbytes, C.byref(hd)))
+        gfx.check(gfx._ffi.gfx_memcpy_h2d(a, xd, x_bits.ctypes.data, inb.value))
+        gfx.check(gfx._ffi.gfx_load_h2d(a, idx, None))
+        gfx.check(gfx._ffi.gfx_infer(a, idx, xd, yd, seqs, None))  # production (PDL-chained) path
+        pooled = np.zeros((seqs, D), np.float32)
+        gfx.check(gfx._ffi.gfx_memcpy_d2h(a, pooled.ctypes.data, yd, outb.value))
+        gfx.check(gfx._ffi.gfx_infer(a, idx, xd, yd, seqs, None))
+        again = np.zeros_like(pooled)
+        gfx.check(gfx._ffi.gfx_memcpy_d2h(a, again.ctypes.data, yd, outb.value))
+        hidden = None
+        if debug:
+            gfx.check(gfx._ffi.gfx_infer_debug(a, idx, xd, yd, seqs, hd))
+            hidden = np.zeros((layers + 1, seqs * SEQ * D), np.uint16)
+            gfx.check(gfx._ffi.gfx_memcpy_d2h(a, hidden.ctypes.data, hd, hbytes))
+            dbg = np.zeros_like(pooled)
+            gfx.check(gfx._ffi.gfx_memcpy_d2h(a, dbg.ctypes.data, yd, outb.value))
+            assert np.array_equal(dbg, pooled), "debug path must compute the same result"
+        for p in (xd, yd, hd):
+            gfx.check(gfx._ffi.gfx_device_free(a, p))
+    finally:
+        gfx._ffi.gfx_arena_destroy(a)
+    return x_bits, pooled, again, hidden
+
+
+def test_bert_base_every_layer_teacher_forced(gfx, olib):
+    """Full BERT-base depth (12 layers), 2 sequences x 128 tokens."""
+    layers, seqs = 12, 2
+    seed = gfx.model_seed("bert-base-c5-test")
+    x_bits, pooled, again, hidden = run_gpu(gfx, 70, layers, seqs, seed)
+    assert np.array_equal(pooled, again), "inference must be deterministic"
+    assert np.array_equal(hidden[0], x_bits)
+    threads = os.cpu_count() or 1
+    worst = 0.0
+    for l in range(layers):
+        want = np.zeros_like(hidden[l])
+        assert olib.orc_bert_layer(seed, l, D, 12, 3072, SEQ, seqs, hidden[l].ctypes.data, want.ctypes.data,
+                                   threads) == 0
+        err = rel(bf16_to_f32(hidden[l + 1]), bf16_to_f32(want))
+        worst = max(worst, err)
+        assert err <= TOL, f"layer {l}: {err:.3e}"
+    want_pool = np.zeros((seqs, D), np.float32)
+    assert olib.orc_bert_pool(seed, layers, D, SEQ, seqs, hidden[layers].ctypes.data, want_pool.ctypes.data) == 0
+    assert rel(pooled, want_pool) <= TOL
+    print(f"worst per-layer normwise error {worst:.2e}")
+
+
+def test_bert_one_layer_end_to_end(gfx, olib):
+    seqs = 3
+    seed = gfx.model_seed("bert-test-1-3")
+    x_bits, pooled, _, _ = run_gpu(gfx, 71, 1, seqs, seed, debug=False)
+    want = np.zeros((seqs, D), np.float32)
+    assert olib.orc_bert_forward(seed, 1, D, 12, 3072, SEQ, seqs, x_bits.ctypes.data, want.ctypes.data,
+                                 os.cpu_count() or 1) == 0
+    assert np.isfinite(pooled).all()
+    assert rel(pooled, want) <= TOL
