@@ -293,6 +293,7 @@ def main():
     extras = {}
     if rank == 0 and not a.no_extras:
         extras = locality_extras(gfx, world)
+        extras.update(c5_extras(gfx, world, peaks))
     cpu = None
     if rank == 0 and not a.no_extras:
         v, desc, kind = cpu_reference_sample(cat, a.policy, 1, n_infer=2, gpus=G, rpm=325 * G)
@@ -364,6 +365,42 @@ def locality_extras(gfx, world):
     out["speedup_replay"] = round(out["lalbo3"]["replay_req_s"] / out["lb"]["replay_req_s"], 3)
     out["speedup_avg_latency"] = round(out["lb"]["sim_avg_latency_s"] / out["lalbo3"]["sim_avg_latency_s"], 3)
     return {"locality_vs_lb_1gpu_paper_regime": out}
+
+
+def c5_extras(gfx, world, peaks):
+    """BASELINE configs[4] (C5) on one B200: 20 BERT-base encoders (bf16, 12
+    layers, 32 x 128-token sequences per request, 164 MiB each), Zipf working
+    set of 20 functions, 325 req/min for 1 minute, LALBO3; HBM arena swept over
+    256/512/1024/2048 MiB. Reports replay throughput, hit rate and the achieved
+    tensor throughput of the inference (all kernels of a forward, CUDA-event
+    timed) against the measured bf16 peak."""
+    if world > 1:
+        return {}
+    specs = gfx.load_model_specs("bert_c5")
+    gfx.register_models(specs)  # catalog rows 0..19 now hold the BERT blobs
+    cat = gfx.catalog_text("bert_c5")
+    sweep = []
+    peak = peaks.get("bf16_tflops", 1590.0)
+    for arena in (256, 512, 1024, 2048):
+        cfg = gfx.sim_config(gpus=1, capacity_mb=float(arena), policy="lalbo3", working_set=20, minutes=1)
+        rep = gfx.Replay(cat, cfg, record_kernels=True)
+        rep.run()
+        rs = [rep.run() for _ in range(2)]
+        rep.close()
+        ms = sum(x.device_ms for x in rs) / len(rs)
+        r = rs[-1]
+        tf = r.mlp_flops / (r.kernel_ms / 1e3) / 1e12 if r.kernel_ms else 0.0
+        sweep.append({"arena_mib": arena, "replay_req_s": round(r.n_requests / (ms / 1e3), 2),
+                      "hit_rate": round(r.hits / (r.hits + r.misses), 4), "misses": int(r.misses),
+                      "h2d_gbs": round(r.h2d_bytes / (r.h2d_ms * 1e6), 2) if r.h2d_ms else 0.0,
+                      "infer_ms_per_request": round(r.kernel_ms / max(1, r.n_requests), 4),
+                      "tensor_tflops": round(tf, 1), "tensor_frac": round(tf / peak, 4)})
+    return {"c5_bert_base_arena_sweep": {
+        "workload": "C5: 20 BERT-base bf16 encoders (12x768, ffn 3072), 32x128 tokens/request, ws 20, "
+                    "325 rpm x 1 min, LALBO3, 1 GPU", "requests": int(rs[-1].n_requests),
+        "tensor_peak_tflops": peak, "peak_source": "MEASURED_PEAKS bf16_tflops (cuBLAS burst)",
+        "note": "tensor_tflops = model flops (GEMMs + attention) / CUDA-event time of the whole forward "
+                "(GEMMs, attention, LayerNorm, pooler, launch gaps)", "sweep": sweep}}
 
 
 if __name__ == "__main__":

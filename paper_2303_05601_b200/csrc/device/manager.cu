@@ -250,7 +250,7 @@ GpuManager::GpuManager(int device, uint64_t capacity_bytes, int manager_id) : de
     GFX_CUDA(cudaMalloc(&act_[0], sizeof(float) * kBatch * kMaxDim));
     GFX_CUDA(cudaMalloc(&act_[1], sizeof(float) * kBatch * kMaxDim));
     GFX_CUDA(cudaMalloc(&ws_, sizeof(float) * kMaxSplits * kBatch * kMaxDim));
-    const int ncnt = kMaxDim / 64 + 2;
+    const int ncnt = 512;  // split-K arrival / done counters per feature tile
     GFX_CUDA(cudaMalloc(&counters_, sizeof(unsigned) * ncnt));
     GFX_CUDA(cudaMalloc(&stats_, sizeof(float) * 2 * kBatch * ncnt));
     GFX_CUDA(cudaMemset(counters_, 0, sizeof(unsigned) * ncnt));
@@ -432,6 +432,8 @@ void GpuManager::infer(int model, const void* in_v, void* out_v, void* debug_hid
         // Layers 1.. and the softmax are programmatic dependents of the kernel
         // before them: their prologue and weight prefetch overlap its tail.
         static const bool trace_on = std::getenv("GFX_TRACE_MLP") != nullptr;
+        static const int ablate = std::getenv("GFX_MLP_ABLATE") ? std::atoi(std::getenv("GFX_MLP_ABLATE")) : 0;
+        a.ablate = ablate;
         std::vector<unsigned long long> tr;
         if (trace_on) {  // debug timeline: per-CTA phase timestamps of this launch
             GFX_CUDA(cudaMalloc(&a.trace, sizeof(unsigned long long) * 8 * a.ntiles * a.splits));
@@ -479,7 +481,7 @@ void GpuManager::reset() {
         s.readers.clear();
         s.live = false;
     }
-    GFX_CUDA(cudaMemset(counters_, 0, sizeof(unsigned) * (kMaxDim / 64 + 2)));
+    GFX_CUDA(cudaMemset(counters_, 0, sizeof(unsigned) * 512));
     GFX_CUDA(cudaDeviceSynchronize());
 }
 

@@ -25,6 +25,8 @@ struct MlpLayerArgs {
     unsigned* counters;    // [ntiles + 1], zero between launches
     float* stats;          // last layer: [ntiles][32][2] per-tile softmax partials
     unsigned long long* trace;  // debug (GFX_TRACE_MLP): per-CTA phase timestamps, else nullptr
+    int ablate;            // debug (GFX_MLP_ABLATE) bitmask, 0 in production: 1 no proxy fence,
+                           // 2 no hi/lo split work, 4 one MMA product, 8 no TMEM drains
     PageTable pt;
 };
 

@@ -57,13 +57,14 @@ using namespace gfx::sm100;
 constexpr int kRows = 32;        // batch rows per request = MMA N
 constexpr int kTileM = 128;      // output features per CTA = MMA M
 constexpr int kTileK = 32;       // fp32 K per stage (= one 128-byte swizzle row)
-constexpr int kLand = 6;         // TMA landing ring: raw fp32 tiles in flight from HBM
-constexpr int kOps = 2;          // converted (hi/lo) operand ring read by the tensor core
+constexpr int kLand = 5;         // TMA landing ring: raw fp32 tiles in flight from HBM
+constexpr int kOps = 3;          // converted (hi/lo) operand ring read by the tensor core
 constexpr int kThreads = 192;    // 6 warps
 constexpr uint32_t kWBytes = kTileM * kTileK * 4;  // 16 KB
 constexpr uint32_t kXBytes = kRows * kTileK * 4;   // 4 KB
 constexpr uint32_t kLandBytes = kWBytes + kXBytes;           // 20 KB, 1024-aligned
 constexpr uint32_t kOpBytes = 2 * kWBytes + 2 * kXBytes;     // 40 KB
+constexpr int kCounterDone = 128;  // counters[kCounterDone + tile]: splits done reducing
 constexpr uint32_t kTmemCols = 64;  // two 32-column accumulators (double-buffered chunks)
 constexpr int kChunk = 4;           // K tiles accumulated in TMEM before draining to fp32 registers
 constexpr int kDrainDelay = 2;      // drain a chunk after converting this many stages of the next
@@ -115,6 +116,11 @@ __device__ __forceinline__ void trace_mark(unsigned long long* tr, int i) {
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
     tr[(static_cast<size_t>(blockIdx.y) * gridDim.x + blockIdx.x) * 8 + i] = t;
 }
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
 }
@@ -122,7 +128,9 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
 __global__ void __launch_bounds__(kThreads, 1)
     mlp_tc_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ MlpLayerArgs a) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
+    // 1024-byte alignment by pointer arithmetic on the shared array itself, so
+    // every derived pointer stays in the shared window (LDS/STS, not generic).
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     __shared__ __align__(8) uint64_t land_full[kLand], land_empty[kLand], op_full[kOps], op_empty[kOps];
     __shared__ __align__(8) uint64_t tfull_bar[2], tempty_bar[2];
     __shared__ uint32_t tmem_base_s;
@@ -213,9 +221,11 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t off = kk * 32;  // 8 fp32 = 32 bytes of the swizzled row
                     const uint64_t ah = umma_desc_sw128(st.w_hi, off), al = umma_desc_sw128(st.w_lo, off);
                     const uint64_t bh = umma_desc_sw128(st.x_hi, off), bl = umma_desc_sw128(st.x_lo, off);
-                    umma_tf32(acc_tmem, al, bh, idesc, ((it % kChunk) | kk) ? 1u : 0u);  // small terms first
-                    umma_tf32(acc_tmem, ah, bl, idesc, 1u);
-                    umma_tf32(acc_tmem, ah, bh, idesc, 1u);
+                    if (!(a.ablate & 4)) {
+                        umma_tf32(acc_tmem, al, bh, idesc, ((it % kChunk) | kk) ? 1u : 0u);  // small terms first
+                        umma_tf32(acc_tmem, ah, bl, idesc, 1u);
+                    }
+                    umma_tf32(acc_tmem, ah, bh, idesc, ((a.ablate & 4) && ((it % kChunk) | kk) == 0) ? 0u : 1u);
                 }
                 umma_commit(&op_empty[s]);  // operand buffer free once these MMAs retire
                 if (it % kChunk == kChunk - 1 || it == nkt - 1) umma_commit(&tfull_bar[chunk & 1]);
@@ -226,6 +236,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int ct = tid - 64;  // 0..127
         const int q = warp & 3;   // this warp's TMEM lane quarter
         const int f = tile * kTileM + q * 32 + lane;
+        // Bias fetched now; its latency hides behind the whole main loop.
+        const float bias = f < N ? *reinterpret_cast<const float*>(translate(a.arena, pt, a.b_off + 4ull * f)) : 0.f;
         const int nchunks = (nkt + kChunk - 1) / kChunk;
         // Accumulator: TMEM lane = feature row of the tile, column = batch row.
         // Each chunk of kChunk K tiles is accumulated by the tensor core, then
@@ -254,6 +266,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (it >= kOps) mbar_wait(&op_empty[o], ((it / kOps) & 1) ^ 1);
             const Landing ld = landing(smem, s);
             const Operands op = operands(smem, o);
+            if (a.ablate & 2) {
+                mbar_arrive(&land_empty[s]);
+                mbar_arrive(&op_full[o]);
+                if (!(a.ablate & 8))
+                    while (drained < nchunks && min(nkt, (drained + 1) * kChunk) - 1 + kDrainDelay <= it) drain(drained++);
+                continue;
+            }
             const float4* w = reinterpret_cast<const float4*>(ld.w);
             const float4* x = reinterpret_cast<const float4*>(ld.x);
             float4 wv[kWBytes / 16 / 128], xv[kXBytes / 16 / 128];
@@ -276,65 +295,70 @@ __global__ void __launch_bounds__(kThreads, 1)
                 reinterpret_cast<float4*>(op.x_hi)[ct + 128 * j] = hi;
                 reinterpret_cast<float4*>(op.x_lo)[ct + 128 * j] = lo;
             }
-            fence_proxy_async_smem();
+            if (!(a.ablate & 1)) fence_proxy_async_smem();
             mbar_arrive(&op_full[o]);
-            while (drained < nchunks && min(nkt, (drained + 1) * kChunk) - 1 + kDrainDelay <= it) drain(drained++);
+            if (!(a.ablate & 8)) while (drained < nchunks && min(nkt, (drained + 1) * kChunk) - 1 + kDrainDelay <= it) drain(drained++);
         }
-        while (drained < nchunks) drain(drained++);
+        if (!(a.ablate & 8)) while (drained < nchunks) drain(drained++);
         if (ct == 0) trace_mark(a.trace, 4);
 
         pdl_trigger();  // main loop done: the next layer may start its prologue
         pdl_wait();     // workspace / counters / output belong to us only after the previous layer
-        bool finisher = true;
-        if (a.splits > 1) {
-            // Partials: ws[tile][split][32 rows][128 features], contiguous 16 KB blocks.
-            const int fl = q * 32 + lane;
-            float* blk = a.ws + (static_cast<size_t>(tile) * a.splits + split) * (kRows * kTileM);
-#pragma unroll
-            for (int b = 0; b < kRows; ++b) blk[b * kTileM + fl] = acc[b];
-            __threadfence();
-            epi_sync();
-            if (ct == 0) last_flag = atomicAdd(&a.counters[tile], 1u) == static_cast<unsigned>(a.splits - 1);
-            epi_sync();
-            finisher = last_flag;
-            if (finisher) {
-                __threadfence();
-                // Gather all partials of the tile into the (now idle) landing ring in
-                // one round of cp.async, then sum in fixed split order (deterministic).
-                float* red = reinterpret_cast<float*>(smem);
-                const float* src = a.ws + static_cast<size_t>(tile) * a.splits * (kRows * kTileM);
-                constexpr int kGroup = (kLand * kLandBytes) / (kRows * kTileM * 4);  // partials per round
-#pragma unroll
-                for (int b = 0; b < kRows; ++b) acc[b] = 0.f;
-                for (int g0 = 0; g0 < a.splits; g0 += kGroup) {
-                    const int ng = a.splits - g0 < kGroup ? a.splits - g0 : kGroup;
-                    const int chunks = ng * kRows * kTileM / 4;  // 16-byte chunks
-                    for (int c = ct; c < chunks; c += 128)
-                        cp_async16(red + 4 * c, src + static_cast<size_t>(g0) * kRows * kTileM + 4 * c);
-                    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
-                    epi_sync();
-                    for (int sp = 0; sp < ng; ++sp) {
-#pragma unroll
-                        for (int b = 0; b < kRows; ++b) acc[b] += red[(sp * kRows + b) * kTileM + fl];
-                    }
-                    epi_sync();
-                }
-                if (ct == 0) a.counters[tile] = 0;
-            }
-        }
-        if (ct == 0) trace_mark(a.trace, 5);
-        if (finisher) {
-            const bool valid = f < N;  // rows >= N are the zero padding of the last weight tile
-            const float bias = valid ? *reinterpret_cast<const float*>(translate(a.arena, pt, a.b_off + 4ull * f)) : 0.f;
+        const bool valid = f < N;  // rows >= N are the zero padding of the last weight tile
+        if (a.splits == 1) {
 #pragma unroll
             for (int b = 0; b < kRows; ++b) {
                 float v = acc[b] + bias;
                 if (a.relu) v = fmaxf(v, 0.f);
-                acc[b] = v;
                 if (valid) a.y[static_cast<size_t>(b) * N + f] = v;
             }
-            if (ct == 0) trace_mark(a.trace, 6);
+        } else {
+            // Split-K: publish this CTA's partial ws[tile][split][32][128], wait
+            // until all splits of the tile have published (the grid is a single
+            // wave, one CTA per SM, so every sibling is resident), then each
+            // split reduces its own rows b = split, split+S, ... in fixed split
+            // order — deterministic, and the reduction is spread over S CTAs.
+            const int fl = q * 32 + lane;
+            const size_t blk = static_cast<size_t>(kRows) * kTileM;
+            float* base = a.ws + static_cast<size_t>(tile) * a.splits * blk;
+#pragma unroll
+            for (int b = 0; b < kRows; ++b) base[static_cast<size_t>(split) * blk + b * kTileM + fl] = acc[b];
+            __threadfence();
+            epi_sync();
+            if (ct == 0) {
+                atomicAdd(&a.counters[tile], 1u);
+                while (ld_acquire(&a.counters[tile]) < static_cast<unsigned>(a.splits)) __nanosleep(64);
+            }
+            epi_sync();
+            // Gather this split's rows of every partial in one round of cp.async
+            // (the landing ring is idle now), then sum in fixed split order.
+            const int nrows = (kRows - split + a.splits - 1) / a.splits;
+            float* red = reinterpret_cast<float*>(smem);  // [nrows][splits][128]
+            const int chunks = nrows * a.splits * (kTileM / 4);
+            for (int c = ct; c < chunks; c += 128) {
+                const int col4 = c % (kTileM / 4), rs = c / (kTileM / 4);
+                const int sp = rs % a.splits, ri = rs / a.splits;
+                const int b = split + ri * a.splits;
+                cp_async16(red + static_cast<size_t>(rs) * kTileM + col4 * 4,
+                           base + static_cast<size_t>(sp) * blk + b * kTileM + col4 * 4);
+            }
+            asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+            epi_sync();
+            for (int ri = 0; ri < nrows; ++ri) {
+                const int b = split + ri * a.splits;
+                float v = 0.f;
+                for (int sp = 0; sp < a.splits; ++sp) v += red[static_cast<size_t>(ri * a.splits + sp) * kTileM + fl];
+                v += bias;
+                if (a.relu) v = fmaxf(v, 0.f);
+                if (valid) a.y[static_cast<size_t>(b) * N + f] = v;
+            }
+            epi_sync();
+            if (ct == 0 && atomicAdd(&a.counters[kCounterDone + tile], 1u) == static_cast<unsigned>(a.splits - 1)) {
+                a.counters[tile] = 0;  // every sibling has left the spin: reset for the next launch
+                a.counters[kCounterDone + tile] = 0;
+            }
         }
+        if (ct == 0) trace_mark(a.trace, 5);
     }
 
     tc_fence_before();
