@@ -42,7 +42,7 @@ __device__ __forceinline__ float gelu(float x) { return 0.5f * x * (1.0f + erff(
 
 // ------------------------------------------------------------------ K2 GEMM
 
-constexpr int kGM = 128, kGN = 128, kGK = 64, kGStages = 4, kGThreads = 192;
+constexpr int kGM = 128, kGN = 128, kGK = 64, kGStages = 3, kGThreads = 192;  // 96 KB: 2 CTAs/SM
 constexpr uint32_t kGTile = 128 * 128;  // 16 KB (A tile = B tile)
 constexpr uint32_t kGStage = 2 * kGTile;
 
@@ -58,10 +58,10 @@ struct GemmArgs {
 };
 
 template <int kEpi>
-__global__ void __launch_bounds__(kGThreads, 1)
+__global__ void __launch_bounds__(kGThreads, 2)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ GemmArgs a) {
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t{1023});
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
     __shared__ __align__(8) uint64_t full_bar[kGStages], empty_bar[kGStages], tmem_bar;
     __shared__ uint32_t tmem_s;
     __shared__ uint32_t pt[GFX_MAX_PAGES];

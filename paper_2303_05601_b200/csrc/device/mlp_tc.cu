@@ -57,17 +57,19 @@ using namespace gfx::sm100;
 constexpr int kRows = 32;        // batch rows per request = MMA N
 constexpr int kTileM = 128;      // output features per CTA = MMA M
 constexpr int kTileK = 32;       // fp32 K per stage (= one 128-byte swizzle row)
-constexpr int kLand = 5;         // TMA landing ring: raw fp32 tiles in flight from HBM
-constexpr int kOps = 3;          // converted (hi/lo) operand ring read by the tensor core
-constexpr int kThreads = 192;    // 6 warps
+constexpr int kLand = 8;         // TMA landing ring: raw fp32 tiles in flight from HBM
+constexpr int kOps = 6;          // converted operand ring: W hi/lo in TMEM, X hi/lo in smem
+constexpr int kThreads = 320;    // 10 warps: TMA, MMA, 4 converters, 4 drain/epilogue
 constexpr uint32_t kWBytes = kTileM * kTileK * 4;  // 16 KB
 constexpr uint32_t kXBytes = kRows * kTileK * 4;   // 4 KB
 constexpr uint32_t kLandBytes = kWBytes + kXBytes;           // 20 KB, 1024-aligned
-constexpr uint32_t kOpBytes = 2 * kWBytes + 2 * kXBytes;     // 40 KB
+constexpr uint32_t kOpBytes = 2 * kXBytes;                   // 8 KB: X hi + X lo (W hi/lo live in TMEM)
 constexpr int kCounterDone = 128;  // counters[kCounterDone + tile]: splits done reducing
-constexpr uint32_t kTmemCols = 64;  // two 32-column accumulators (double-buffered chunks)
+// TMEM: columns [0,64) two 32-column fp32 accumulators (double-buffered chunks);
+// operand stage o: W_hi at 64 + 64o, W_lo at 64 + 64o + 32 (lane = weight row, column = k).
+constexpr uint32_t kTmemCols = 512;
+static_assert(64 + 64 * kOps <= 512, "TMEM budget");
 constexpr int kChunk = 4;           // K tiles accumulated in TMEM before draining to fp32 registers
-constexpr int kDrainDelay = 2;      // drain a chunk after converting this many stages of the next
 
 struct Landing {
     uint8_t* w;
@@ -78,14 +80,12 @@ __device__ __forceinline__ Landing landing(uint8_t* base, int s) {
     return {p, p + kWBytes};
 }
 struct Operands {
-    uint8_t* w_hi;
-    uint8_t* w_lo;
     uint8_t* x_hi;
     uint8_t* x_lo;
 };
 __device__ __forceinline__ Operands operands(uint8_t* base, int s) {
     uint8_t* p = base + static_cast<size_t>(kLand) * kLandBytes + static_cast<size_t>(s) * kOpBytes;
-    return {p, p + kWBytes, p + 2 * kWBytes, p + 2 * kWBytes + kXBytes};
+    return {p, p + kXBytes};
 }
 
 __device__ __forceinline__ const char* translate(const char* arena, const uint32_t* pt, uint64_t v) {
@@ -105,7 +105,7 @@ __device__ __forceinline__ void split_tf32(const float4& v, float4& hi, float4& 
     }
 }
 
-__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
+__device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }  // drain warps
 // Programmatic dependent launch: wait for the previous kernel of the stream
 // (no-op without the launch attribute) / let the next one start its prologue.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull_bar[b], 1);
-            mbar_init(&tempty_bar[b], 128);
+            mbar_init(&tempty_bar[b], 128);  // the 4 drain warps
         }
         mbar_fence_init();
         tma_prefetch_desc(&tmap_x);
@@ -216,25 +216,78 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&op_full[s], (it / kOps) & 1);
                 tc_fence_after();
                 const Operands st = operands(smem, s);
+                const uint32_t a_hi = tmem + 64u + 64u * static_cast<uint32_t>(s), a_lo = a_hi + 32u;
 #pragma unroll
                 for (int kk = 0; kk < kTileK / 8; ++kk) {
-                    const uint32_t off = kk * 32;  // 8 fp32 = 32 bytes of the swizzled row
-                    const uint64_t ah = umma_desc_sw128(st.w_hi, off), al = umma_desc_sw128(st.w_lo, off);
+                    const uint32_t off = kk * 32;  // 8 fp32 = 32 bytes of the swizzled X row
                     const uint64_t bh = umma_desc_sw128(st.x_hi, off), bl = umma_desc_sw128(st.x_lo, off);
+                    const uint32_t ck = static_cast<uint32_t>(kk * 8);  // 8 TMEM columns per K=8 slice
                     if (!(a.ablate & 4)) {
-                        umma_tf32(acc_tmem, al, bh, idesc, ((it % kChunk) | kk) ? 1u : 0u);  // small terms first
-                        umma_tf32(acc_tmem, ah, bl, idesc, 1u);
+                        umma_tf32_ts(acc_tmem, a_lo + ck, bh, idesc, ((it % kChunk) | kk) ? 1u : 0u);  // small terms first
+                        umma_tf32_ts(acc_tmem, a_hi + ck, bl, idesc, 1u);
                     }
-                    umma_tf32(acc_tmem, ah, bh, idesc, ((a.ablate & 4) && ((it % kChunk) | kk) == 0) ? 0u : 1u);
+                    umma_tf32_ts(acc_tmem, a_hi + ck, bh, idesc, ((a.ablate & 4) && ((it % kChunk) | kk) == 0) ? 0u : 1u);
                 }
                 umma_commit(&op_empty[s]);  // operand buffer free once these MMAs retire
                 if (it % kChunk == kChunk - 1 || it == nkt - 1) umma_commit(&tfull_bar[chunk & 1]);
             }
         }
-    } else {
-        // ---------------- hi/lo split, then epilogue ----------------
+    } else if (warp < 6) {
+        // ---------------- converters: hi/lo split into the operand ring ----------------
         const int ct = tid - 64;  // 0..127
         const int q = warp & 3;   // this warp's TMEM lane quarter
+        for (int it = 0; it < nkt; ++it) {
+            const int s = it % kLand;
+            const int o = it % kOps;
+            mbar_wait(&land_full[s], (it / kLand) & 1);
+            if (it == 0 && ct == 0) trace_mark(a.trace, 3);
+            if (it >= kOps) mbar_wait(&op_empty[o], ((it / kOps) & 1) ^ 1);
+            const Landing ld = landing(smem, s);
+            const Operands op = operands(smem, o);
+            if (a.ablate & 2) {
+                mbar_arrive(&land_empty[s]);
+                mbar_arrive(&op_full[o]);
+                continue;
+            }
+            // This thread owns weight row r = 32q + lane of the tile (its TMEM
+            // lane): read the row's 8 swizzled 16-byte chunks (conflict-free),
+            // split into hi/lo in registers, store both as 32 TMEM columns.
+            const int r = q * 32 + lane;
+            const float4* wrow = reinterpret_cast<const float4*>(ld.w + r * 128);
+            float whi[32], wlo[32];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float4 v = wrow[j ^ (r & 7)];
+                float4 h, l;
+                split_tf32(v, h, l);
+                whi[4 * j] = h.x; whi[4 * j + 1] = h.y; whi[4 * j + 2] = h.z; whi[4 * j + 3] = h.w;
+                wlo[4 * j] = l.x; wlo[4 * j + 1] = l.y; wlo[4 * j + 2] = l.z; wlo[4 * j + 3] = l.w;
+            }
+            const float4* x = reinterpret_cast<const float4*>(ld.x);
+            float4 xv[kXBytes / 16 / 128];
+#pragma unroll
+            for (int j = 0; j < static_cast<int>(kXBytes / 16 / 128); ++j) xv[j] = x[ct + 128 * j];
+            mbar_arrive(&land_empty[s]);  // landing slot back to the TMA producer
+            tc_fence_after();             // order after the MMAs that last read stage o
+            const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
+            tmem_st_32x32b_x32(lane_base + 64u + 64u * static_cast<uint32_t>(o), whi);
+            tmem_st_32x32b_x32(lane_base + 96u + 64u * static_cast<uint32_t>(o), wlo);
+#pragma unroll
+            for (int j = 0; j < static_cast<int>(kXBytes / 16 / 128); ++j) {
+                float4 hi, lo;
+                split_tf32(xv[j], hi, lo);
+                reinterpret_cast<float4*>(op.x_hi)[ct + 128 * j] = hi;
+                reinterpret_cast<float4*>(op.x_lo)[ct + 128 * j] = lo;
+            }
+            tmem_st_wait();
+            tc_fence_before();
+            if (!(a.ablate & 1)) fence_proxy_async_smem();
+            mbar_arrive(&op_full[o]);
+        }
+    } else {
+        // ---------------- drain + epilogue warps ----------------
+        const int ct = tid - 192;  // 0..127
+        const int q = warp & 3;    // TMEM lane quarter (warps 6..9 -> 2,3,0,1)
         const int f = tile * kTileM + q * 32 + lane;
         // Bias fetched now; its latency hides behind the whole main loop.
         const float bias = f < N ? *reinterpret_cast<const float*>(translate(a.arena, pt, a.b_off + 4ull * f)) : 0.f;
@@ -247,8 +300,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         float acc[kRows];
 #pragma unroll
         for (int b = 0; b < kRows; ++b) acc[b] = 0.f;
-        int drained = 0;
-        auto drain = [&](int c) {
+        for (int c = 0; c < nchunks; ++c) {
             mbar_wait(&tfull_bar[c & 1], (c >> 1) & 1);
             tc_fence_after();
             float part[kRows];
@@ -257,49 +309,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int b = 0; b < kRows; ++b) acc[b] += part[b];
             tc_fence_before();
             mbar_arrive(&tempty_bar[c & 1]);
-        };
-        for (int it = 0; it < nkt; ++it) {
-            const int s = it % kLand;
-            const int o = it % kOps;
-            mbar_wait(&land_full[s], (it / kLand) & 1);
-            if (it == 0 && ct == 0) trace_mark(a.trace, 3);
-            if (it >= kOps) mbar_wait(&op_empty[o], ((it / kOps) & 1) ^ 1);
-            const Landing ld = landing(smem, s);
-            const Operands op = operands(smem, o);
-            if (a.ablate & 2) {
-                mbar_arrive(&land_empty[s]);
-                mbar_arrive(&op_full[o]);
-                if (!(a.ablate & 8))
-                    while (drained < nchunks && min(nkt, (drained + 1) * kChunk) - 1 + kDrainDelay <= it) drain(drained++);
-                continue;
-            }
-            const float4* w = reinterpret_cast<const float4*>(ld.w);
-            const float4* x = reinterpret_cast<const float4*>(ld.x);
-            float4 wv[kWBytes / 16 / 128], xv[kXBytes / 16 / 128];
-#pragma unroll
-            for (int j = 0; j < static_cast<int>(kWBytes / 16 / 128); ++j) wv[j] = w[ct + 128 * j];
-#pragma unroll
-            for (int j = 0; j < static_cast<int>(kXBytes / 16 / 128); ++j) xv[j] = x[ct + 128 * j];
-            mbar_arrive(&land_empty[s]);  // landing slot back to the TMA producer
-#pragma unroll
-            for (int j = 0; j < static_cast<int>(kWBytes / 16 / 128); ++j) {
-                float4 hi, lo;
-                split_tf32(wv[j], hi, lo);
-                reinterpret_cast<float4*>(op.w_hi)[ct + 128 * j] = hi;
-                reinterpret_cast<float4*>(op.w_lo)[ct + 128 * j] = lo;
-            }
-#pragma unroll
-            for (int j = 0; j < static_cast<int>(kXBytes / 16 / 128); ++j) {
-                float4 hi, lo;
-                split_tf32(xv[j], hi, lo);
-                reinterpret_cast<float4*>(op.x_hi)[ct + 128 * j] = hi;
-                reinterpret_cast<float4*>(op.x_lo)[ct + 128 * j] = lo;
-            }
-            if (!(a.ablate & 1)) fence_proxy_async_smem();
-            mbar_arrive(&op_full[o]);
-            if (!(a.ablate & 8)) while (drained < nchunks && min(nkt, (drained + 1) * kChunk) - 1 + kDrainDelay <= it) drain(drained++);
         }
-        if (!(a.ablate & 8)) while (drained < nchunks) drain(drained++);
         if (ct == 0) trace_mark(a.trace, 4);
 
         pdl_trigger();  // main loop done: the next layer may start its prologue
