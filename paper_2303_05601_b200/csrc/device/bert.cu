@@ -41,10 +41,12 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
 __device__ __forceinline__ float gelu(float x) { return 0.5f * x * (1.0f + erff(x * 0.70710678118654752f)); }
 
 // ------------------------------------------------------------------ K2 GEMM
+// Persistent: one CTA per SM loops over 128 x kBN output tiles; the TMEM holds
+// two accumulators so the epilogue of tile i overlaps the MMAs of tile i+1.
 
-constexpr int kGM = 128, kGN = 128, kGK = 64, kGStages = 3, kGThreads = 192;  // 96 KB: 2 CTAs/SM
-constexpr uint32_t kGTile = 128 * 128;  // 16 KB (A tile = B tile)
-constexpr uint32_t kGStage = 2 * kGTile;
+constexpr int kGM = 128, kGK = 64, kGThreads = 192;
+constexpr uint32_t kGATile = 128 * 128;  // A: 128 rows x 64 bf16 (16 KB)
+constexpr uint32_t kGSmem = 192 * 1024;  // stage ring budget
 
 enum Epi : int { kEpiBias = 0, kEpiGelu = 1, kEpiResid = 2 };
 
@@ -53,36 +55,43 @@ struct GemmArgs {
     uint64_t w_off, b_off;        // weight tiles, fp32 bias
     __nv_bfloat16* y;             // [T x N]
     const __nv_bfloat16* resid;   // [T x N] (kEpiResid)
-    int K, N;
+    int T, K, N;
     PageTable pt;
 };
 
-template <int kEpi>
-__global__ void __launch_bounds__(kGThreads, 2)
+template <int kEpi, int kBN>
+__global__ void __launch_bounds__(kGThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ GemmArgs a) {
+    constexpr uint32_t kBBytes = kBN * 128;            // B: kBN rows x 64 bf16
+    constexpr uint32_t kStage = kGATile + kBBytes;
+    constexpr int kStages = static_cast<int>(kGSmem / kStage);
+    constexpr uint32_t kTmemCols = 2 * kBN <= 256 ? 256 : 512;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
-    __shared__ __align__(8) uint64_t full_bar[kGStages], empty_bar[kGStages], tmem_bar;
+    __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], tfull_bar[2], tempty_bar[2];
     __shared__ uint32_t tmem_s;
     __shared__ uint32_t pt[GFX_MAX_PAGES];
-    __shared__ float bias_s[kGN];
+    __shared__ float bias_s[kBN];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    const int n0 = blockIdx.x * kGN, m0 = blockIdx.y * kGM;
-    const int nkt = a.K / kGK;
-    const int ktiles_row = a.K / kGK;
+    const int n_tiles = a.N / kBN, m_tiles = a.T / kGM, tiles = n_tiles * m_tiles;
+    const int nk = a.K / kGK;
+    const int ktiles_row = a.K / kGK;  // blob weight tiles per 128 rows
 
     for (int i = tid; i < static_cast<int>(a.pt.n); i += kGThreads) pt[i] = a.pt.page[i];
     if (tid == 0) {
-        for (int s = 0; s < kGStages; ++s) {
+        for (int s = 0; s < kStages; ++s) {
             mbar_init(&full_bar[s], 1);
             mbar_init(&empty_bar[s], 1);
         }
-        mbar_init(&tmem_bar, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&tfull_bar[b], 1);
+            mbar_init(&tempty_bar[b], 128);
+        }
         mbar_fence_init();
         tma_prefetch_desc(&tmap_x);
     }
-    if (warp == 1) tmem_alloc<128>(&tmem_s);
+    if (warp == 1) tmem_alloc<kTmemCols>(&tmem_s);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -90,97 +99,115 @@ __global__ void __launch_bounds__(kGThreads, 2)
 
     if (warp == 0) {
         if (lane == 0) {
-            const int pre = nkt < kGStages ? nkt : kGStages;
-            for (int it = 0; it < pre; ++it) {  // weights: before the grid dependency
-                uint8_t* st = smem + static_cast<size_t>(it) * kGStage;
-                mbar_arrive_expect_tx(&full_bar[it], kGStage);
-                const uint64_t v = a.w_off + (static_cast<uint64_t>(blockIdx.x) * ktiles_row + it) * kGTile;
-                tma_bulk_g2s(st + kGTile, translate(a.arena, pt, v), kGTile, &full_bar[it]);
-            }
-            pdl_wait();
-            for (int it = 0; it < pre; ++it)
-                tma_tile2d_g2s(smem + static_cast<size_t>(it) * kGStage, &tmap_x, it * kGK, m0, &full_bar[it]);
-            for (int it = pre; it < nkt; ++it) {
-                const int s = it % kGStages;
-                mbar_wait(&empty_bar[s], ((it / kGStages) & 1) ^ 1);
-                uint8_t* st = smem + static_cast<size_t>(s) * kGStage;
-                mbar_arrive_expect_tx(&full_bar[s], kGStage);
-                const uint64_t v = a.w_off + (static_cast<uint64_t>(blockIdx.x) * ktiles_row + it) * kGTile;
-                tma_bulk_g2s(st + kGTile, translate(a.arena, pt, v), kGTile, &full_bar[s]);
-                tma_tile2d_g2s(st, &tmap_x, it * kGK, m0, &full_bar[s]);
+            // Producer: one continuous stage ring across this CTA's tiles.
+            int g = 0;
+            bool waited = false;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
+                const int m0 = (t / n_tiles) * kGM, nb = t % n_tiles;
+                for (int k = 0; k < nk; ++k, ++g) {
+                    const int s = g % kStages;
+                    if (g >= kStages) mbar_wait(&empty_bar[s], ((g / kStages) & 1) ^ 1);
+                    uint8_t* st = smem + static_cast<size_t>(s) * kStage;
+                    mbar_arrive_expect_tx(&full_bar[s], kStage);
+#pragma unroll
+                    for (int h = 0; h < kBN / 128; ++h) {  // weights first: independent of the previous kernel
+                        const uint64_t v = a.w_off + (static_cast<uint64_t>(nb * (kBN / 128) + h) * ktiles_row + k) * kGATile;
+                        tma_bulk_g2s(st + kGATile + h * kGATile, translate(a.arena, pt, v), kGATile, &full_bar[s]);
+                    }
+                    if (!waited) {
+                        pdl_wait();
+                        waited = true;
+                    }
+                    tma_tile2d_g2s(st, &tmap_x, k * kGK, m0, &full_bar[s]);
+                }
             }
         }
     } else if (warp == 1) {
         if (lane == 0) {
-            constexpr uint32_t idesc = umma_idesc<kGM, kGN, 1>();  // BF16 x BF16 -> F32
-            for (int it = 0; it < nkt; ++it) {
-                const int s = it % kGStages;
-                mbar_wait(&full_bar[s], (it / kGStages) & 1);
+            constexpr uint32_t idesc = umma_idesc<kGM, kBN, 1>();  // BF16 x BF16 -> F32, M=128, N=kBN
+            int g = 0, i = 0;
+            for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+                const int b = i & 1;
+                if (i >= 2) mbar_wait(&tempty_bar[b], ((i >> 1) & 1) ^ 1);  // epilogue drained tile i-2
                 tc_fence_after();
-                uint8_t* st = smem + static_cast<size_t>(s) * kGStage;
+                const uint32_t acc = tmem + static_cast<uint32_t>(b * kBN);
+                for (int k = 0; k < nk; ++k, ++g) {
+                    const int s = g % kStages;
+                    mbar_wait(&full_bar[s], (g / kStages) & 1);
+                    tc_fence_after();
+                    uint8_t* st = smem + static_cast<size_t>(s) * kStage;
 #pragma unroll
-                for (int kk = 0; kk < kGK / 16; ++kk) {  // K = 16 bf16 = 32 bytes per MMA
-                    umma_f16(tmem, umma_desc_sw128(st, kk * 32), umma_desc_sw128(st + kGTile, kk * 32), idesc,
-                             (it | kk) ? 1u : 0u);
+                    for (int kk = 0; kk < kGK / 16; ++kk)  // K = 16 bf16 = 32 bytes per MMA
+                        umma_f16(acc, umma_desc_sw128(st, kk * 32), umma_desc_sw128(st + kGATile, kk * 32), idesc,
+                                 (k | kk) ? 1u : 0u);
+                    umma_commit(&empty_bar[s]);
                 }
-                umma_commit(&empty_bar[s]);
+                umma_commit(&tfull_bar[b]);
             }
-            umma_commit(&tmem_bar);
         }
     } else {
         // Epilogue: TMEM lane = token row, column = output feature.
-        const int q = warp & 3;
-        const int row = m0 + q * 32 + lane;
-        bias_s[tid - 64] = *reinterpret_cast<const float*>(translate(a.arena, pt, a.b_off + 4ull * (n0 + tid - 64)));
-        asm volatile("bar.sync 1, 128;\n" ::: "memory");  // epilogue warps only
-        mbar_wait(&tmem_bar, 0);
-        tc_fence_after();
-        pdl_trigger();
-        __nv_bfloat16* yrow = a.y + static_cast<size_t>(row) * a.N + n0;
+        const int q = warp & 3, ct = tid - 64;
+        int i = 0;
+        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+            const int m0 = (t / n_tiles) * kGM, n0 = (t % n_tiles) * kBN;
+            const int b = i & 1;
+            asm volatile("bar.sync 1, 128;\n" ::: "memory");  // previous tile's bias reads done
+            for (int c = ct; c < kBN; c += 128)
+                bias_s[c] = *reinterpret_cast<const float*>(translate(a.arena, pt, a.b_off + 4ull * (n0 + c)));
+            asm volatile("bar.sync 1, 128;\n" ::: "memory");
+            mbar_wait(&tfull_bar[b], (i >> 1) & 1);
+            tc_fence_after();
+            if (t + static_cast<int>(gridDim.x) >= tiles) pdl_trigger();  // last tile: let the next kernel start
+            const int row = m0 + q * 32 + lane;
+            __nv_bfloat16* yrow = a.y + static_cast<size_t>(row) * a.N + n0;
 #pragma unroll 1
-        for (int c = 0; c < kGN / 32; ++c) {
-            float v[32];
-            tmem_ld_32x32b_x32(tmem + static_cast<uint32_t>(c * 32) + (static_cast<uint32_t>(q * 32) << 16), v);
-            float r[32];
-            if (kEpi == kEpiResid) {
-                const uint4* rp = reinterpret_cast<const uint4*>(a.resid + static_cast<size_t>(row) * a.N + n0 + c * 32);
+            for (int c = 0; c < kBN / 32; ++c) {
+                float v[32];
+                tmem_ld_32x32b_x32(tmem + static_cast<uint32_t>(b * kBN + c * 32) + (static_cast<uint32_t>(q * 32) << 16), v);
+                float r[32];
+                if (kEpi == kEpiResid) {
+                    const uint4* rp = reinterpret_cast<const uint4*>(a.resid + static_cast<size_t>(row) * a.N + n0 + c * 32);
 #pragma unroll
-                for (int i = 0; i < 4; ++i) {
-                    const uint4 u = rp[i];
-                    const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+                    for (int u = 0; u < 4; ++u) {
+                        const uint4 w = rp[u];
+                        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&w);
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const float2 f2 = __bfloat1622float2(h2[j]);
-                        r[i * 8 + 2 * j] = f2.x;
-                        r[i * 8 + 2 * j + 1] = f2.y;
+                        for (int j = 0; j < 4; ++j) {
+                            const float2 f2 = __bfloat1622float2(h2[j]);
+                            r[u * 8 + 2 * j] = f2.x;
+                            r[u * 8 + 2 * j + 1] = f2.y;
+                        }
                     }
                 }
-            }
-            uint4 out[4];
-            __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(out);
+                uint4 out[4];
+                __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(out);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                float x0 = v[2 * j] + bias_s[c * 32 + 2 * j];
-                float x1 = v[2 * j + 1] + bias_s[c * 32 + 2 * j + 1];
-                if (kEpi == kEpiGelu) {
-                    x0 = gelu(x0);
-                    x1 = gelu(x1);
+                for (int j = 0; j < 16; ++j) {
+                    float x0 = v[2 * j] + bias_s[c * 32 + 2 * j];
+                    float x1 = v[2 * j + 1] + bias_s[c * 32 + 2 * j + 1];
+                    if (kEpi == kEpiGelu) {
+                        x0 = gelu(x0);
+                        x1 = gelu(x1);
+                    }
+                    if (kEpi == kEpiResid) {
+                        x0 += r[2 * j];
+                        x1 += r[2 * j + 1];
+                    }
+                    o2[j] = __floats2bfloat162_rn(x0, x1);
                 }
-                if (kEpi == kEpiResid) {
-                    x0 += r[2 * j];
-                    x1 += r[2 * j + 1];
-                }
-                o2[j] = __floats2bfloat162_rn(x0, x1);
-            }
-            uint4* dst = reinterpret_cast<uint4*>(yrow + c * 32);
+                uint4* dst = reinterpret_cast<uint4*>(yrow + c * 32);
 #pragma unroll
-            for (int i = 0; i < 4; ++i) dst[i] = out[i];
+                for (int u = 0; u < 4; ++u) dst[u] = out[u];
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty_bar[b]);  // accumulator b free for tile i+2
         }
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (warp == 1) tmem_dealloc<128>(tmem);
+    if (warp == 1) tmem_dealloc<kTmemCols>(tmem);
 }
 
 // ------------------------------------------------------------------ K3 attention
@@ -188,8 +215,7 @@ __global__ void __launch_bounds__(kGThreads, 2)
 // rows 16w..16w+15; mma.sync m16n8k16 bf16 -> fp32.
 
 constexpr int kS = 128, kDh = 64;
-constexpr int kKPitch = kDh + 8;   // bf16 elements per K row (bank-conflict-free B loads)
-constexpr int kVPitch = kS + 8;    // bf16 elements per V^T row
+constexpr int kKPitch = kDh + 8;   // bf16 per K / V row in smem (144 B: conflict-free LDS.32 and ldmatrix)
 
 __device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
     asm volatile(
@@ -203,28 +229,30 @@ __device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
     return *reinterpret_cast<uint32_t*>(&h);
 }
 
+__device__ __forceinline__ void ldsm_x4_trans(uint32_t (&r)[4], const void* p) {
+    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(smem_u32(p)));
+}
+
 __global__ void __launch_bounds__(256) attention_kernel(const __nv_bfloat16* __restrict__ qkv,
                                                         __nv_bfloat16* __restrict__ ctx, int heads) {
     __shared__ __align__(16) __nv_bfloat16 ks[kS * kKPitch];
-    __shared__ __align__(16) __nv_bfloat16 vts[kDh * kVPitch];
+    __shared__ __align__(16) __nv_bfloat16 vs[kS * kKPitch];
     const int seq = blockIdx.x / heads, h = blockIdx.x % heads;
     const int d = heads * kDh, ld = 3 * d;
     const size_t tok0 = static_cast<size_t>(seq) * kS;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     pdl_wait();
-    // K rows and V transposed into shared memory.
+    // K and V rows (128 B each) into padded shared rows, 16-byte cp.async chunks.
     for (int i = tid; i < kS * (kDh / 8); i += 256) {
         const int t = i / (kDh / 8), c = (i % (kDh / 8)) * 8;
-        const uint4 kv = *reinterpret_cast<const uint4*>(qkv + (tok0 + t) * ld + d + h * kDh + c);
-        *reinterpret_cast<uint4*>(&ks[t * kKPitch + c]) = kv;
-        const uint4 vv = *reinterpret_cast<const uint4*>(qkv + (tok0 + t) * ld + 2 * d + h * kDh + c);
-        const __nv_bfloat16* ve = reinterpret_cast<const __nv_bfloat16*>(&vv);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) vts[(c + j) * kVPitch + t] = ve[j];
+        const __nv_bfloat16* src = qkv + (tok0 + t) * ld + h * kDh + c;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(&ks[t * kKPitch + c])), "l"(src + d));
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(&vs[t * kKPitch + c])),
+                     "l"(src + 2 * d));
     }
-    __syncthreads();
-    pdl_trigger();
-
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
     const int g = lane >> 2, tq = lane & 3;  // mma fragment coordinates
     const int r0 = warp * 16 + g;            // this thread's query rows: r0, r0 + 8
     // Q fragments for the 4 k16 steps of d_head = 64.
@@ -239,6 +267,9 @@ __global__ void __launch_bounds__(256) attention_kernel(const __nv_bfloat16* __r
         qa[kk][2] = *reinterpret_cast<const uint32_t*>(q0 + c + 8);
         qa[kk][3] = *reinterpret_cast<const uint32_t*>(q1 + c + 8);
     }
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    pdl_trigger();
     // S = Q K^T: 16 n8 tiles of keys.
     float sc[16][4];
 #pragma unroll
@@ -288,11 +319,16 @@ __global__ void __launch_bounds__(256) attention_kernel(const __nv_bfloat16* __r
         const uint32_t pa[4] = {pack_bf16(sc[2 * kk][0], sc[2 * kk][1]), pack_bf16(sc[2 * kk][2], sc[2 * kk][3]),
                                 pack_bf16(sc[2 * kk + 1][0], sc[2 * kk + 1][1]),
                                 pack_bf16(sc[2 * kk + 1][2], sc[2 * kk + 1][3])};
+        // B fragments of V (keys x dims) for two 8-wide dim tiles per ldmatrix.x4.trans:
+        // lane l addresses row (key) kk*16 + (l&7) + 8*((l>>3)&1), dims + 8*(l>>4).
 #pragma unroll
-        for (int dt = 0; dt < 8; ++dt) {
-            const __nv_bfloat16* vr = &vts[(dt * 8 + g) * kVPitch + kk * 16 + 2 * tq];
-            const uint32_t b[2] = {*reinterpret_cast<const uint32_t*>(vr), *reinterpret_cast<const uint32_t*>(vr + 8)};
-            mma_bf16_16816(oc[dt], pa, b);
+        for (int dp = 0; dp < 4; ++dp) {
+            uint32_t bv[4];
+            const int key = kk * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
+            ldsm_x4_trans(bv, &vs[key * kKPitch + dp * 16 + ((lane >> 4) << 3)]);
+            const uint32_t b0[2] = {bv[0], bv[1]}, b1[2] = {bv[2], bv[3]};
+            mma_bf16_16816(oc[2 * dp], pa, b0);
+            mma_bf16_16816(oc[2 * dp + 1], pa, b1);
         }
     }
     const float i0 = 1.f / l0, i1 = 1.f / l1;
@@ -309,15 +345,16 @@ __global__ void __launch_bounds__(256) attention_kernel(const __nv_bfloat16* __r
 
 template <int kD>
 __global__ void __launch_bounds__(256) layernorm_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
-                                                        const char* arena, PageTable ptab, uint64_t g_off,
-                                                        uint64_t b_off, int rows) {
-    __shared__ float gam[kD], bet[kD];
-    __shared__ uint32_t pt[GFX_MAX_PAGES];
-    for (int i = threadIdx.x; i < static_cast<int>(ptab.n); i += 256) pt[i] = ptab.page[i];
-    __syncthreads();
-    for (int i = threadIdx.x; i < kD; i += 256) {
-        gam[i] = *reinterpret_cast<const float*>(translate(arena, pt, g_off + 4ull * i));
-        bet[i] = *reinterpret_cast<const float*>(translate(arena, pt, b_off + 4ull * i));
+                                                        const char* arena, const __grid_constant__ PageTable ptab,
+                                                        uint64_t g_off, uint64_t b_off, int rows) {
+    __shared__ __align__(16) float gam[kD], bet[kD];
+    // gamma / beta: one 16-byte chunk per thread, translated straight from the
+    // page table parameter (256 B-aligned vectors: a chunk never straddles a page).
+    for (int c = threadIdx.x; c < kD / 4; c += 256) {
+        *reinterpret_cast<float4*>(&gam[4 * c]) =
+            *reinterpret_cast<const float4*>(translate(arena, ptab.page, g_off + 16ull * c));
+        *reinterpret_cast<float4*>(&bet[4 * c]) =
+            *reinterpret_cast<const float4*>(translate(arena, ptab.page, b_off + 16ull * c));
     }
     __syncthreads();
     pdl_wait();
@@ -420,24 +457,39 @@ void launch_pdl(Kern k, dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool
     GFX_CUDA(cudaLaunchKernelEx(&cfg, k, args...));
 }
 
-template <int kEpi>
-void gemm(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_off, const __nv_bfloat16* x,
-          __nv_bfloat16* y, const __nv_bfloat16* resid, int T, int K, int N, cudaStream_t s, bool pdl) {
-    if (T % kGM || N % kGN || K % kGK) throw std::runtime_error("bert gemm: T, N multiple of 128, K of 64");
+template <int kEpi, int kBN>
+void gemm_bn(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_off, const __nv_bfloat16* x,
+             __nv_bfloat16* y, const __nv_bfloat16* resid, int T, int K, int N, cudaStream_t s, bool pdl) {
     CUtensorMap tm;
     if (!encode_tensor_map_2d(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, x, static_cast<uint64_t>(K),
                               static_cast<uint64_t>(T), static_cast<uint64_t>(K) * 2, kGK, kGM,
                               CU_TENSOR_MAP_SWIZZLE_128B))
         throw CudaError("cuTensorMapEncodeTiled failed (bert gemm)");
-    GemmArgs a{arena, w_off, b_off, y, resid, K, N, pt};
+    GemmArgs a{arena, w_off, b_off, y, resid, T, K, N, pt};
     static bool attr_set = false;
-    const size_t smem = static_cast<size_t>(kGStage) * kGStages + 1024;
+    const size_t smem = kGSmem + 1024;
+    static int sms = 0;
     if (!attr_set) {
-        GFX_CUDA(cudaFuncSetAttribute(gemm_bf16_kernel<kEpi>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        GFX_CUDA(cudaFuncSetAttribute(gemm_bf16_kernel<kEpi, kBN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(smem)));
+        int dev = 0;
+        GFX_CUDA(cudaGetDevice(&dev));
+        GFX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
         attr_set = true;
     }
-    launch_pdl(gemm_bf16_kernel<kEpi>, dim3(N / kGN, T / kGM), dim3(kGThreads), smem, s, pdl, tm, a);
+    const int tiles = (T / kGM) * (N / kBN);
+    launch_pdl(gemm_bf16_kernel<kEpi, kBN>, dim3(tiles < sms ? tiles : sms), dim3(kGThreads), smem, s, pdl, tm, a);
+}
+
+// 128 x 256 tiles when N leaves enough of them to fill the GPU, else 128 x 128.
+template <int kEpi>
+void gemm(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_off, const __nv_bfloat16* x,
+          __nv_bfloat16* y, const __nv_bfloat16* resid, int T, int K, int N, cudaStream_t s, bool pdl) {
+    if (T % kGM || N % 128 || K % kGK) throw std::runtime_error("bert gemm: T, N multiple of 128, K of 64");
+    if (N % 256 == 0 && (T / kGM) * (N / 256) >= 148)
+        gemm_bn<kEpi, 256>(arena, pt, w_off, b_off, x, y, resid, T, K, N, s, pdl);
+    else
+        gemm_bn<kEpi, 128>(arena, pt, w_off, b_off, x, y, resid, T, K, N, s, pdl);
 }
 
 }  // namespace
