@@ -7,11 +7,15 @@
 //   are the MMA N side), act = ReLU on hidden layers; the last layer also
 //   produces softmax(Y) rows.
 //
-// Precision: fp32 inputs are split v = hi + lo with hi = v with the low 13
-// mantissa bits cleared (exactly representable in TF32) and lo = v - hi
-// (exact). D += W_lo.X_hi + W_hi.X_lo + W_hi.X_hi, FP32 accumulation in TMEM:
-// ~fp32 accuracy (the dropped W_lo.X_lo term is < 2^-20 relative), which the
-// north-star fp32 tolerance (1e-5) requires — plain TF32 would not meet it.
+// Precision: fp32 inputs are split v = hi + lo with hi = v rounded to the
+// nearest TF32 value and lo = v - hi (exact). The B operand stacks the batch
+// planes [X_hi; X_lo] as 64 MMA columns, so per K=8 slice two MMAs
+// (W_lo.[X_hi;X_lo], then W_hi.[X_hi;X_lo]) accumulate all four products into
+// a 128 x 64 fp32 TMEM accumulator; the drain adds the two 32-column halves.
+// ~fp32 accuracy, which the north-star fp32 tolerance (1e-5) requires — plain
+// TF32 would not meet it. (Measured on B200, tools/mma_rate.cu: a tcgen05.mma
+// with M=128 costs ~40 cycles at N=32 and ~48 at N=64, so two N=64 MMAs per
+// slice are 1.6x cheaper than the classic three N=32 3xTF32 products.)
 //
 // Bound: batch 32 gives 16 flop per weight byte; three TF32 MMAs per product
 // still leave the tensor pipe far from its limit, so the kernel is bound by
@@ -27,8 +31,8 @@
 //   warps 2-5   split each landed tile into hi/lo planes of a 2-deep operand
 //               ring (elementwise, so the swizzled layout is preserved),
 //               release the landing slot, fence.proxy.async and arrive;
-//   warp 1      one elected thread issues 12 tcgen05.mma (4 K slices x 3
-//               products) per stage into a 128x32 fp32 TMEM accumulator and
+//   warp 1      one elected thread issues 8 tcgen05.mma (4 K slices x 2
+//               N=64 products) per stage into a 128x64 fp32 TMEM accumulator and
 //               commits the stage back to the producer; accumulators are
 //               double-buffered per chunk of 4 K tiles;
 //   warps 2-5   drain each finished chunk (tcgen05.ld of their 32-lane TMEM
@@ -65,10 +69,13 @@ constexpr uint32_t kXBytes = kRows * kTileK * 4;   // 4 KB
 constexpr uint32_t kLandBytes = kWBytes + kXBytes;           // 20 KB, 1024-aligned
 constexpr uint32_t kOpBytes = 2 * kXBytes;                   // 8 KB: X hi + X lo (W hi/lo live in TMEM)
 constexpr int kCounterDone = 128;  // counters[kCounterDone + tile]: splits done reducing
-// TMEM: columns [0,64) two 32-column fp32 accumulators (double-buffered chunks);
-// operand stage o: W_hi at 64 + 64o, W_lo at 64 + 64o + 32 (lane = weight row, column = k).
+// TMEM: columns [0,128) two 64-column fp32 accumulators (double-buffered
+// chunks; columns 0-31 of one = products with X_hi, 32-63 = with X_lo);
+// operand stage o: W_hi at 128 + 64o, W_lo at 128 + 64o + 32 (lane = weight row, column = k).
+constexpr uint32_t kAccCols = 2 * kRows;
+constexpr uint32_t kOpBase = 2 * kAccCols;
 constexpr uint32_t kTmemCols = 512;
-static_assert(64 + 64 * kOps <= 512, "TMEM budget");
+static_assert(kOpBase + 64 * kOps <= 512, "TMEM budget");
 constexpr int kChunk = 4;           // K tiles accumulated in TMEM before draining to fp32 registers
 
 struct Landing {
@@ -206,27 +213,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 1) {
         // ---------------- MMA issuer ----------------
         if (lane == 0) {
-            constexpr uint32_t idesc = umma_idesc<kTileM, kRows, 2>();  // TF32 x TF32 -> F32
+            constexpr uint32_t idesc = umma_idesc<kTileM, 2 * kRows, 2>();  // TF32 x TF32 -> F32, N = 64
             for (int it = 0; it < nkt; ++it) {
                 const int s = it % kOps;
                 const int chunk = it / kChunk;
-                const uint32_t acc_tmem = tmem + static_cast<uint32_t>((chunk & 1) * 32);
+                const uint32_t acc_tmem = tmem + static_cast<uint32_t>((chunk & 1) * kAccCols);
                 // Chunk c reuses accumulator buffer c&1: wait until chunk c-2 was drained.
                 if (it % kChunk == 0 && chunk >= 2) mbar_wait(&tempty_bar[chunk & 1], ((chunk >> 1) & 1) ^ 1);
                 mbar_wait(&op_full[s], (it / kOps) & 1);
                 tc_fence_after();
                 const Operands st = operands(smem, s);
-                const uint32_t a_hi = tmem + 64u + 64u * static_cast<uint32_t>(s), a_lo = a_hi + 32u;
+                const uint32_t a_hi = tmem + kOpBase + 64u * static_cast<uint32_t>(s), a_lo = a_hi + 32u;
 #pragma unroll
                 for (int kk = 0; kk < kTileK / 8; ++kk) {
-                    const uint32_t off = kk * 32;  // 8 fp32 = 32 bytes of the swizzled X row
-                    const uint64_t bh = umma_desc_sw128(st.x_hi, off), bl = umma_desc_sw128(st.x_lo, off);
+                    // B = [X_hi; X_lo]: 64 K-major rows (x_lo directly follows x_hi).
+                    const uint64_t b = umma_desc_sw128(st.x_hi, kk * 32);
                     const uint32_t ck = static_cast<uint32_t>(kk * 8);  // 8 TMEM columns per K=8 slice
-                    if (!(a.ablate & 4)) {
-                        umma_tf32_ts(acc_tmem, a_lo + ck, bh, idesc, ((it % kChunk) | kk) ? 1u : 0u);  // small terms first
-                        umma_tf32_ts(acc_tmem, a_hi + ck, bl, idesc, 1u);
-                    }
-                    umma_tf32_ts(acc_tmem, a_hi + ck, bh, idesc, ((a.ablate & 4) && ((it % kChunk) | kk) == 0) ? 0u : 1u);
+                    if (!(a.ablate & 4)) umma_tf32_ts(acc_tmem, a_lo + ck, b, idesc, ((it % kChunk) | kk) ? 1u : 0u);
+                    umma_tf32_ts(acc_tmem, a_hi + ck, b, idesc, ((a.ablate & 4) && ((it % kChunk) | kk) == 0) ? 0u : 1u);
                 }
                 umma_commit(&op_empty[s]);  // operand buffer free once these MMAs retire
                 if (it % kChunk == kChunk - 1 || it == nkt - 1) umma_commit(&tfull_bar[chunk & 1]);
@@ -270,8 +274,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_arrive(&land_empty[s]);  // landing slot back to the TMA producer
             tc_fence_after();             // order after the MMAs that last read stage o
             const uint32_t lane_base = tmem + (static_cast<uint32_t>(q * 32) << 16);
-            tmem_st_32x32b_x32(lane_base + 64u + 64u * static_cast<uint32_t>(o), whi);
-            tmem_st_32x32b_x32(lane_base + 96u + 64u * static_cast<uint32_t>(o), wlo);
+            tmem_st_32x32b_x32(lane_base + kOpBase + 64u * static_cast<uint32_t>(o), whi);
+            tmem_st_32x32b_x32(lane_base + kOpBase + 32u + 64u * static_cast<uint32_t>(o), wlo);
 #pragma unroll
             for (int j = 0; j < static_cast<int>(kXBytes / 16 / 128); ++j) {
                 float4 hi, lo;
@@ -303,10 +307,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int c = 0; c < nchunks; ++c) {
             mbar_wait(&tfull_bar[c & 1], (c >> 1) & 1);
             tc_fence_after();
-            float part[kRows];
-            tmem_ld_32x32b_x32(tmem + static_cast<uint32_t>((c & 1) * 32) + (static_cast<uint32_t>(q * 32) << 16), part);
+            float ph[kRows], pl[kRows];
+            const uint32_t src = tmem + static_cast<uint32_t>((c & 1) * kAccCols) + (static_cast<uint32_t>(q * 32) << 16);
+            tmem_ld_32x32b_x32(src + kRows, pl);  // products with X_lo (small)
+            tmem_ld_32x32b_x32(src, ph);
 #pragma unroll
-            for (int b = 0; b < kRows; ++b) acc[b] += part[b];
+            for (int b = 0; b < kRows; ++b) acc[b] += ph[b] + pl[b];
             tc_fence_before();
             mbar_arrive(&tempty_bar[c & 1]);
         }
