@@ -318,13 +318,13 @@ def main():
         "service_p50_ms": round(r.service_p50_ms, 4), "service_p99_ms": round(r.service_p99_ms, 4),
         "hit_rate": round(r.hits / max(1, r.hits + r.misses), 6), "misses": int(r.misses),
         "decision_digest": f"{int(r.decision_digest):016x}",
-        "roofline": {"kernel": "K1 forward: mlp_tc_kernel x layers (tcgen05 3xTF32) + softmax_rows_kernel", "bound": "hbm",
+        "roofline": {"kernel": "K1 v6 mlp_forward_kernel (whole forward, one persistent launch, tcgen05 3xTF32)", "bound": "hbm",
                      "achieved": round(achieved, 1), "peak": peaks.get("hbm_gbs"), "unit": "GB/s",
                      "frac": round(achieved / peaks.get("hbm_gbs", 1), 4), "traffic": ncu_traffic(),
                      "peak_source": peak_kind,
                      "tflops": round(flops / (kernel_ms / 1e3) / 1e12, 3) if kernel_ms else 0,
                      "kernel_ms_per_step": round(kernel_ms / a.steps / max(1, world), 3),
-                     "note": "algorithmic bytes = fp32 weights+biases + batch-32 in/out activations per inference; time = CUDA events on the compute stream around each inference (all layer launches + softmax), summed over the step"},
+                     "note": "algorithmic bytes = fp32 weights+biases + batch-32 in/out activations per inference; time = CUDA events on the compute stream around each inference launch, summed over the step"},
         "load_roofline": {"path": "pinned-host H2D (copy engine)", "achieved": round(h2d_bytes / (h2d_ms * 1e6), 2)
                           if h2d_ms else 0, "peak": H2D_PEAK_GBS, "unit": "GB/s",
                           "frac": round(h2d_bytes / (h2d_ms * 1e6) / H2D_PEAK_GBS, 4) if h2d_ms else 0,

@@ -254,6 +254,10 @@ GpuManager::GpuManager(int device, uint64_t capacity_bytes, int manager_id) : de
     GFX_CUDA(cudaMalloc(&counters_, sizeof(unsigned) * ncnt));
     GFX_CUDA(cudaMalloc(&stats_, sizeof(float) * 2 * kBatch * ncnt));
     GFX_CUDA(cudaMemset(counters_, 0, sizeof(unsigned) * ncnt));
+    GFX_CUDA(cudaMalloc(&fwd_opnd_, kMlpOpndLayerBytes * GFX_MAX_LAYERS));
+    GFX_CUDA(cudaMalloc(&fwd_part_, sizeof(float) * kMlpPartLayerFloats * GFX_MAX_LAYERS));
+    GFX_CUDA(cudaMalloc(&fwd_cnt_, sizeof(unsigned) * kMlpCounters));
+    GFX_CUDA(cudaMemset(fwd_cnt_, 0, sizeof(unsigned) * kMlpCounters));
     GFX_CUDA(cudaDeviceSynchronize());
 }
 
@@ -271,6 +275,9 @@ GpuManager::~GpuManager() {
     cudaFree(ws_);
     cudaFree(counters_);
     cudaFree(stats_);
+    cudaFree(fwd_opnd_);
+    cudaFree(fwd_part_);
+    cudaFree(fwd_cnt_);
     bert_ws_.release();
     cudaStreamDestroy(compute_);
     cudaStreamDestroy(copy_);
@@ -406,6 +413,119 @@ void GpuManager::infer(int model, const void* in_v, void* out_v, void* debug_hid
     }
     const float* in = static_cast<const float*>(in_v);
     float* out = static_cast<float*>(out_v);
+    static const bool layerwise = std::getenv("GFX_MLP_LAYERWISE") != nullptr;  // debug A/B: K1 v5 per-layer path
+    if (!layerwise) {
+        MlpFwdArgs f{};
+        f.arena = arena_;
+        build_page_table(s, f.pt);
+        f.in = in;
+        f.L = blob.desc.n_layers;
+        f.logits = out;
+        f.probs = out + static_cast<size_t>(kBatch) * blob.desc.dims[f.L];
+        f.opnd = fwd_opnd_;
+        f.part = fwd_part_;
+        f.cnt = fwd_cnt_;
+        f.grid = sm_count_;
+        static const int ablate = std::getenv("GFX_MLP_ABLATE") ? std::atoi(std::getenv("GFX_MLP_ABLATE")) : 0;
+        f.ablate = ablate;
+        for (int l = 0; l < f.L; ++l) {
+            MlpFwdLayer& ly = f.layer[l];
+            ly.w_off = blob.w_off[l];
+            ly.b_off = blob.b_off[l];
+            ly.K = blob.desc.dims[l];
+            ly.N = blob.desc.dims[l + 1];
+            ly.tiles = (ly.N + kWTileRows - 1) / kWTileRows;
+            ly.splits = mlp_fwd_splits(ly.K, ly.N, f.grid);
+        }
+        static const bool trace_on = std::getenv("GFX_TRACE_MLP") != nullptr;
+        if (trace_on) {
+            GFX_CUDA(cudaMalloc(&f.trace, sizeof(unsigned long long) * (32 * f.grid + 576 + 16 * f.grid)));
+            GFX_CUDA(cudaMemset(f.trace, 0, sizeof(unsigned long long) * (32 * f.grid + 576 + 16 * f.grid)));
+        }
+        if (layer_timer) GFX_CUDA(cudaEventRecord(layer_timer->next(), compute_));
+        static const int repeat = std::getenv("GFX_MLP_REPEAT") ? std::atoi(std::getenv("GFX_MLP_REPEAT")) : 0;
+        if (repeat > 0) {  // debug: device time of back-to-back forwards of this model (CUDA events)
+            cudaEvent_t e0, e1;
+            GFX_CUDA(cudaEventCreate(&e0));
+            GFX_CUDA(cudaEventCreate(&e1));
+            GFX_CUDA(cudaEventRecord(e0, compute_));
+            for (int r = 0; r < repeat; ++r) {
+                f.epoch = fwd_epoch_++;
+                launch_mlp_forward(f, compute_);
+            }
+            GFX_CUDA(cudaEventRecord(e1, compute_));
+            GFX_CUDA(cudaEventSynchronize(e1));
+            float ms = 0;
+            GFX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+            std::fprintf(stderr, "[repeat] model %d: %.2f us per forward (%d back-to-back launches)\n", model,
+                         1e3 * ms / repeat, repeat);
+            GFX_CUDA(cudaEventDestroy(e0));
+            GFX_CUDA(cudaEventDestroy(e1));
+        }
+        f.epoch = fwd_epoch_++;
+        launch_mlp_forward(f, compute_);
+        ++kernel_launches;
+        if (trace_on) {  // debug timeline: µs after the first CTA started, min / median / max over CTAs
+            std::vector<unsigned long long> tr(static_cast<size_t>(48) * f.grid + 576);
+            GFX_CUDA(cudaStreamSynchronize(compute_));
+            GFX_CUDA(cudaMemcpy(tr.data(), f.trace, tr.size() * 8, cudaMemcpyDeviceToHost));
+            GFX_CUDA(cudaFree(f.trace));
+            unsigned long long t0 = ~0ull;
+            const size_t nct = static_cast<size_t>(f.grid) * 32;
+            for (size_t i = 0; i < nct; i += 32) t0 = std::min(t0, tr[i]);
+            static const char* names[4] = {"mma first", "mma last", "epi start", "tile done"};
+            std::fprintf(stderr, "[trace] model %d grid %d\n", model, f.grid);
+            for (int ph = 0; ph < 32; ++ph) {
+                std::vector<double> v;
+                for (size_t i = 0; i < nct; i += 32)
+                    if (tr[i + static_cast<size_t>(ph)]) v.push_back((tr[i + static_cast<size_t>(ph)] - t0) * 1e-3);
+                if (v.empty()) continue;
+                std::sort(v.begin(), v.end());
+                char nm[32];
+                if (ph == 0) std::snprintf(nm, sizeof nm, "start");
+                else if (ph == 1) std::snprintf(nm, sizeof nm, "setup");
+                else if (ph == 31) std::snprintf(nm, sizeof nm, "end");
+                else if (ph >= 26 && ph < 30) std::snprintf(nm, sizeof nm, "L%d %s", (ph - 26) / 2, ph % 2 ? "gathered" : "siblings");
+                else if (ph >= 18 && ph <= 30 && f.L <= 4) {
+                    static const char* sub[13] = {"L0 part stored", "L0 fenced", "L0 arrived", "L0 sib seen", "L0 cp.async issued",
+                                                  "L0 cp.async done", "L0 emitted", "L0 done-sync", "", "", "", "", "L0 done fenced"};
+                    std::snprintf(nm, sizeof nm, "%s", sub[ph - 18]);
+                }
+                else std::snprintf(nm, sizeof nm, "L%d %s", (ph - 2) / 4, names[(ph - 2) % 4]);
+                std::fprintf(stderr, "  %-16s n=%3zu %8.2f %8.2f %8.2f\n", nm, v.size(), v.front(), v[v.size() / 2],
+                             v.back());
+            }
+            std::fprintf(stderr, "  CTA 0 steps (us): Wreq Xreq Wlanded WloDone xFull mmaIssued\n");
+            for (int st = 0; st < 64; ++st) {
+                const unsigned long long* p = tr.data() + nct + st * 8;
+                if (!p[0] && !p[5]) break;
+                auto us = [&](unsigned long long t) { return t ? (t - t0) * 1e-3 : -1.0; };
+                std::fprintf(stderr, "   %2d %7.2f %7.2f %7.2f %7.2f %7.2f %7.2f\n", st, us(p[0]), us(p[1]), us(p[2]),
+                             us(p[3]), us(p[4]), us(p[5]));
+            }
+            static const char* pn[16] = {"mma: wait tempty", "mma: wait ready", "", "",
+                                         "mma: commits+rest", "conv: wait w_full", "", "conv: work",
+                                         "wprod: wait slot", "xprod: wait slot", "xprod: wait flag", "drain: wait tfull",
+                                         "drain: epilogue", "mma: MMAs", "", "steps"};
+            std::fprintf(stderr, "  cycles per CTA, mean over CTAs with work (per step in brackets):\n");
+            for (int i = 0; i < 16; ++i) {
+                if (!pn[i][0]) continue;
+                double sum = 0, steps = 0;
+                int n = 0;
+                for (int c = 0; c < f.grid; ++c) {
+                    const unsigned long long st = tr[nct + 576 + c * 16 + 15];
+                    if (!st) continue;
+                    sum += static_cast<double>(tr[nct + 576 + c * 16 + i]);
+                    steps += static_cast<double>(st);
+                    ++n;
+                }
+                if (n) std::fprintf(stderr, "   %-22s %10.0f  (%7.1f)\n", pn[i], sum / n, sum / steps);
+            }
+        }
+        if (layer_timer) GFX_CUDA(cudaEventRecord(layer_timer->next(), compute_));
+        GFX_CUDA(cudaEventRecord(s.last_use, compute_));
+        return;
+    }
     MlpLayerArgs a{};
     a.arena = arena_;
     build_page_table(s, a.pt);
@@ -482,6 +602,7 @@ void GpuManager::reset() {
         s.live = false;
     }
     GFX_CUDA(cudaMemset(counters_, 0, sizeof(unsigned) * 512));
+    GFX_CUDA(cudaMemset(fwd_cnt_, 0, sizeof(unsigned) * kMlpCounters));
     GFX_CUDA(cudaDeviceSynchronize());
 }
 

@@ -122,6 +122,11 @@ private:
     unsigned* counters_ = nullptr;
     float* stats_ = nullptr;
     int max_dim_ = 0;
+    // K1 v6 forward workspace
+    char* fwd_opnd_ = nullptr;
+    float* fwd_part_ = nullptr;
+    unsigned* fwd_cnt_ = nullptr;
+    unsigned fwd_epoch_ = 0;  // launches of the forward kernel on this manager's workspace
 };
 
 }  // namespace gfx

@@ -1,4 +1,5 @@
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstddef>
@@ -40,6 +41,40 @@ void launch_softmax_rows(const float* logits, float* probs, int rows, int C, cud
 // Fills `count` consecutive tensors of n values, tensor t from seed + t.
 void launch_fill_params(float* dst, uint64_t n, uint64_t seed, uint32_t tensor, float scale, cudaStream_t s,
                         uint64_t count = 1);
+
+// K1 v6: whole forward in one persistent cooperative launch (mlp_fwd.cu).
+constexpr int kMlpMaxDim = 8192;
+constexpr size_t kMlpOpndLayerBytes = static_cast<size_t>(kMlpMaxDim / 32) * 8192;  // operand blocks per layer input
+constexpr size_t kMlpPartLayerFloats = static_cast<size_t>(160) * 32 * 128;        // split-K partials per layer
+constexpr int kMlpCounters = 8192;
+
+struct MlpFwdLayer {
+    uint64_t w_off, b_off;  // model-blob offsets of the weight tiles and the bias
+    int K, N;
+    int tiles, splits;      // units = tiles x splits <= grid
+};
+
+struct MlpFwdArgs {
+    CUtensorMap tmap_in;    // layer-0 input tiles (filled by launch_mlp_forward)
+    const char* arena;
+    const float* in;        // [32 x K0] request input, row-major
+    float* logits;          // [32 x C]
+    float* probs;           // [32 x C] softmax rows
+    char* opnd;             // operand blocks, layer l's input at opnd + l * kMlpOpndLayerBytes
+    float* part;            // split-K partials, layer l at part + l * kMlpPartLayerFloats
+    unsigned* cnt;          // kMlpCounters dataflow counters: two banks, bank (epoch & 1) zero at launch
+    unsigned epoch;         // launch sequence number on this workspace (stream-ordered)
+    int L;
+    int grid;
+    int ablate;             // debug bitmask (0 in production): 1 = W_hi taken as rn_tf32 instead of trunc
+    unsigned long long* trace;  // debug (GFX_TRACE_MLP): [grid][32] %globaltimer marks, else nullptr
+    MlpFwdLayer layer[GFX_MAX_LAYERS];
+    PageTable pt;
+};
+
+int mlp_fwd_splits(int K, int N, int grid);
+size_t mlp_fwd_smem();
+void launch_mlp_forward(MlpFwdArgs& a, cudaStream_t stream);
 
 // Weight tiles of the blob: 128 x 32 fp32, K-major SWIZZLE_128B image (16 KB).
 constexpr int kWTileRows = 128;
