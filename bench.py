@@ -34,6 +34,7 @@ sys.path.insert(0, ROOT)
 METRIC = "trace-replay requests/sec + p50/p99 latency at 1/2/4/8 B200; cache hit rate"
 H2D_PEAK_GBS = 55.6       # measured pinned H2D, 1 GiB copies on this pool (gpurun_out/probe.txt)
 HOST_LINK_NOMINAL = 64.0  # PCIe Gen5 x16 per direction, nominal
+NVLINK_PEER_GBS = 770.0   # measured peer copy per direction on this pool (B200_PROFILING.md)
 
 
 def parse():
@@ -238,7 +239,11 @@ def main():
     ndev = 1 if world == 1 and G == 1 else G
     if world == 1 and G > 1:
         ndev = G  # single process driving G devices
-    rep = gfx.Replay(cat, cfg, n_devices=ndev, only_gpu=only, record_kernels=True, record_requests=True)
+    p2p = G > 1  # false misses fetch from the lowest-id holder over NVLink (in-process or CUDA IPC)
+    rep = gfx.Replay(cat, cfg, n_devices=ndev, only_gpu=only, use_p2p=p2p, record_kernels=True,
+                     record_requests=True)
+    if world > 1:
+        rep.connect_peers()
 
     for _ in range(a.warmup):
         rep.run()
@@ -261,6 +266,9 @@ def main():
     flops = allreduce_sum(world, sum(x.mlp_flops for x in res))
     h2d_bytes = allreduce_sum(world, sum(x.h2d_bytes for x in res))
     h2d_ms = allreduce_sum(world, sum(x.h2d_ms for x in res))
+    p2p_loads = int(allreduce_sum(world, sum(x.loads_p2p for x in res)))
+    p2p_bytes = allreduce_sum(world, sum(x.p2p_bytes for x in res))
+    p2p_ms = allreduce_sum(world, sum(x.p2p_ms for x in res))
     rep.close()
 
     # e2e: same replay with host buffers through the public C-ABI.
@@ -278,7 +286,10 @@ def main():
     for i in range(n):
         gfx._ffi.check(gfx._ffi.gfx_host_fill_params(hin[i].ctypes.data, hin.shape[1],
                                                      gfx._ffi.gfx_input_seed(i), 0xFFFFFFFF, 1.0))
-    rep2 = gfx.Replay(cat, cfg, n_devices=ndev, only_gpu=only, host_io=True, host_inputs=hin, host_outputs=hout)
+    rep2 = gfx.Replay(cat, cfg, n_devices=ndev, only_gpu=only, use_p2p=p2p, host_io=True, host_inputs=hin,
+                      host_outputs=hout)
+    if world > 1:
+        rep2.connect_peers()
     for _ in range(max(1, a.warmup)):
         rep2.run()
     barrier(world)
@@ -329,7 +340,12 @@ def main():
         "load_roofline": {"path": "pinned-host H2D (copy engine)", "achieved": round(h2d_bytes / (h2d_ms * 1e6), 2)
                           if h2d_ms else 0, "peak": H2D_PEAK_GBS, "unit": "GB/s",
                           "frac": round(h2d_bytes / (h2d_ms * 1e6) / H2D_PEAK_GBS, 4) if h2d_ms else 0,
-                          "nominal_pcie_gbs": HOST_LINK_NOMINAL, "bytes_per_step": int(r.h2d_bytes)},
+                          "nominal_pcie_gbs": HOST_LINK_NOMINAL, "bytes_per_step": int(r.h2d_bytes),
+                          "note": "achieved = H2D bytes / summed H2D load-event time; NVLink peer fetches (G > 1) "
+                                  "are timed separately (p2p_*)",
+                          "p2p_loads_per_step": p2p_loads // a.steps, "p2p_bytes_per_step": int(p2p_bytes // a.steps),
+                          "p2p_achieved_gbs": round(p2p_bytes / (p2p_ms * 1e6), 2) if p2p_ms else None,
+                          "p2p_peak_gbs": NVLINK_PEER_GBS},
         "e2e": {"value": round(e2e_val, 2), "unit": "requests/s",
                 "h2d_bytes_per_step": int(er.io_h2d_bytes + er.h2d_bytes), "d2h_bytes_per_step": int(er.io_d2h_bytes),
                 "note": "gfx_replay with pinned host inputs/outputs; request I/O + model loads inside the timed region"},

@@ -194,6 +194,7 @@ typedef struct {
     double sim_p50_s, sim_p99_s, sim_avg_latency_s; /* virtual-time latency from the schedule */
     double mlp_flops;            /* algorithmic flops of all inferences */
     double mlp_weight_bytes;     /* algorithmic weight+activation bytes of all inferences */
+    double p2p_ms;               /* sum of peer-fetch (NVLink) event times */
 } gfx_replay_result;
 
 /* Reusable replay context: managers, device buffers and timing events are
@@ -206,6 +207,17 @@ int gfx_replay_run(gfx_replay_t r, gfx_replay_result* out);
 int gfx_replay_outputs(gfx_replay_t r, void* host, uint64_t bytes);
 /* Per-request model row and device service time (ms) of the last run. */
 int gfx_replay_requests(gfx_replay_t r, int32_t* model_idx, double* service_ms, int64_t n);
+/* One process per GPU (only_gpu >= 0, use_p2p): NVLink peer fetch between
+ * processes. Each rank exports its arena and flag words as a CUDA IPC blob,
+ * the ranks exchange blobs (e.g. an all-gather over torch.distributed), and
+ * every rank imports all gpu_count blobs (index = GPU id) before the first
+ * run. Ordering is device-side (cuStreamWaitValue32 / WriteValue32 on the
+ * flag words); page tables of peer arenas are derived from the shared
+ * deterministic schedule. Replaces nothing in the reference (its loads are
+ * constants, proj/src/cluster.cpp:163-167). */
+uint64_t gfx_replay_ipc_blob_bytes(void);
+int gfx_replay_ipc_export(gfx_replay_t r, void* blob, uint64_t bytes);
+int gfx_replay_ipc_import(gfx_replay_t r, const void* blobs, int32_t n);
 int gfx_replay_destroy(gfx_replay_t r);
 /* create + run + destroy */
 int gfx_replay(const gfx_replay_args* args, gfx_replay_result* out);

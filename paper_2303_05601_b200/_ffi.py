@@ -54,7 +54,7 @@ class ReplayResultC(C.Structure):
                                    "io_d2h_bytes")] + [
         (n, C.c_double) for n in ("device_ms", "host_ms", "sched_ms", "kernel_ms", "h2d_ms",
                                    "service_p50_ms", "service_p99_ms", "sim_p50_s", "sim_p99_s",
-                                   "sim_avg_latency_s", "mlp_flops", "mlp_weight_bytes")]
+                                   "sim_avg_latency_s", "mlp_flops", "mlp_weight_bytes", "p2p_ms")]
 
 
 def _sig(name, res, args):
@@ -100,6 +100,9 @@ gfx_replay_run = _sig("gfx_replay_run", C.c_int, [_vp, C.POINTER(ReplayResultC)]
 gfx_replay_outputs = _sig("gfx_replay_outputs", C.c_int, [_vp, _vp, C.c_uint64])
 gfx_replay_requests = _sig("gfx_replay_requests", C.c_int, [_vp, _vp, _vp, C.c_int64])
 gfx_replay_destroy = _sig("gfx_replay_destroy", C.c_int, [_vp])
+gfx_replay_ipc_blob_bytes = _sig("gfx_replay_ipc_blob_bytes", C.c_uint64, [])
+gfx_replay_ipc_export = _sig("gfx_replay_ipc_export", C.c_int, [_vp, _vp, C.c_uint64])
+gfx_replay_ipc_import = _sig("gfx_replay_ipc_import", C.c_int, [_vp, _vp, C.c_int32])
 
 
 def check(rc: int):

@@ -11,6 +11,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstring>
+#include <set>
 #include <chrono>
 #include <cmath>
 #include <memory>
@@ -103,9 +105,76 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
     int family = 0;
     bool full_outputs = false;
     // timing
-    KernelTimer layer_timer, load_timer, req_timer;
+    KernelTimer layer_timer, load_timer, p2p_timer, req_timer;
     std::vector<cudaEvent_t> req_start, req_end;
     std::vector<int> req_gpu;
+    // ---- cross-process peers (one process per GPU, only_gpu mode) ----
+    // Another rank's GPU: its arena and flag words mapped by CUDA IPC, plus a
+    // host shadow of its page allocator. The shadow is exact because every
+    // rank runs the same bit-exact control plane and a manager allocates the
+    // lowest free pages (GpuManager::allocate), so the page table of any model
+    // on any GPU is known here without asking that rank.
+    struct RemoteArena {
+        char* arena = nullptr;
+        uint32_t* flags = nullptr;
+        uint32_t npages = 0;
+        std::set<uint32_t> free;
+        std::vector<std::vector<uint32_t>> pages;
+        void reset() {
+            free.clear();
+            for (uint32_t p = 0; p < npages; ++p) free.insert(p);
+            for (auto& v : pages) v.clear();
+        }
+        void evict(int m) {
+            for (uint32_t p : pages[static_cast<size_t>(m)]) free.insert(p);
+            pages[static_cast<size_t>(m)].clear();
+        }
+        void load(int m, uint32_t n) {
+            auto& v = pages[static_cast<size_t>(m)];
+            v.clear();
+            for (uint32_t i = 0; i < n; ++i) {
+                v.push_back(*free.begin());
+                free.erase(free.begin());
+            }
+        }
+    };
+    std::vector<RemoteArena> remotes;  // index = GPU id (unused for only_gpu)
+    // This rank's flag words (device, IPC-exported), written by peers' copy
+    // streams: loaded[s][m] = loads of model m completed on GPU s (so far, all
+    // runs), read_done[m][r] = fetches of our model m completed by GPU r.
+    uint32_t* flags = nullptr;
+    bool ipc = false;
+    size_t M = 0;
+    std::vector<uint32_t> load_cnt;   // [G][M] loads decided so far (all runs)
+    std::vector<uint32_t> fetch_cnt;  // [G src][M][G reader] peer fetches decided so far
+    size_t fl_loaded(int g, int m) const { return static_cast<size_t>(g) * M + static_cast<size_t>(m); }
+    size_t fl_read(int m, int r) const {
+        return static_cast<size_t>(gpu_count()) * M + static_cast<size_t>(m) * gpu_count() + static_cast<size_t>(r);
+    }
+    uint32_t& fetches(int src, int m, int r) {
+        return fetch_cnt[(static_cast<size_t>(src) * M + static_cast<size_t>(m)) * gpu_count() + static_cast<size_t>(r)];
+    }
+    bool remote_fetch(int gpu, int source) const {
+        return ipc && args.use_p2p && source >= 0 && source != gpu;
+    }
+    // Host bookkeeping of every GPU's dispatch (all ranks see the whole stream).
+    void track(int gpu, int model, bool hit, const std::vector<int>& evicted, int source) {
+        if (hit) return;
+        const bool mine = gpu == args.only_gpu;
+        for (int v : evicted)
+            if (!mine) remotes[static_cast<size_t>(gpu)].evict(v);
+        if (remote_fetch(gpu, source)) ++fetches(source, model, gpu);
+        if (!mine) remotes[static_cast<size_t>(gpu)].load(model, ModelStore::get().at(model).pages);
+        ++load_cnt[fl_loaded(gpu, model)];
+    }
+    // Before our pages of model v are reused: every peer fetch of v decided so far has completed.
+    void wait_peer_reads(GpuManager& m, int v) {
+        for (int r = 0; r < gpu_count(); ++r) {
+            const uint32_t c = fetches(args.only_gpu, v, r);
+            if (c) m.copy_wait_geq(flags + fl_read(v, r), c);
+        }
+    }
+
     // counters of the current run
     gfx_replay_result res{};
     std::vector<cudaEvent_t> pending_in;  // per GPU: event of the last input copy
@@ -149,6 +218,7 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
             mgrs[g] = std::make_unique<GpuManager>(dev_of[g], cap_bytes, g);
             mgrs[g]->layer_timer = args.record_kernels ? &layer_timer : nullptr;
             mgrs[g]->load_timer = &load_timer;
+            mgrs[g]->p2p_timer = &p2p_timer;
             DevBufs& b = bufs[g];
             GFX_CUDA(cudaSetDevice(dev_of[g]));
             // Inputs: every request this GPU might serve (ids are global).
@@ -186,10 +256,67 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
         req_start.assign(n, nullptr);
         req_end.assign(n, nullptr);
         req_gpu.assign(n, -1);
+        M = catalog.size();
+        if (args.only_gpu >= 0) {
+            GFX_CUDA(cudaSetDevice(dev_of[static_cast<size_t>(args.only_gpu)]));
+            const size_t words = 2 * static_cast<size_t>(G) * M;
+            GFX_CUDA(cudaMalloc(&flags, words * 4));
+            GFX_CUDA(cudaMemset(flags, 0, words * 4));
+            GFX_CUDA(cudaDeviceSynchronize());
+            load_cnt.assign(static_cast<size_t>(G) * M, 0);
+            fetch_cnt.assign(static_cast<size_t>(G) * M * static_cast<size_t>(G), 0);
+        }
+    }
+
+    struct IpcBlob {
+        cudaIpcMemHandle_t arena;
+        cudaIpcMemHandle_t flags;
+        uint64_t arena_pages;
+        int32_t gpu;
+        int32_t models;
+    };
+
+    void ipc_export(void* out, uint64_t bytes) {
+        if (args.only_gpu < 0) throw std::invalid_argument("ipc export needs only_gpu (one process per GPU)");
+        if (bytes < sizeof(IpcBlob)) throw std::invalid_argument("ipc blob buffer too small");
+        GpuManager& m = *mgrs[static_cast<size_t>(args.only_gpu)];
+        m.activate();
+        IpcBlob b{};
+        GFX_CUDA(cudaIpcGetMemHandle(&b.arena, m.arena()));
+        GFX_CUDA(cudaIpcGetMemHandle(&b.flags, flags));
+        b.arena_pages = m.total_pages();
+        b.gpu = args.only_gpu;
+        b.models = static_cast<int32_t>(M);
+        std::memcpy(out, &b, sizeof b);
+    }
+
+    void ipc_import(const void* blobs, int n) {
+        if (args.only_gpu < 0) throw std::invalid_argument("ipc import needs only_gpu (one process per GPU)");
+        if (n != gpu_count()) throw std::invalid_argument("ipc import needs one blob per GPU");
+        GFX_CUDA(cudaSetDevice(dev_of[static_cast<size_t>(args.only_gpu)]));
+        remotes.assign(static_cast<size_t>(n), RemoteArena{});
+        const IpcBlob* b = static_cast<const IpcBlob*>(blobs);
+        for (int g = 0; g < n; ++g) {
+            if (b[g].gpu != g || static_cast<size_t>(b[g].models) != M)
+                throw std::invalid_argument("ipc blob " + std::to_string(g) + " is not GPU " + std::to_string(g) +
+                                            " of the same catalog");
+            if (g == args.only_gpu) continue;
+            RemoteArena& ra = remotes[static_cast<size_t>(g)];
+            void* p = nullptr;
+            GFX_CUDA(cudaIpcOpenMemHandle(&p, b[g].arena, cudaIpcMemLazyEnablePeerAccess));
+            ra.arena = static_cast<char*>(p);
+            GFX_CUDA(cudaIpcOpenMemHandle(&p, b[g].flags, cudaIpcMemLazyEnablePeerAccess));
+            ra.flags = static_cast<uint32_t*>(p);
+            ra.npages = static_cast<uint32_t>(b[g].arena_pages);
+            ra.pages.assign(M, {});
+            ra.reset();
+        }
+        ipc = true;
     }
 
     void on_begin_execution(int gpu, const gpufaas::Request& req, int model, bool hit,
                             const std::vector<int>& evicted, int source, gpufaas::SimTime, gpufaas::SimTime) override {
+        if (ipc) track(gpu, model, hit, evicted, source);
         if (args.only_gpu >= 0 && gpu != args.only_gpu) return;
         GpuManager& m = *mgrs[static_cast<size_t>(gpu)];
         DevBufs& b = bufs[static_cast<size_t>(gpu)];
@@ -203,19 +330,40 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
         }
         if (!hit) {
             if (e0) GFX_CUDA(cudaEventRecord(e0, m.copy_stream()));
-            for (int v : evicted) m.evict(v);
+            for (int v : evicted) {
+                if (ipc) wait_peer_reads(m, v);
+                m.evict(v);
+            }
             GpuManager* src = nullptr;
             if (args.use_p2p && source >= 0 && mgrs[static_cast<size_t>(source)] &&
                 mgrs[static_cast<size_t>(source)]->resident(model))
                 src = mgrs[static_cast<size_t>(source)].get();
-            const uint64_t bytes = m.load(model, src);
-            if (src) {
+            if (remote_fetch(gpu, source)) {
+                // Another rank holds it: NVLink fetch out of its IPC-mapped
+                // arena once its load counter shows the load complete, then
+                // tell it our read is done (it waits on that before reusing
+                // the pages).
+                RemoteArena& ra = remotes[static_cast<size_t>(source)];
+                const uint64_t bytes = m.load_remote(model, ra.arena, ra.pages[static_cast<size_t>(model)],
+                                                     flags + fl_loaded(source, model),
+                                                     load_cnt[fl_loaded(source, model)]);
+                m.copy_write(ra.flags + fl_read(model, gpu), fetches(source, model, gpu));
                 res.loads_p2p++;
                 res.p2p_bytes += bytes;
             } else {
-                res.loads_h2d++;
-                res.h2d_bytes += bytes;
+                const uint64_t bytes = m.load(model, src);
+                if (src) {
+                    res.loads_p2p++;
+                    res.p2p_bytes += bytes;
+                } else {
+                    res.loads_h2d++;
+                    res.h2d_bytes += bytes;
+                }
             }
+            if (ipc)  // our load of `model` is complete: publish the count to every peer
+                for (int r = 0; r < gpu_count(); ++r)
+                    if (r != gpu) m.copy_write(remotes[static_cast<size_t>(r)].flags + fl_loaded(gpu, model),
+                                               load_cnt[fl_loaded(gpu, model)]);
         } else if (e0) {
             GFX_CUDA(cudaEventRecord(e0, m.compute_stream()));
         }
@@ -253,15 +401,19 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
 
     void run(gfx_replay_result* out) {
         res = gfx_replay_result{};
-        layer_timer.used = load_timer.used = req_timer.used = 0;
+        layer_timer.used = load_timer.used = p2p_timer.used = req_timer.used = 0;
         std::fill(req_start.begin(), req_start.end(), nullptr);
         std::fill(req_end.begin(), req_end.end(), nullptr);
         const int G = gpu_count();
         for (int g = 0; g < G; ++g) {
             if (!mgrs[g]) continue;
+            if (ipc)  // peers may still be reading our pages from the previous run
+                for (int v = 0; v < static_cast<int>(M); ++v) wait_peer_reads(*mgrs[g], v);
             mgrs[g]->reset();
             mgrs[g]->kernel_launches = 0;
         }
+        for (RemoteArena& ra : remotes)
+            if (ra.arena) ra.reset();
         const auto h0 = std::chrono::steady_clock::now();
         for (int g = 0; g < G; ++g) {
             if (!mgrs[g]) continue;
@@ -331,6 +483,8 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
             res.kernel_ms += elapsed_ms(layer_timer.ev[i], layer_timer.ev[i + 1]);
         for (size_t i = 0; i + 1 < load_timer.used; i += 2)
             res.h2d_ms += elapsed_ms(load_timer.ev[i], load_timer.ev[i + 1]);
+        for (size_t i = 0; i + 1 < p2p_timer.used; i += 2)
+            res.p2p_ms += elapsed_ms(p2p_timer.ev[i], p2p_timer.ev[i + 1]);
         if (args.record_requests) {
             std::vector<double> svc;
             for (size_t r = 0; r < req_start.size(); ++r)
@@ -362,8 +516,13 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
             cudaEventDestroy(bufs[g].start);
             cudaEventDestroy(bufs[g].stop);
         }
-        for (KernelTimer* t : {&layer_timer, &load_timer, &req_timer})
+        for (KernelTimer* t : {&layer_timer, &load_timer, &p2p_timer, &req_timer})
             for (cudaEvent_t e : t->ev) cudaEventDestroy(e);
+        for (RemoteArena& ra : remotes) {
+            if (ra.arena) cudaIpcCloseMemHandle(ra.arena);
+            if (ra.flags) cudaIpcCloseMemHandle(ra.flags);
+        }
+        if (flags) cudaFree(flags);
     }
 };
 
@@ -619,6 +778,13 @@ int gfx_replay_requests(gfx_replay_t r, int32_t* model_idx, double* service_ms, 
                                     : -1.0;
         }
     });
+}
+uint64_t gfx_replay_ipc_blob_bytes(void) { return sizeof(gfx_replay_s::IpcBlob); }
+int gfx_replay_ipc_export(gfx_replay_t r, void* blob, uint64_t bytes) {
+    return guarded([&] { r->ipc_export(blob, bytes); });
+}
+int gfx_replay_ipc_import(gfx_replay_t r, const void* blobs, int32_t n) {
+    return guarded([&] { r->ipc_import(blobs, n); });
 }
 int gfx_replay_destroy(gfx_replay_t r) {
     return guarded([&] { delete r; });

@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <stdexcept>
 
@@ -486,7 +487,8 @@ template <int kEpi>
 void gemm(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_off, const __nv_bfloat16* x,
           __nv_bfloat16* y, const __nv_bfloat16* resid, int T, int K, int N, cudaStream_t s, bool pdl) {
     if (T % kGM || N % 128 || K % kGK) throw std::runtime_error("bert gemm: T, N multiple of 128, K of 64");
-    if (N % 256 == 0 && (T / kGM) * (N / 256) >= 148)
+    static const int force_bn = std::getenv("GFX_BERT_BN") ? std::atoi(std::getenv("GFX_BERT_BN")) : 0;  // debug A/B
+    if (N % 256 == 0 && (force_bn == 256 || (force_bn == 0 && (T / kGM) * (N / 256) >= 148)))
         gemm_bn<kEpi, 256>(arena, pt, w_off, b_off, x, y, resid, T, K, N, s, pdl);
     else
         gemm_bn<kEpi, 128>(arena, pt, w_off, b_off, x, y, resid, T, K, N, s, pdl);

@@ -1,6 +1,8 @@
 // GPU Manager implementation — see manager.cuh.
 #include "manager.cuh"
 
+#include <cuda.h>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -329,23 +331,94 @@ void GpuManager::evict(int model) {
     s.live = false;
 }
 
-// The load that replaces profile.load_time_us (proj/src/cluster.cpp:163-167).
-uint64_t GpuManager::load(int model, GpuManager* src) {
-    const ModelBlob& blob = ModelStore::get().at(model);
+// Lowest free pages first (deterministic: peers replay it as a shadow, see
+// gfx_capi.cu RemoteArena).
+GpuManager::Slot& GpuManager::allocate(int model, const ModelBlob& blob) {
     Slot& s = slot(model);
     if (s.live) throw std::logic_error("load of resident model " + std::to_string(model));
     if (free_.size() < blob.pages)
         throw std::logic_error("arena out of pages: the control plane's capacity model and the arena disagree");
-    activate();
     s.pages.clear();
     for (uint32_t i = 0; i < blob.pages; ++i) {
         s.pages.push_back(*free_.begin());
         free_.erase(free_.begin());
     }
+    return s;
+}
+
+namespace {
+using StreamWaitValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+using StreamWriteValue32Fn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+template <typename Fn>
+Fn driver_fn(const char* name) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    GFX_CUDA(cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || p == nullptr) throw CudaError(std::string(name) + " entry point unavailable");
+    return reinterpret_cast<Fn>(p);
+}
+}  // namespace
+
+void GpuManager::copy_wait_geq(const uint32_t* addr, uint32_t value) {
+    static StreamWaitValue32Fn fn = driver_fn<StreamWaitValue32Fn>("cuStreamWaitValue32");
+    activate();
+    if (fn(copy_, reinterpret_cast<CUdeviceptr>(addr), value, CU_STREAM_WAIT_VALUE_GEQ) != CUDA_SUCCESS)
+        throw CudaError("cuStreamWaitValue32 failed");
+}
+
+void GpuManager::copy_write(uint32_t* addr, uint32_t value) {
+    static StreamWriteValue32Fn fn = driver_fn<StreamWriteValue32Fn>("cuStreamWriteValue32");
+    activate();
+    // Default flags: the write is ordered after (and fenced behind) the prior copies of the stream.
+    if (fn(copy_, reinterpret_cast<CUdeviceptr>(addr), value, CU_STREAM_WRITE_VALUE_DEFAULT) != CUDA_SUCCESS)
+        throw CudaError("cuStreamWriteValue32 failed");
+}
+
+// NVLink fetch from another process's arena (IPC-mapped): the same page-run
+// copies as the in-process peer path, ordered by a device-side wait on the
+// holder's load counter instead of an event.
+uint64_t GpuManager::load_remote(int model, const char* src_arena, const std::vector<uint32_t>& sp,
+                                 const uint32_t* wait_addr, uint32_t wait_value) {
+    const ModelBlob& blob = ModelStore::get().at(model);
+    if (sp.size() != blob.pages) throw std::logic_error("remote page table does not match the model");
+    activate();
+    Slot& s = allocate(model, blob);
     cudaEvent_t t0 = nullptr, t1 = nullptr;
-    if (load_timer) {
-        t0 = load_timer->next();
-        t1 = load_timer->next();
+    copy_wait_geq(wait_addr, wait_value);  // outside the timed copy: the holder's load may still run
+    if (p2p_timer) {
+        t0 = p2p_timer->next();
+        t1 = p2p_timer->next();
+        GFX_CUDA(cudaEventRecord(t0, copy_));
+    }
+    uint32_t i = 0;
+    while (i < blob.pages) {
+        uint32_t j = i + 1;
+        while (j < blob.pages && s.pages[j] == s.pages[j - 1] + 1 && sp[j] == sp[j - 1] + 1) ++j;
+        const uint64_t off = static_cast<uint64_t>(i) * kPageBytes;
+        const uint64_t len = std::min<uint64_t>(static_cast<uint64_t>(j - i) * kPageBytes, blob.bytes - off);
+        GFX_CUDA(cudaMemcpyAsync(arena_ + static_cast<uint64_t>(s.pages[i]) * kPageBytes,
+                                 src_arena + static_cast<uint64_t>(sp[i]) * kPageBytes, len, cudaMemcpyDeviceToDevice,
+                                 copy_));
+        i = j;
+    }
+    if (p2p_timer) GFX_CUDA(cudaEventRecord(t1, copy_));
+    GFX_CUDA(cudaEventRecord(s.loaded, copy_));
+    s.live = true;
+    GFX_CUDA(cudaStreamWaitEvent(compute_, s.loaded, 0));
+    return blob.bytes;
+}
+
+// The load that replaces profile.load_time_us (proj/src/cluster.cpp:163-167).
+uint64_t GpuManager::load(int model, GpuManager* src) {
+    const ModelBlob& blob = ModelStore::get().at(model);
+    activate();
+    Slot& s = allocate(model, blob);
+    cudaEvent_t t0 = nullptr, t1 = nullptr;
+    if (src) GFX_CUDA(cudaStreamWaitEvent(copy_, src->loaded_event(model), 0));  // holder's copy complete
+    KernelTimer* timer = src ? p2p_timer : load_timer;
+    if (timer) {
+        t0 = timer->next();
+        t1 = timer->next();
         GFX_CUDA(cudaEventRecord(t0, copy_));
     }
     if (src == nullptr) {
@@ -366,7 +439,6 @@ uint64_t GpuManager::load(int model, GpuManager* src) {
         // the holder's copy is complete, copy runs contiguous on both sides,
         // and register the fetch as a reader of the holder's pages.
         const std::vector<uint32_t>& sp = src->pages_of(model);
-        GFX_CUDA(cudaStreamWaitEvent(copy_, src->loaded_event(model), 0));
         uint32_t i = 0;
         while (i < blob.pages) {
             uint32_t j = i + 1;
@@ -379,7 +451,7 @@ uint64_t GpuManager::load(int model, GpuManager* src) {
             i = j;
         }
     }
-    if (load_timer) GFX_CUDA(cudaEventRecord(t1, copy_));
+    if (timer) GFX_CUDA(cudaEventRecord(t1, copy_));
     GFX_CUDA(cudaEventRecord(s.loaded, copy_));
     if (src) src->add_reader(model, s.loaded);
     s.live = true;

@@ -83,6 +83,16 @@ public:
     void infer(int model, const void* in, void* out, void* debug_hidden = nullptr);
     void reset();  // synchronise and drop every resident model
 
+    // Cross-process peers (one process per GPU): fetch a model from another
+    // rank's arena mapped into this process by CUDA IPC, `src_pages` being that
+    // arena's page table for the model; the copy stream first waits until the
+    // 32-bit word `wait_addr` >= `wait_value` (the holder's load is done).
+    uint64_t load_remote(int model, const char* src_arena, const std::vector<uint32_t>& src_pages,
+                         const uint32_t* wait_addr, uint32_t wait_value);
+    // Stream memory operations on the copy stream (device-side cross-process ordering).
+    void copy_wait_geq(const uint32_t* addr, uint32_t value);
+    void copy_write(uint32_t* addr, uint32_t value);
+
     cudaStream_t compute_stream() const { return compute_; }
     cudaStream_t copy_stream() const { return copy_; }
     cudaEvent_t loaded_event(int model) const;
@@ -93,7 +103,8 @@ public:
 
     // Instrumentation (all optional).
     KernelTimer* layer_timer = nullptr;   // records around every layer launch
-    KernelTimer* load_timer = nullptr;    // records around every model load
+    KernelTimer* load_timer = nullptr;    // records around every pinned-host model load
+    KernelTimer* p2p_timer = nullptr;     // records around every peer (NVLink) fetch
     int64_t kernel_launches = 0;
 
 private:
@@ -106,6 +117,7 @@ private:
     };
     Slot& slot(int model);
     void build_page_table(const Slot& s, PageTable& pt) const;
+    Slot& allocate(int model, const ModelBlob& blob);
 
     int device_;
     int id_;

@@ -90,6 +90,28 @@ class Replay:
         _ffi.check(_ffi.gfx_replay_requests(self.h, mi.ctypes.data, svc.ctypes.data, n_requests))
         return mi, svc
 
+    def ipc_export(self) -> bytes:
+        """This rank's CUDA IPC blob (arena + flag words) for cross-process peer fetch."""
+        n = int(_ffi.gfx_replay_ipc_blob_bytes())
+        buf = (C.c_char * n)()
+        _ffi.check(_ffi.gfx_replay_ipc_export(self.h, buf, n))
+        return bytes(buf)
+
+    def ipc_import(self, blobs: list[bytes]):
+        """Map every rank's blob (index = GPU id) before the first run."""
+        n = int(_ffi.gfx_replay_ipc_blob_bytes())
+        if any(len(b) != n for b in blobs):
+            raise ValueError("ipc blobs of the wrong size")
+        buf = C.create_string_buffer(b"".join(blobs), n * len(blobs))
+        _ffi.check(_ffi.gfx_replay_ipc_import(self.h, buf, len(blobs)))
+
+    def connect_peers(self, group=None):
+        """All-gather the IPC blobs over torch.distributed (one process per GPU) and import them."""
+        import torch.distributed as dist
+        blobs = [None] * dist.get_world_size(group)
+        dist.all_gather_object(blobs, self.ipc_export(), group=group)
+        self.ipc_import(blobs)
+
     def close(self):
         if self.h:
             _ffi.check(_ffi.gfx_replay_destroy(self.h))

@@ -123,6 +123,23 @@ __global__ void __launch_bounds__(128, 1) issue_rate(int steps, int mode, long l
             }
             t1 = clock64();
         }
+    } else if (mode >= 10 && mode <= 12) {
+        // bf16 SS M128 x N x K16, 4 per iteration (one 64-wide K stage), operands rotating over
+        // 4 stages of A (16 KB) + B (N x 128 B): 10 -> N=128, 11 -> N=256, 12 -> N=256 same address
+        if (threadIdx.x == 0) {
+            const int N = mode == 10 ? 128 : 256;
+            const uint32_t idesc = N == 128 ? umma_idesc<128, 128, 1>() : umma_idesc<128, 256, 1>();
+            const uint32_t stage = 16384 + N * 128;
+            t0 = clock64();
+            for (int st = 0; st < steps; ++st) {
+                const uint8_t* a0 = sm + (mode == 12 ? 0 : (st & 3)) * stage;
+                const uint64_t ad = umma_desc_sw128(a0, 0), bd = umma_desc_sw128(a0 + 16384, 0);
+#pragma unroll
+                for (int kk = 0; kk < 4; ++kk) umma_f16(tm + (st & 1) * 256, ad + kk * 2, bd + kk * 2, idesc, 1u);
+                umma_commit(&bar[0]);
+            }
+            t1 = clock64();
+        }
     } else if (mode == 2 || mode == 3) {
         if (threadIdx.x < 32) {
             t0 = clock64();
@@ -160,10 +177,11 @@ int main() {
     cudaMemset(gsrc, 0, 1ull << 30);
     const char* names[] = {"lane0 empty", "lane0 4xMMA+commit", "warp empty", "warp 4xMMA+commit (elect)",
                            "lane0 4xMMA rotating slots", "lane0 4xSS+4xTS rotating", "TS N64+N32 x4 rot",
-                           "TS N64 x4 rot", "TS 2xN64 x4 rot (v5)", "TS N64+N32 x4 fixed B"};
+                           "TS N64 x4 rot", "TS 2xN64 x4 rot (v5)", "TS N64+N32 x4 fixed B",
+                           "bf16 SS N128 K16 x4 rot", "bf16 SS N256 K16 x4 rot", "bf16 SS N256 K16 x4 same"};
     for (int tma : {0}) {
         const int steps = 4000;
-        for (int mode = 0; mode < 10; ++mode) {
+        for (int mode = 0; mode < 13; ++mode) {
             issue_rate<<<sms, 128, 201 * 1024>>>(steps, mode, d, gsrc, tma);
             cudaError_t e = cudaDeviceSynchronize();
             if (e != cudaSuccess) {
