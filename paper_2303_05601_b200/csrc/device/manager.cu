@@ -248,14 +248,6 @@ GpuManager::GpuManager(int device, uint64_t capacity_bytes, int manager_id) : de
     GFX_CUDA(cudaStreamCreateWithFlags(&compute_, cudaStreamNonBlocking));
     GFX_CUDA(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
     GFX_CUDA(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, device_));
-    max_dim_ = kMaxDim;
-    GFX_CUDA(cudaMalloc(&act_[0], sizeof(float) * kBatch * kMaxDim));
-    GFX_CUDA(cudaMalloc(&act_[1], sizeof(float) * kBatch * kMaxDim));
-    GFX_CUDA(cudaMalloc(&ws_, sizeof(float) * kMaxSplits * kBatch * kMaxDim));
-    const int ncnt = 512;  // split-K arrival / done counters per feature tile
-    GFX_CUDA(cudaMalloc(&counters_, sizeof(unsigned) * ncnt));
-    GFX_CUDA(cudaMalloc(&stats_, sizeof(float) * 2 * kBatch * ncnt));
-    GFX_CUDA(cudaMemset(counters_, 0, sizeof(unsigned) * ncnt));
     GFX_CUDA(cudaMalloc(&fwd_opnd_, kMlpOpndLayerBytes * GFX_MAX_LAYERS));
     GFX_CUDA(cudaMalloc(&fwd_part_, sizeof(float) * kMlpPartLayerFloats * GFX_MAX_LAYERS));
     GFX_CUDA(cudaMalloc(&fwd_cnt_, sizeof(unsigned) * kMlpCounters));
@@ -272,11 +264,6 @@ GpuManager::~GpuManager() {
         if (s.last_use) cudaEventDestroy(s.last_use);
     }
     cudaFree(arena_);
-    cudaFree(act_[0]);
-    cudaFree(act_[1]);
-    cudaFree(ws_);
-    cudaFree(counters_);
-    cudaFree(stats_);
     cudaFree(fwd_opnd_);
     cudaFree(fwd_part_);
     cudaFree(fwd_cnt_);
@@ -466,7 +453,8 @@ void GpuManager::build_page_table(const Slot& s, PageTable& pt) const {
 }
 
 // The batched inference that replaces profile.infer_time_us
-// (proj/src/cluster.cpp:161,167): one K1 launch per layer on the compute stream.
+// (proj/src/cluster.cpp:161,167): MLP -> one K1 launch (the whole forward),
+// BERT -> the K2-K4 chain, on the compute stream.
 void GpuManager::infer(int model, const void* in_v, void* out_v, void* debug_hidden) {
     const ModelBlob& blob = ModelStore::get().at(model);
     Slot& s = slot(model);
@@ -485,8 +473,7 @@ void GpuManager::infer(int model, const void* in_v, void* out_v, void* debug_hid
     }
     const float* in = static_cast<const float*>(in_v);
     float* out = static_cast<float*>(out_v);
-    static const bool layerwise = std::getenv("GFX_MLP_LAYERWISE") != nullptr;  // debug A/B: K1 v5 per-layer path
-    if (!layerwise) {
+    {
         MlpFwdArgs f{};
         f.arena = arena_;
         build_page_table(s, f.pt);
@@ -511,8 +498,8 @@ void GpuManager::infer(int model, const void* in_v, void* out_v, void* debug_hid
         }
         static const bool trace_on = std::getenv("GFX_TRACE_MLP") != nullptr;
         if (trace_on) {
-            GFX_CUDA(cudaMalloc(&f.trace, sizeof(unsigned long long) * (32 * f.grid + 576 + 16 * f.grid)));
-            GFX_CUDA(cudaMemset(f.trace, 0, sizeof(unsigned long long) * (32 * f.grid + 576 + 16 * f.grid)));
+            GFX_CUDA(cudaMalloc(&f.trace, sizeof(unsigned long long) * mlp_trace_words(f.grid)));
+            GFX_CUDA(cudaMemset(f.trace, 0, sizeof(unsigned long long) * mlp_trace_words(f.grid)));
         }
         if (layer_timer) GFX_CUDA(cudaEventRecord(layer_timer->next(), compute_));
         static const int repeat = std::getenv("GFX_MLP_REPEAT") ? std::atoi(std::getenv("GFX_MLP_REPEAT")) : 0;
@@ -537,130 +524,17 @@ void GpuManager::infer(int model, const void* in_v, void* out_v, void* debug_hid
         f.epoch = fwd_epoch_++;
         launch_mlp_forward(f, compute_);
         ++kernel_launches;
-        if (trace_on) {  // debug timeline: µs after the first CTA started, min / median / max over CTAs
-            std::vector<unsigned long long> tr(static_cast<size_t>(48) * f.grid + 576);
+        if (trace_on) {  // debug timeline (GFX_TRACE_MLP)
+            std::vector<unsigned long long> tr(mlp_trace_words(f.grid));
             GFX_CUDA(cudaStreamSynchronize(compute_));
             GFX_CUDA(cudaMemcpy(tr.data(), f.trace, tr.size() * 8, cudaMemcpyDeviceToHost));
             GFX_CUDA(cudaFree(f.trace));
-            unsigned long long t0 = ~0ull;
-            const size_t nct = static_cast<size_t>(f.grid) * 32;
-            for (size_t i = 0; i < nct; i += 32) t0 = std::min(t0, tr[i]);
-            static const char* names[4] = {"mma first", "mma last", "epi start", "tile done"};
-            std::fprintf(stderr, "[trace] model %d grid %d\n", model, f.grid);
-            for (int ph = 0; ph < 32; ++ph) {
-                std::vector<double> v;
-                for (size_t i = 0; i < nct; i += 32)
-                    if (tr[i + static_cast<size_t>(ph)]) v.push_back((tr[i + static_cast<size_t>(ph)] - t0) * 1e-3);
-                if (v.empty()) continue;
-                std::sort(v.begin(), v.end());
-                char nm[32];
-                if (ph == 0) std::snprintf(nm, sizeof nm, "start");
-                else if (ph == 1) std::snprintf(nm, sizeof nm, "setup");
-                else if (ph == 31) std::snprintf(nm, sizeof nm, "end");
-                else if (ph >= 26 && ph < 30) std::snprintf(nm, sizeof nm, "L%d %s", (ph - 26) / 2, ph % 2 ? "gathered" : "siblings");
-                else if (ph >= 18 && ph <= 30 && f.L <= 4) {
-                    static const char* sub[13] = {"L0 part stored", "L0 fenced", "L0 arrived", "L0 sib seen", "L0 cp.async issued",
-                                                  "L0 cp.async done", "L0 emitted", "L0 done-sync", "", "", "", "", "L0 done fenced"};
-                    std::snprintf(nm, sizeof nm, "%s", sub[ph - 18]);
-                }
-                else std::snprintf(nm, sizeof nm, "L%d %s", (ph - 2) / 4, names[(ph - 2) % 4]);
-                std::fprintf(stderr, "  %-16s n=%3zu %8.2f %8.2f %8.2f\n", nm, v.size(), v.front(), v[v.size() / 2],
-                             v.back());
-            }
-            std::fprintf(stderr, "  CTA 0 steps (us): Wreq Xreq Wlanded WloDone xFull mmaIssued\n");
-            for (int st = 0; st < 64; ++st) {
-                const unsigned long long* p = tr.data() + nct + st * 8;
-                if (!p[0] && !p[5]) break;
-                auto us = [&](unsigned long long t) { return t ? (t - t0) * 1e-3 : -1.0; };
-                std::fprintf(stderr, "   %2d %7.2f %7.2f %7.2f %7.2f %7.2f %7.2f\n", st, us(p[0]), us(p[1]), us(p[2]),
-                             us(p[3]), us(p[4]), us(p[5]));
-            }
-            static const char* pn[16] = {"mma: wait tempty", "mma: wait ready", "", "",
-                                         "mma: commits+rest", "conv: wait w_full", "", "conv: work",
-                                         "wprod: wait slot", "xprod: wait slot", "xprod: wait flag", "drain: wait tfull",
-                                         "drain: epilogue", "mma: MMAs", "", "steps"};
-            std::fprintf(stderr, "  cycles per CTA, mean over CTAs with work (per step in brackets):\n");
-            for (int i = 0; i < 16; ++i) {
-                if (!pn[i][0]) continue;
-                double sum = 0, steps = 0;
-                int n = 0;
-                for (int c = 0; c < f.grid; ++c) {
-                    const unsigned long long st = tr[nct + 576 + c * 16 + 15];
-                    if (!st) continue;
-                    sum += static_cast<double>(tr[nct + 576 + c * 16 + i]);
-                    steps += static_cast<double>(st);
-                    ++n;
-                }
-                if (n) std::fprintf(stderr, "   %-22s %10.0f  (%7.1f)\n", pn[i], sum / n, sum / steps);
-            }
+            mlp_trace_report(tr, f.grid, f.L, model);
         }
         if (layer_timer) GFX_CUDA(cudaEventRecord(layer_timer->next(), compute_));
         GFX_CUDA(cudaEventRecord(s.last_use, compute_));
         return;
     }
-    MlpLayerArgs a{};
-    a.arena = arena_;
-    build_page_table(s, a.pt);
-    a.ws = ws_;
-    a.counters = counters_;
-    a.stats = stats_;
-    a.ldws = max_dim_;
-    const int L = blob.desc.n_layers;
-    const int C = blob.desc.dims[L];
-    const float* x = in;
-    for (int l = 0; l < L; ++l) {
-        a.K = blob.desc.dims[l];
-        a.N = blob.desc.dims[l + 1];
-        a.x = x;
-        const bool last = l + 1 == L;
-        a.y = last ? out : act_[l & 1];
-        a.probs = nullptr;  // softmax runs as its own row-parallel kernel
-        a.relu = last ? 0 : 1;
-        a.w_off = blob.w_off[l];
-        a.b_off = blob.b_off[l];
-        a.ntiles = mlp_layer_tiles(a.N);
-        a.splits = mlp_layer_splits(a.K, a.N, sm_count_);
-        if (l == 0 && layer_timer) GFX_CUDA(cudaEventRecord(layer_timer->next(), compute_));
-        // Layers 1.. and the softmax are programmatic dependents of the kernel
-        // before them: their prologue and weight prefetch overlap its tail.
-        static const bool trace_on = std::getenv("GFX_TRACE_MLP") != nullptr;
-        static const int ablate = std::getenv("GFX_MLP_ABLATE") ? std::atoi(std::getenv("GFX_MLP_ABLATE")) : 0;
-        a.ablate = ablate;
-        std::vector<unsigned long long> tr;
-        if (trace_on) {  // debug timeline: per-CTA phase timestamps of this launch
-            GFX_CUDA(cudaMalloc(&a.trace, sizeof(unsigned long long) * 8 * a.ntiles * a.splits));
-            GFX_CUDA(cudaMemset(a.trace, 0, sizeof(unsigned long long) * 8 * a.ntiles * a.splits));
-        }
-        launch_mlp_layer(a, compute_, /*pdl=*/l > 0 && !trace_on);
-        if (trace_on) {
-            tr.resize(static_cast<size_t>(8) * a.ntiles * a.splits);
-            GFX_CUDA(cudaStreamSynchronize(compute_));
-            GFX_CUDA(cudaMemcpy(tr.data(), a.trace, tr.size() * 8, cudaMemcpyDeviceToHost));
-            GFX_CUDA(cudaFree(a.trace));
-            a.trace = nullptr;
-            unsigned long long t0 = ~0ull;
-            for (size_t i = 0; i < tr.size(); i += 8) t0 = std::min(t0, tr[i]);
-            std::fprintf(stderr, "[trace] layer %d K=%d N=%d grid %dx%d (us after first CTA start: min/med/max)\n", l,
-                         a.K, a.N, a.ntiles, a.splits);
-            const char* names[7] = {"start", "prologue", "tma_issued", "first_data", "mainloop_end", "splitk_done",
-                                    "store_done"};
-            for (int ph = 0; ph < 7; ++ph) {
-                std::vector<double> v;
-                for (size_t i = 0; i < tr.size(); i += 8)
-                    if (tr[i + static_cast<size_t>(ph)]) v.push_back((tr[i + static_cast<size_t>(ph)] - t0) * 1e-3);
-                if (v.empty()) continue;
-                std::sort(v.begin(), v.end());
-                std::fprintf(stderr, "  %-13s n=%3zu %8.2f %8.2f %8.2f\n", names[ph], v.size(), v.front(),
-                             v[v.size() / 2], v.back());
-            }
-        }
-        ++kernel_launches;
-        x = a.y;
-    }
-    launch_softmax_rows(out, out + static_cast<size_t>(kBatch) * C, kBatch, C, compute_);
-    ++kernel_launches;
-    if (layer_timer) GFX_CUDA(cudaEventRecord(layer_timer->next(), compute_));  // one pair per inference
-    GFX_CUDA(cudaEventRecord(s.last_use, compute_));
 }
 
 void GpuManager::reset() {
@@ -673,7 +547,6 @@ void GpuManager::reset() {
         s.readers.clear();
         s.live = false;
     }
-    GFX_CUDA(cudaMemset(counters_, 0, sizeof(unsigned) * 512));
     GFX_CUDA(cudaMemset(fwd_cnt_, 0, sizeof(unsigned) * kMlpCounters));
     GFX_CUDA(cudaDeviceSynchronize());
 }

@@ -102,7 +102,7 @@ public:
     void activate() const;  // cudaSetDevice
 
     // Instrumentation (all optional).
-    KernelTimer* layer_timer = nullptr;   // records around every layer launch
+    KernelTimer* layer_timer = nullptr;   // records around every inference
     KernelTimer* load_timer = nullptr;    // records around every pinned-host model load
     KernelTimer* p2p_timer = nullptr;     // records around every peer (NVLink) fetch
     int64_t kernel_launches = 0;
@@ -127,13 +127,8 @@ private:
     std::vector<Slot> slots_;
     cudaStream_t compute_ = nullptr, copy_ = nullptr;
     int sm_count_ = 148;
-    // inference workspace
-    float* act_[2] = {nullptr, nullptr};
-    float* ws_ = nullptr;
+    // inference workspaces
     BertWorkspace bert_ws_;
-    unsigned* counters_ = nullptr;
-    float* stats_ = nullptr;
-    int max_dim_ = 0;
     // K1 v6 forward workspace
     char* fwd_opnd_ = nullptr;
     float* fwd_part_ = nullptr;

@@ -4,40 +4,12 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <vector>
 
 #include "common.cuh"
 
 namespace gfx {
 
-constexpr int kMaxSplits = 32;
-
-struct MlpLayerArgs {
-    const float* x;        // [32 x K] activations, row-major, device (read through a TMA tensor map)
-    float* y;              // [32 x N] output rows
-    float* probs;          // last layer: [32 x N] softmax rows; else nullptr
-    const char* arena;     // arena base
-    uint64_t w_off;        // model-blob offset of W: ceil(N/128) x (K/32) swizzled 16 KB tiles
-    uint64_t b_off;        // model-blob offset of b [N]
-    int K, N;
-    int splits, ntiles;
-    int relu;
-    int ldws;              // leading dimension of the split-K workspace
-    float* ws;             // split-K partials [tiles][splits][32][128]
-    unsigned* counters;    // [ntiles + 1], zero between launches
-    float* stats;          // last layer: [ntiles][32][2] per-tile softmax partials
-    unsigned long long* trace;  // debug (GFX_TRACE_MLP): per-CTA phase timestamps, else nullptr
-    int ablate;            // debug (GFX_MLP_ABLATE) bitmask, 0 in production: 1 no proxy fence,
-                           // 2 no hi/lo split work, 4 one MMA product, 8 no TMEM drains
-    PageTable pt;
-};
-
-int mlp_layer_splits(int K, int N, int sm_count);
-int mlp_layer_tiles(int N);
-size_t mlp_layer_smem();
-// pdl: launch as a programmatic dependent of the previous kernel in the stream
-// (only when that previous operation is a kernel, not an event wait).
-void launch_mlp_layer(const MlpLayerArgs& a, cudaStream_t stream, bool pdl);
-void launch_softmax_rows(const float* logits, float* probs, int rows, int C, cudaStream_t s);
 // Fills `count` consecutive tensors of n values, tensor t from seed + t.
 void launch_fill_params(float* dst, uint64_t n, uint64_t seed, uint32_t tensor, float scale, cudaStream_t s,
                         uint64_t count = 1);
@@ -75,6 +47,9 @@ struct MlpFwdArgs {
 int mlp_fwd_splits(int K, int N, int grid);
 size_t mlp_fwd_smem();
 void launch_mlp_forward(MlpFwdArgs& a, cudaStream_t stream);
+// Debug timeline (GFX_TRACE_MLP): buffer size in 64-bit words and the stderr report.
+size_t mlp_trace_words(int grid);
+void mlp_trace_report(const std::vector<unsigned long long>& trace, int grid, int layers, int model);
 
 // Weight tiles of the blob: 128 x 32 fp32, K-major SWIZZLE_128B image (16 KB).
 constexpr int kWTileRows = 128;

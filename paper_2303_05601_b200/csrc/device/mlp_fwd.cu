@@ -57,6 +57,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <vector>
+#include <cstdio>
+#include <algorithm>
 #include <cstdlib>
 #include <stdexcept>
 
@@ -650,6 +653,68 @@ int mlp_fwd_splits(int K, int N, int grid) {
     if (s > kRows) s = kRows;
     return s < 1 ? 1 : s;
 }
+
+size_t mlp_trace_words(int grid) { return static_cast<size_t>(48) * grid + 576; }
+
+// Debug report of a traced launch (GFX_TRACE_MLP=1): per-phase %globaltimer marks
+// (µs after the first CTA started; min / median / max over CTAs), CTA 0's
+// per-step timeline and the per-role cycle accounting.
+void mlp_trace_report(const std::vector<unsigned long long>& tr, int grid, int L, int model) {
+    struct {
+        int grid, L;
+    } f{grid, L};
+    unsigned long long t0 = ~0ull;
+    const size_t nct = static_cast<size_t>(f.grid) * 32;
+    for (size_t i = 0; i < nct; i += 32) t0 = std::min(t0, tr[i]);
+    static const char* names[4] = {"mma first", "mma last", "epi start", "tile done"};
+    std::fprintf(stderr, "[trace] model %d grid %d\n", model, f.grid);
+    for (int ph = 0; ph < 32; ++ph) {
+        std::vector<double> v;
+        for (size_t i = 0; i < nct; i += 32)
+            if (tr[i + static_cast<size_t>(ph)]) v.push_back((tr[i + static_cast<size_t>(ph)] - t0) * 1e-3);
+        if (v.empty()) continue;
+        std::sort(v.begin(), v.end());
+        char nm[32];
+        if (ph == 0) std::snprintf(nm, sizeof nm, "start");
+        else if (ph == 1) std::snprintf(nm, sizeof nm, "setup");
+        else if (ph == 31) std::snprintf(nm, sizeof nm, "end");
+        else if (ph >= 26 && ph < 30) std::snprintf(nm, sizeof nm, "L%d %s", (ph - 26) / 2, ph % 2 ? "gathered" : "siblings");
+        else if (ph >= 18 && ph <= 30 && f.L <= 4) {
+            static const char* sub[13] = {"L0 part stored", "L0 fenced", "L0 arrived", "L0 sib seen", "L0 cp.async issued",
+                                          "L0 cp.async done", "L0 emitted", "L0 done-sync", "", "", "", "", "L0 done fenced"};
+            std::snprintf(nm, sizeof nm, "%s", sub[ph - 18]);
+        }
+        else std::snprintf(nm, sizeof nm, "L%d %s", (ph - 2) / 4, names[(ph - 2) % 4]);
+        std::fprintf(stderr, "  %-16s n=%3zu %8.2f %8.2f %8.2f\n", nm, v.size(), v.front(), v[v.size() / 2],
+                     v.back());
+    }
+    std::fprintf(stderr, "  CTA 0 steps (us): Wreq Xreq Wlanded WloDone xFull mmaIssued\n");
+    for (int st = 0; st < 64; ++st) {
+        const unsigned long long* p = tr.data() + nct + st * 8;
+        if (!p[0] && !p[5]) break;
+        auto us = [&](unsigned long long t) { return t ? (t - t0) * 1e-3 : -1.0; };
+        std::fprintf(stderr, "   %2d %7.2f %7.2f %7.2f %7.2f %7.2f %7.2f\n", st, us(p[0]), us(p[1]), us(p[2]),
+                     us(p[3]), us(p[4]), us(p[5]));
+    }
+    static const char* pn[16] = {"mma: wait tempty", "mma: wait ready", "", "",
+                                 "mma: commits+rest", "conv: wait w_full", "", "conv: work",
+                                 "wprod: wait slot", "xprod: wait slot", "xprod: wait flag", "drain: wait tfull",
+                                 "drain: epilogue", "mma: MMAs", "", "steps"};
+    std::fprintf(stderr, "  cycles per CTA, mean over CTAs with work (per step in brackets):\n");
+    for (int i = 0; i < 16; ++i) {
+        if (!pn[i][0]) continue;
+        double sum = 0, steps = 0;
+        int n = 0;
+        for (int c = 0; c < f.grid; ++c) {
+            const unsigned long long st = tr[nct + 576 + c * 16 + 15];
+            if (!st) continue;
+            sum += static_cast<double>(tr[nct + 576 + c * 16 + i]);
+            steps += static_cast<double>(st);
+            ++n;
+        }
+        if (n) std::fprintf(stderr, "   %-22s %10.0f  (%7.1f)\n", pn[i], sum / n, sum / steps);
+    }
+    }
 
 size_t mlp_fwd_smem() { return static_cast<size_t>(kSlotBytes) * kSlots + kGatherBytes + 1024; }
 
