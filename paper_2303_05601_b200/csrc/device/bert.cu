@@ -18,6 +18,9 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
+#include <cstdio>
+#include <vector>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -45,13 +48,14 @@ __device__ __forceinline__ float gelu(float x) { return 0.5f * x * (1.0f + erff(
 // Persistent: one CTA per SM loops over 128 x kBN output tiles; the TMEM holds
 // two accumulators so the epilogue of tile i overlaps the MMAs of tile i+1.
 
-constexpr int kGM = 128, kGK = 64, kGThreads = 192;
+constexpr int kGM = 128, kGK = 64, kGThreads = 320;  // TMA, MMA, 8 epilogue warps
 constexpr uint32_t kGATile = 128 * 128;  // A: 128 rows x 64 bf16 (16 KB)
 constexpr uint32_t kGSmem = 192 * 1024;  // stage ring budget
 
 enum Epi : int { kEpiBias = 0, kEpiGelu = 1, kEpiResid = 2 };
 
 struct GemmArgs {
+    unsigned long long* trace;    // debug (GFX_TRACE_GEMM): [grid][16] %globaltimer marks, else nullptr
     const char* arena;
     uint64_t w_off, b_off;        // weight tiles, fp32 bias
     __nv_bfloat16* y;             // [T x N]
@@ -62,19 +66,31 @@ struct GemmArgs {
 
 template <int kEpi, int kBN>
 __global__ void __launch_bounds__(kGThreads, 1)
-    gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ GemmArgs a) {
+    gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_y,
+                     const __grid_constant__ CUtensorMap tmap_r, const __grid_constant__ GemmArgs a) {
     constexpr uint32_t kBBytes = kBN * 128;            // B: kBN rows x 64 bf16
     constexpr uint32_t kStage = kGATile + kBBytes;
     constexpr int kStages = static_cast<int>(kGSmem / kStage);
     constexpr uint32_t kTmemCols = 2 * kBN <= 256 ? 256 : 512;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
-    __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], tfull_bar[2], tempty_bar[2];
+    // Epilogue staging: per epilogue half, two 128 x 32 bf16 boxes (8 KB,
+    // SWIZZLE_64B image) for the coalesced TMA store of each 32-column chunk
+    // (and the residual load).
+    uint8_t* stage_out = smem + kGSmem;
+    __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], tfull_bar[2], tempty_bar[2], res_bar[2][2];
     __shared__ uint32_t tmem_s;
     __shared__ uint32_t pt[GFX_MAX_PAGES];
     __shared__ float bias_s[kBN];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    auto mark = [&](int i) {
+        if (a.trace == nullptr) return;
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        a.trace[blockIdx.x * 16 + i] = t;
+    };
+    if (tid == 0) mark(0);
     const int n_tiles = a.N / kBN, m_tiles = a.T / kGM, tiles = n_tiles * m_tiles;
     const int nk = a.K / kGK;
     const int ktiles_row = a.K / kGK;  // blob weight tiles per 128 rows
@@ -87,16 +103,21 @@ __global__ void __launch_bounds__(kGThreads, 1)
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull_bar[b], 1);
-            mbar_init(&tempty_bar[b], 128);
+            mbar_init(&tempty_bar[b], 256);
+            mbar_init(&res_bar[0][b], 1);
+            mbar_init(&res_bar[1][b], 1);
         }
         mbar_fence_init();
         tma_prefetch_desc(&tmap_x);
+        tma_prefetch_desc(&tmap_y);
+        if (kEpi == kEpiResid) tma_prefetch_desc(&tmap_r);
     }
     if (warp == 1) tmem_alloc<kTmemCols>(&tmem_s);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_s;
+    if (tid == 0) mark(1);
 
     if (warp == 0) {
         if (lane == 0) {
@@ -136,6 +157,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
                     const int s = g % kStages;
                     mbar_wait(&full_bar[s], (g / kStages) & 1);
                     tc_fence_after();
+                    if (g == 0) mark(2);
                     uint8_t* st = smem + static_cast<size_t>(s) * kStage;
 #pragma unroll
                     for (int kk = 0; kk < kGK / 16; ++kk)  // K = 16 bf16 = 32 bytes per MMA
@@ -144,40 +166,58 @@ __global__ void __launch_bounds__(kGThreads, 1)
                     umma_commit(&empty_bar[s]);
                 }
                 umma_commit(&tfull_bar[b]);
+                if (i < 4) mark(3 + i);  // last MMA of tile i issued
             }
         }
     } else {
-        // Epilogue: TMEM lane = token row, column = output feature.
-        const int q = warp & 3, ct = tid - 64;
-        int i = 0;
+        // Epilogue (8 warps): TMEM lane = token row, column = output feature.
+        // Two warps per TMEM lane quarter; half h takes the even / odd 32-column
+        // chunks, with its own staging boxes, named barrier and store thread.
+        const int q = warp & 3, h = (warp - 2) >> 2, ct = tid - 64, ht = ct & 127;
+        const uint32_t hbar = 1u + static_cast<uint32_t>(h);
+        auto half_sync = [&] { asm volatile("bar.sync %0, 128;\n" ::"r"(hbar) : "memory"); };
+        int i = 0, e = 0;
         for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
             const int m0 = (t / n_tiles) * kGM, n0 = (t % n_tiles) * kBN;
             const int b = i & 1;
-            asm volatile("bar.sync 1, 128;\n" ::: "memory");  // previous tile's bias reads done
-            for (int c = ct; c < kBN; c += 128)
+            asm volatile("bar.sync 3, 256;\n" ::: "memory");  // previous tile's bias reads done
+            for (int c = ct; c < kBN; c += 256)
                 bias_s[c] = *reinterpret_cast<const float*>(translate(a.arena, pt, a.b_off + 4ull * (n0 + c)));
-            asm volatile("bar.sync 1, 128;\n" ::: "memory");
+            asm volatile("bar.sync 3, 256;\n" ::: "memory");
             mbar_wait(&tfull_bar[b], (i >> 1) & 1);
             tc_fence_after();
+            if (ct == 0 && i < 4) mark(7 + i);  // tile i accumulated
             if (t + static_cast<int>(gridDim.x) >= tiles) pdl_trigger();  // last tile: let the next kernel start
-            const int row = m0 + q * 32 + lane;
-            __nv_bfloat16* yrow = a.y + static_cast<size_t>(row) * a.N + n0;
+            // Thread = accumulator row (TMEM lane q*32+lane) = output row m0 + q*32 + lane.
+            // Per 32-column chunk: TMEM -> registers -> bias / GELU / residual ->
+            // bf16 into a staging box (row = 64 B, SWIZZLE_64B: chunk j of row r
+            // at j ^ ((r >> 1) & 3)), then one thread of the half TMA-stores the
+            // box: coalesced, and the store drains while the next chunk computes.
+            const int r = q * 32 + lane;
 #pragma unroll 1
-            for (int c = 0; c < kBN / 32; ++c) {
+            for (int c = h; c < kBN / 32; c += 2, ++e) {
+                const int sb = e & 1;
+                uint8_t* box = stage_out + (h * 2 + sb) * 8192;
+                if (ht == 0) bulk_wait_group_read<1>();  // the store that last read this box is done
+                half_sync();
+                if (kEpi == kEpiResid && ht == 0) {
+                    mbar_arrive_expect_tx(&res_bar[h][sb], 8192);
+                    tma_tile2d_g2s(box, &tmap_r, n0 + c * 32, m0, &res_bar[h][sb]);
+                }
                 float v[32];
                 tmem_ld_32x32b_x32(tmem + static_cast<uint32_t>(b * kBN + c * 32) + (static_cast<uint32_t>(q * 32) << 16), v);
-                float r[32];
+                float rs[32];
                 if (kEpi == kEpiResid) {
-                    const uint4* rp = reinterpret_cast<const uint4*>(a.resid + static_cast<size_t>(row) * a.N + n0 + c * 32);
+                    mbar_wait(&res_bar[h][sb], (e >> 1) & 1);
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
-                        const uint4 w = rp[u];
+                        const uint4 w = *reinterpret_cast<const uint4*>(box + r * 64 + ((u ^ ((r >> 1) & 3)) << 4));
                         const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&w);
 #pragma unroll
                         for (int j = 0; j < 4; ++j) {
                             const float2 f2 = __bfloat1622float2(h2[j]);
-                            r[u * 8 + 2 * j] = f2.x;
-                            r[u * 8 + 2 * j + 1] = f2.y;
+                            rs[u * 8 + 2 * j] = f2.x;
+                            rs[u * 8 + 2 * j + 1] = f2.y;
                         }
                     }
                 }
@@ -192,18 +232,26 @@ __global__ void __launch_bounds__(kGThreads, 1)
                         x1 = gelu(x1);
                     }
                     if (kEpi == kEpiResid) {
-                        x0 += r[2 * j];
-                        x1 += r[2 * j + 1];
+                        x0 += rs[2 * j];
+                        x1 += rs[2 * j + 1];
                     }
                     o2[j] = __floats2bfloat162_rn(x0, x1);
                 }
-                uint4* dst = reinterpret_cast<uint4*>(yrow + c * 32);
 #pragma unroll
-                for (int u = 0; u < 4; ++u) dst[u] = out[u];
+                for (int u = 0; u < 4; ++u)
+                    *reinterpret_cast<uint4*>(box + r * 64 + ((u ^ ((r >> 1) & 3)) << 4)) = out[u];
+                fence_proxy_async_smem();  // generic-proxy writes -> the TMA store reads
+                half_sync();
+                if (ht == 0) {
+                    tma_tile2d_s2g(&tmap_y, n0 + c * 32, m0, box);
+                    bulk_commit_group();
+                }
             }
             tc_fence_before();
             mbar_arrive(&tempty_bar[b]);  // accumulator b free for tile i+2
+            if (ct == 0 && i < 4) mark(11 + i);  // tile i stored
         }
+        if (ht == 0) bulk_wait_group<0>();  // every output box written before the CTA exits
     }
     tc_fence_before();
     __syncthreads();
@@ -466,9 +514,20 @@ void gemm_bn(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_
                               static_cast<uint64_t>(T), static_cast<uint64_t>(K) * 2, kGK, kGM,
                               CU_TENSOR_MAP_SWIZZLE_128B))
         throw CudaError("cuTensorMapEncodeTiled failed (bert gemm)");
-    GemmArgs a{arena, w_off, b_off, y, resid, T, K, N, pt};
+    // Output (and residual) as 32-column x 128-row boxes, SWIZZLE_64B: the epilogue's staging layout.
+    CUtensorMap tmy, tmr;
+    if (!encode_tensor_map_2d(&tmy, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, y, static_cast<uint64_t>(N),
+                              static_cast<uint64_t>(T), static_cast<uint64_t>(N) * 2, 32, kGM,
+                              CU_TENSOR_MAP_SWIZZLE_64B))
+        throw CudaError("cuTensorMapEncodeTiled failed (bert gemm output)");
+    if (!encode_tensor_map_2d(&tmr, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, resid ? resid : y, static_cast<uint64_t>(N),
+                              static_cast<uint64_t>(T), static_cast<uint64_t>(N) * 2, 32, kGM,
+                              CU_TENSOR_MAP_SWIZZLE_64B))
+        throw CudaError("cuTensorMapEncodeTiled failed (bert gemm residual)");
+    static const bool trace_on = std::getenv("GFX_TRACE_GEMM") != nullptr;
+    GemmArgs a{nullptr, arena, w_off, b_off, y, resid, T, K, N, pt};
     static bool attr_set = false;
-    const size_t smem = kGSmem + 1024;
+    const size_t smem = kGSmem + 4 * 8192 + 1024;
     static int sms = 0;
     if (!attr_set) {
         GFX_CUDA(cudaFuncSetAttribute(gemm_bf16_kernel<kEpi, kBN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -479,16 +538,44 @@ void gemm_bn(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_
         attr_set = true;
     }
     const int tiles = (T / kGM) * (N / kBN);
-    launch_pdl(gemm_bf16_kernel<kEpi, kBN>, dim3(tiles < sms ? tiles : sms), dim3(kGThreads), smem, s, pdl, tm, a);
+    const int grid = tiles < sms ? tiles : sms;
+    if (trace_on) {
+        GFX_CUDA(cudaMalloc(&a.trace, sizeof(unsigned long long) * 16 * grid));
+        GFX_CUDA(cudaMemset(a.trace, 0, sizeof(unsigned long long) * 16 * grid));
+    }
+    launch_pdl(gemm_bf16_kernel<kEpi, kBN>, dim3(grid), dim3(kGThreads), smem, s, pdl, tm, tmy, tmr, a);
+    if (trace_on) {  // debug timeline: µs after the first CTA started, min / median / max over CTAs
+        std::vector<unsigned long long> tr(static_cast<size_t>(16) * grid);
+        GFX_CUDA(cudaStreamSynchronize(s));
+        GFX_CUDA(cudaMemcpy(tr.data(), a.trace, tr.size() * 8, cudaMemcpyDeviceToHost));
+        GFX_CUDA(cudaFree(a.trace));
+        unsigned long long t0 = ~0ull;
+        for (int c = 0; c < grid; ++c) t0 = std::min(t0, tr[c * 16]);
+        static const char* nm[16] = {"start", "setup", "first stage", "mma0 issued", "mma1 issued", "mma2 issued",
+                                     "mma3 issued", "acc0 ready", "acc1 ready", "acc2 ready", "acc3 ready",
+                                     "tile0 stored", "tile1 stored", "tile2 stored", "tile3 stored", ""};
+        std::fprintf(stderr, "[gemm trace] T %d K %d N %d tile 128x%d grid %d tiles %d\n", T, K, N, kBN, grid, tiles);
+        for (int ph = 0; ph < 15; ++ph) {
+            std::vector<double> v;
+            for (int c = 0; c < grid; ++c)
+                if (tr[c * 16 + ph]) v.push_back((tr[c * 16 + ph] - t0) * 1e-3);
+            if (v.empty()) continue;
+            std::sort(v.begin(), v.end());
+            std::fprintf(stderr, "  %-14s n=%3zu %8.2f %8.2f %8.2f\n", nm[ph], v.size(), v.front(), v[v.size() / 2],
+                         v.back());
+        }
+    }
 }
 
-// 128 x 256 tiles when N leaves enough of them to fill the GPU, else 128 x 128.
+// 128 x 256 tiles: a tcgen05.mma with smem operands costs >= ~119 cycles
+// whatever N (tools/gemm_rate.cu: N=256 runs at its 128-cycle floor, N=128 at
+// 119 vs 64), so the widest tile wins even when it leaves SMs idle (N = 768:
+// 96 tiles). 128 x 192 was measured at ~210 cycles per MMA.
 template <int kEpi>
 void gemm(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_off, const __nv_bfloat16* x,
           __nv_bfloat16* y, const __nv_bfloat16* resid, int T, int K, int N, cudaStream_t s, bool pdl) {
     if (T % kGM || N % 128 || K % kGK) throw std::runtime_error("bert gemm: T, N multiple of 128, K of 64");
-    static const int force_bn = std::getenv("GFX_BERT_BN") ? std::atoi(std::getenv("GFX_BERT_BN")) : 0;  // debug A/B
-    if (N % 256 == 0 && (force_bn == 256 || (force_bn == 0 && (T / kGM) * (N / 256) >= 148)))
+    if (N % 256 == 0)
         gemm_bn<kEpi, 256>(arena, pt, w_off, b_off, x, y, resid, T, K, N, s, pdl);
     else
         gemm_bn<kEpi, 128>(arena, pt, w_off, b_off, x, y, resid, T, K, N, s, pdl);
