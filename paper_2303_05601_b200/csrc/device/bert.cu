@@ -64,11 +64,23 @@ struct GemmArgs {
     PageTable pt;
 };
 
-template <int kEpi, int kBN>
+// kPair: 2-SM tcgen05 (cta_group::2). A CTA pair (cluster of 2) computes a
+// 256 x kBN tile: each CTA stages its own 128 rows of A and its half of the
+// kBN rows of B (32 KB per K stage instead of 48 KB), the even CTA issues one
+// M = 256 MMA per K slice that reads both CTAs' smem, and each CTA's TMEM holds
+// its own 128 rows of D for its own epilogue. Halving the per-CTA stage is the
+// point: 6 stages (1.6 µs of MMA work) instead of 4 (1.07 µs) cover the TMA
+// latency under load, which bounded the single-CTA MMA phase at ~78 % of
+// issue rate (GFX_TRACE_GEMM; multicasting B alone did not help).
+// Barriers: each CTA's full barrier counts its own bytes; the odd CTA's warp 1
+// relays "stage s landed" to the even CTA's pair_full; the issuer's commits
+// multicast to both CTAs' empty / tfull barriers; both epilogues arrive on the
+// even CTA's tempty.
+template <int kEpi, int kBN, bool kPair>
 __global__ void __launch_bounds__(kGThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_y,
                      const __grid_constant__ CUtensorMap tmap_r, const __grid_constant__ GemmArgs a) {
-    constexpr uint32_t kBBytes = kBN * 128;            // B: kBN rows x 64 bf16
+    constexpr uint32_t kBBytes = (kPair ? kBN / 2 : kBN) * 128;  // B: this CTA's rows x 64 bf16
     constexpr uint32_t kStage = kGATile + kBBytes;
     constexpr int kStages = static_cast<int>(kGSmem / kStage);
     constexpr uint32_t kTmemCols = 2 * kBN <= 256 ? 256 : 512;
@@ -79,6 +91,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
     // (and the residual load).
     uint8_t* stage_out = smem + kGSmem;
     __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], tfull_bar[2], tempty_bar[2], res_bar[2][2];
+    __shared__ __align__(8) uint64_t pair_full[kStages];
     __shared__ uint32_t tmem_s;
     __shared__ uint32_t pt[GFX_MAX_PAGES];
     __shared__ float bias_s[kBN];
@@ -91,7 +104,20 @@ __global__ void __launch_bounds__(kGThreads, 1)
         a.trace[blockIdx.x * 16 + i] = t;
     };
     if (tid == 0) mark(0);
-    const int n_tiles = a.N / kBN, m_tiles = a.T / kGM, tiles = n_tiles * m_tiles;
+    auto smark = [&](int g, int i) {  // per-stage timeline of CTAs 0 and 1 (GFX_TRACE_GEMM)
+        if (a.trace == nullptr || blockIdx.x > 1 || g >= 64) return;
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        a.trace[static_cast<size_t>(gridDim.x) * 16 + blockIdx.x * 256 + g * 4 + i] = t;
+    };
+    const int n_tiles = a.N / kBN, m_tiles = a.T / kGM;
+    // Tile sequence of this CTA: single -> tiles t = blockIdx.x (step grid);
+    // pair -> pair tiles t = cluster id (step clusters), rows 2*(t / n) + rank.
+    const uint32_t rank = kPair ? cluster_ctarank() : 0u;
+    const int t_first = kPair ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+    const int t_step = kPair ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
+    const int tiles = kPair ? n_tiles * (m_tiles / 2) : n_tiles * m_tiles;
+    auto tile_m0 = [&](int t) { return kPair ? ((t / n_tiles) * 2 + static_cast<int>(rank)) * kGM : (t / n_tiles) * kGM; };
     const int nk = a.K / kGK;
     const int ktiles_row = a.K / kGK;  // blob weight tiles per 128 rows
 
@@ -100,10 +126,11 @@ __global__ void __launch_bounds__(kGThreads, 1)
         for (int s = 0; s < kStages; ++s) {
             mbar_init(&full_bar[s], 1);
             mbar_init(&empty_bar[s], 1);
+            mbar_init(&pair_full[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull_bar[b], 1);
-            mbar_init(&tempty_bar[b], 256);
+            mbar_init(&tempty_bar[b], kPair ? 16 : 8);  // epilogue warps (of both CTAs in pair mode)
             mbar_init(&res_bar[0][b], 1);
             mbar_init(&res_bar[1][b], 1);
         }
@@ -112,9 +139,15 @@ __global__ void __launch_bounds__(kGThreads, 1)
         tma_prefetch_desc(&tmap_y);
         if (kEpi == kEpiResid) tma_prefetch_desc(&tmap_r);
     }
-    if (warp == 1) tmem_alloc<kTmemCols>(&tmem_s);
+    if (warp == 1) {
+        if (kPair)
+            tmem_alloc_pair<kTmemCols>(&tmem_s);
+        else
+            tmem_alloc<kTmemCols>(&tmem_s);
+    }
     tc_fence_before();
     __syncthreads();
+    if (kPair) cluster_sync();  // the peer's barriers exist before any remote arrive reaches them
     tc_fence_after();
     const uint32_t tmem = tmem_s;
     if (tid == 0) mark(1);
@@ -124,16 +157,20 @@ __global__ void __launch_bounds__(kGThreads, 1)
             // Producer: one continuous stage ring across this CTA's tiles.
             int g = 0;
             bool waited = false;
-            for (int t = blockIdx.x; t < tiles; t += gridDim.x) {
-                const int m0 = (t / n_tiles) * kGM, nb = t % n_tiles;
+            for (int t = t_first; t < tiles; t += t_step) {
+                const int m0 = tile_m0(t), nb = t % n_tiles;
                 for (int k = 0; k < nk; ++k, ++g) {
                     const int s = g % kStages;
                     if (g >= kStages) mbar_wait(&empty_bar[s], ((g / kStages) & 1) ^ 1);
                     uint8_t* st = smem + static_cast<size_t>(s) * kStage;
                     mbar_arrive_expect_tx(&full_bar[s], kStage);
+                    // Weights first (independent of the previous kernel); pair: this
+                    // CTA's half of the kBN rows (blob tiles of 128 rows).
+                    constexpr int kBTiles = static_cast<int>(kBBytes / kGATile);
 #pragma unroll
-                    for (int h = 0; h < kBN / 128; ++h) {  // weights first: independent of the previous kernel
-                        const uint64_t v = a.w_off + (static_cast<uint64_t>(nb * (kBN / 128) + h) * ktiles_row + k) * kGATile;
+                    for (int h = 0; h < kBTiles; ++h) {
+                        const int bt = nb * (kBN / 128) + (kPair ? static_cast<int>(rank) * kBTiles : 0) + h;
+                        const uint64_t v = a.w_off + (static_cast<uint64_t>(bt) * ktiles_row + k) * kGATile;
                         tma_bulk_g2s(st + kGATile + h * kGATile, translate(a.arena, pt, v), kGATile, &full_bar[s]);
                     }
                     if (!waited) {
@@ -141,31 +178,59 @@ __global__ void __launch_bounds__(kGThreads, 1)
                         waited = true;
                     }
                     tma_tile2d_g2s(st, &tmap_x, k * kGK, m0, &full_bar[s]);
+                    smark(g, 0);
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            constexpr uint32_t idesc = umma_idesc<kGM, kBN, 1>();  // BF16 x BF16 -> F32, M=128, N=kBN
+        if (kPair && rank == 1) {
+            // Odd CTA of the pair: relay "my half of stage s landed" to the issuer.
+            if (lane == 0) {
+                int g = 0;
+                for (int t = t_first; t < tiles; t += t_step)
+                    for (int k = 0; k < nk; ++k, ++g) {
+                        const int s = g % kStages;
+                        mbar_wait(&full_bar[s], (g / kStages) & 1);
+                        smark(g, 1);
+                        mbar_arrive_remote(&pair_full[s], 0);
+                        smark(g, 2);
+                    }
+            }
+        } else if (lane == 0) {
+            constexpr uint32_t idesc = umma_idesc<kPair ? 2 * kGM : kGM, kBN, 1>();  // BF16 x BF16 -> F32
             int g = 0, i = 0;
-            for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
+            for (int t = t_first; t < tiles; t += t_step, ++i) {
                 const int b = i & 1;
-                if (i >= 2) mbar_wait(&tempty_bar[b], ((i >> 1) & 1) ^ 1);  // epilogue drained tile i-2
+                if (i >= 2) mbar_wait(&tempty_bar[b], ((i >> 1) & 1) ^ 1);  // epilogue(s) drained tile i-2
                 tc_fence_after();
                 const uint32_t acc = tmem + static_cast<uint32_t>(b * kBN);
                 for (int k = 0; k < nk; ++k, ++g) {
                     const int s = g % kStages;
                     mbar_wait(&full_bar[s], (g / kStages) & 1);
+                    smark(g, 1);
+                    if (kPair) mbar_wait(&pair_full[s], (g / kStages) & 1);
+                    smark(g, 2);
                     tc_fence_after();
                     if (g == 0) mark(2);
                     uint8_t* st = smem + static_cast<size_t>(s) * kStage;
 #pragma unroll
-                    for (int kk = 0; kk < kGK / 16; ++kk)  // K = 16 bf16 = 32 bytes per MMA
-                        umma_f16(acc, umma_desc_sw128(st, kk * 32), umma_desc_sw128(st + kGATile, kk * 32), idesc,
-                                 (k | kk) ? 1u : 0u);
-                    umma_commit(&empty_bar[s]);
+                    for (int kk = 0; kk < kGK / 16; ++kk) {  // K = 16 bf16 = 32 bytes per MMA
+                        const uint64_t ad = umma_desc_sw128(st, kk * 32), bd = umma_desc_sw128(st + kGATile, kk * 32);
+                        if (kPair)
+                            umma_f16_pair(acc, ad, bd, idesc, (k | kk) ? 1u : 0u);
+                        else
+                            umma_f16(acc, ad, bd, idesc, (k | kk) ? 1u : 0u);
+                    }
+                    smark(g, 3);
+                    if (kPair)
+                        umma_commit_pair_multicast(&empty_bar[s], 0x3);
+                    else
+                        umma_commit(&empty_bar[s]);
                 }
-                umma_commit(&tfull_bar[b]);
+                if (kPair)
+                    umma_commit_pair_multicast(&tfull_bar[b], 0x3);
+                else
+                    umma_commit(&tfull_bar[b]);
                 if (i < 4) mark(3 + i);  // last MMA of tile i issued
             }
         }
@@ -177,8 +242,8 @@ __global__ void __launch_bounds__(kGThreads, 1)
         const uint32_t hbar = 1u + static_cast<uint32_t>(h);
         auto half_sync = [&] { asm volatile("bar.sync %0, 128;\n" ::"r"(hbar) : "memory"); };
         int i = 0, e = 0;
-        for (int t = blockIdx.x; t < tiles; t += gridDim.x, ++i) {
-            const int m0 = (t / n_tiles) * kGM, n0 = (t % n_tiles) * kBN;
+        for (int t = t_first; t < tiles; t += t_step, ++i) {
+            const int m0 = tile_m0(t), n0 = (t % n_tiles) * kBN;
             const int b = i & 1;
             asm volatile("bar.sync 3, 256;\n" ::: "memory");  // previous tile's bias reads done
             for (int c = ct; c < kBN; c += 256)
@@ -187,7 +252,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
             mbar_wait(&tfull_bar[b], (i >> 1) & 1);
             tc_fence_after();
             if (ct == 0 && i < 4) mark(7 + i);  // tile i accumulated
-            if (t + static_cast<int>(gridDim.x) >= tiles) pdl_trigger();  // last tile: let the next kernel start
+            if (t + t_step >= tiles) pdl_trigger();  // last tile: let the next kernel start
             // Thread = accumulator row (TMEM lane q*32+lane) = output row m0 + q*32 + lane.
             // Per 32-column chunk: TMEM -> registers -> bias / GELU / residual ->
             // bf16 into a staging box (row = 64 B, SWIZZLE_64B: chunk j of row r
@@ -248,15 +313,27 @@ __global__ void __launch_bounds__(kGThreads, 1)
                 }
             }
             tc_fence_before();
-            mbar_arrive(&tempty_bar[b]);  // accumulator b free for tile i+2
+            __syncwarp();
+            if (lane == 0) {  // accumulator b free for tile i+2 (the issuer's barrier)
+                if (kPair && rank == 1)
+                    mbar_arrive_remote(&tempty_bar[b], 0);
+                else
+                    mbar_arrive(&tempty_bar[b]);
+            }
             if (ct == 0 && i < 4) mark(11 + i);  // tile i stored
         }
         if (ht == 0) bulk_wait_group<0>();  // every output box written before the CTA exits
     }
     tc_fence_before();
     __syncthreads();
+    if (kPair) cluster_sync();  // no MMA / remote arrive may target an exited CTA
     tc_fence_after();
-    if (warp == 1) tmem_dealloc<kTmemCols>(tmem);
+    if (warp == 1) {
+        if (kPair)
+            tmem_dealloc_pair<kTmemCols>(tmem);
+        else
+            tmem_dealloc<kTmemCols>(tmem);
+    }
 }
 
 // ------------------------------------------------------------------ K3 attention
@@ -396,83 +473,132 @@ template <int kD>
 __global__ void __launch_bounds__(256) layernorm_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
                                                         const char* arena, const __grid_constant__ PageTable ptab,
                                                         uint64_t g_off, uint64_t b_off, int rows) {
-    __shared__ __align__(16) float gam[kD], bet[kD];
-    // gamma / beta: one 16-byte chunk per thread, translated straight from the
-    // page table parameter (256 B-aligned vectors: a chunk never straddles a page).
-    for (int c = threadIdx.x; c < kD / 4; c += 256) {
-        *reinterpret_cast<float4*>(&gam[4 * c]) =
-            *reinterpret_cast<const float4*>(translate(arena, ptab.page, g_off + 16ull * c));
-        *reinterpret_cast<float4*>(&bet[4 * c]) =
-            *reinterpret_cast<const float4*>(translate(arena, ptab.page, b_off + 16ull * c));
-    }
-    __syncthreads();
-    pdl_wait();
+    // One warp per row, kRowsPerWarp rows per warp with every load of a row
+    // issued before any math (HBM latency, not arithmetic, bounds this
+    // kernel). gamma / beta come straight into registers from the arena (lane
+    // l owns columns 8(l + 32i) .. +7, 256 B-aligned vectors: a 16-byte chunk
+    // never straddles a page), no shared-memory staging or block barrier.
+    constexpr int kPer = kD / 256;  // uint4 (8 bf16) chunks per lane per row
+    constexpr int kRowsPerWarp = 2;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int row = blockIdx.x * 8 + warp;
-    if (row >= rows) return;
-    constexpr int kPer = kD / 256;  // uint4 (8 bf16) chunks per lane
-    float v[kPer * 8];
-    const __nv_bfloat16* xr = x + static_cast<size_t>(row) * kD;
+    float gam[kPer * 8], bet[kPer * 8];
 #pragma unroll
     for (int i = 0; i < kPer; ++i) {
-        const uint4 u = *reinterpret_cast<const uint4*>(xr + (i * 32 + lane) * 8);
-        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&u);
+        const uint64_t c = static_cast<uint64_t>(i * 32 + lane) * 8;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const float2 f = __bfloat1622float2(h2[j]);
-            v[i * 8 + 2 * j] = f.x;
-            v[i * 8 + 2 * j + 1] = f.y;
+        for (int hh = 0; hh < 2; ++hh) {
+            const float4 g = *reinterpret_cast<const float4*>(translate(arena, ptab.page, g_off + 4 * (c + 4 * hh)));
+            const float4 bb = *reinterpret_cast<const float4*>(translate(arena, ptab.page, b_off + 4 * (c + 4 * hh)));
+            gam[i * 8 + 4 * hh] = g.x, gam[i * 8 + 4 * hh + 1] = g.y, gam[i * 8 + 4 * hh + 2] = g.z,
+            gam[i * 8 + 4 * hh + 3] = g.w;
+            bet[i * 8 + 4 * hh] = bb.x, bet[i * 8 + 4 * hh + 1] = bb.y, bet[i * 8 + 4 * hh + 2] = bb.z,
+            bet[i * 8 + 4 * hh + 3] = bb.w;
         }
     }
-    float s = 0.f;
+    pdl_wait();
+    const int row0 = (blockIdx.x * 8 + warp) * kRowsPerWarp;
+    uint4 raw[kRowsPerWarp][kPer];
 #pragma unroll
-    for (int i = 0; i < kPer * 8; ++i) s += v[i];
+    for (int rr = 0; rr < kRowsPerWarp; ++rr) {
+        const int row = row0 + rr;
+        if (row >= rows) break;
+        const __nv_bfloat16* xr = x + static_cast<size_t>(row) * kD;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-    const float mean = s / kD;
-    float q = 0.f;
-#pragma unroll
-    for (int i = 0; i < kPer * 8; ++i) {
-        const float t = v[i] - mean;
-        q += t * t;
+        for (int i = 0; i < kPer; ++i) raw[rr][i] = *reinterpret_cast<const uint4*>(xr + (i * 32 + lane) * 8);
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
-    const float rstd = rsqrtf(q / kD + 1e-12f);
-    __nv_bfloat16* yr = y + static_cast<size_t>(row) * kD;
+    for (int rr = 0; rr < kRowsPerWarp; ++rr) {
+        const int row = row0 + rr;
+        if (row >= rows) break;
+        float v[kPer * 8];
 #pragma unroll
-    for (int i = 0; i < kPer; ++i) {
-        uint4 u;
-        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
-        const int c0 = (i * 32 + lane) * 8;
+        for (int i = 0; i < kPer; ++i) {
+            const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw[rr][i]);
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-            h2[j] = __floats2bfloat162_rn((v[i * 8 + 2 * j] - mean) * rstd * gam[c0 + 2 * j] + bet[c0 + 2 * j],
-                                          (v[i * 8 + 2 * j + 1] - mean) * rstd * gam[c0 + 2 * j + 1] + bet[c0 + 2 * j + 1]);
-        *reinterpret_cast<uint4*>(yr + c0) = u;
+            for (int j = 0; j < 4; ++j) {
+                const float2 f = __bfloat1622float2(h2[j]);
+                v[i * 8 + 2 * j] = f.x;
+                v[i * 8 + 2 * j + 1] = f.y;
+            }
+        }
+        float s = 0.f;
+#pragma unroll
+        for (int i = 0; i < kPer * 8; ++i) s += v[i];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        const float mean = s / kD;
+        float q = 0.f;
+#pragma unroll
+        for (int i = 0; i < kPer * 8; ++i) {
+            const float t = v[i] - mean;
+            q += t * t;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+        const float rstd = rsqrtf(q / kD + 1e-12f);
+        __nv_bfloat16* yr = y + static_cast<size_t>(row) * kD;
+#pragma unroll
+        for (int i = 0; i < kPer; ++i) {
+            uint4 u;
+            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                h2[j] = __floats2bfloat162_rn((v[i * 8 + 2 * j] - mean) * rstd * gam[i * 8 + 2 * j] + bet[i * 8 + 2 * j],
+                                              (v[i * 8 + 2 * j + 1] - mean) * rstd * gam[i * 8 + 2 * j + 1] +
+                                                  bet[i * 8 + 2 * j + 1]);
+            *reinterpret_cast<uint4*>(yr + (i * 32 + lane) * 8) = u;
+        }
     }
 }
 
 // ------------------------------------------------------------------ pooler
 
+// Pooler: out[b][n] = tanh(Wp[n] . x[b, token 0] + bp[n]) for the batch's
+// [CLS] rows — a 32 x 768 x 768 product. Block = 8 output features (one warp
+// each); the [CLS] rows are staged in shared memory once per block; each lane
+// holds 3 16-byte chunks of its warp's weight row in registers (swizzled blob
+// tile layout, one page translation per chunk).
 __global__ void __launch_bounds__(256) pooler_kernel(const __nv_bfloat16* __restrict__ x, float* __restrict__ out,
-                                                     const char* arena, PageTable ptab, uint64_t w_off, uint64_t b_off,
-                                                     int d, int seq, int batch) {
-    __shared__ uint32_t pt[GFX_MAX_PAGES];
-    for (int i = threadIdx.x; i < static_cast<int>(ptab.n); i += 256) pt[i] = ptab.page[i];
-    __syncthreads();
-    pdl_wait();
+                                                     const char* arena, const __grid_constant__ PageTable ptab,
+                                                     uint64_t w_off, uint64_t b_off, int d, int seq, int batch) {
+    constexpr int kD = 768, kChunks = kD / 8 / 32;  // 16-byte chunks per lane
+    extern __shared__ __align__(16) uint8_t cls_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n = blockIdx.x * 8 + warp;
+    uint4 w[kChunks];
+    float bias = 0.f;
+    if (n < d) {
+#pragma unroll
+        for (int i = 0; i < kChunks; ++i) {
+            const int k = (i * 32 + lane) * 8;
+            const uint64_t r = static_cast<uint64_t>(n % 128);
+            const uint64_t off = w_off + (static_cast<uint64_t>(n / 128) * (kD / 64) + k / 64) * 16384 + r * 128 +
+                                 ((((k % 64) >> 3) ^ (r & 7)) << 4);
+            w[i] = *reinterpret_cast<const uint4*>(translate(arena, ptab.page, off));
+        }
+        bias = *reinterpret_cast<const float*>(translate(arena, ptab.page, b_off + 4ull * n));
+    }
+    pdl_wait();
+    for (int i = threadIdx.x; i < batch * kD / 8; i += 256) {
+        const int b = i / (kD / 8), c = i % (kD / 8);
+        reinterpret_cast<uint4*>(cls_raw)[i] =
+            *reinterpret_cast<const uint4*>(x + static_cast<size_t>(b) * seq * kD + c * 8);
+    }
+    __syncthreads();
     if (n >= d) return;
-    const float bias = *reinterpret_cast<const float*>(translate(arena, pt, b_off + 4ull * n));
     for (int b = 0; b < batch; ++b) {
-        const __nv_bfloat16* xr = x + static_cast<size_t>(b) * seq * d;  // [CLS] = token 0
         float acc = 0.f;
-        for (int k = lane; k < d; k += 32) {
-            const uint16_t wb =
-                *reinterpret_cast<const uint16_t*>(translate(arena, pt, w_off + bf16_tile_offset(n, k, d)));
-            acc += __uint_as_float(static_cast<uint32_t>(wb) << 16) * __bfloat162float(xr[k]);
+#pragma unroll
+        for (int i = 0; i < kChunks; ++i) {
+            const uint4 xv = reinterpret_cast<const uint4*>(cls_raw)[b * (kD / 8) + i * 32 + lane];
+            const __nv_bfloat162* xh = reinterpret_cast<const __nv_bfloat162*>(&xv);
+            const __nv_bfloat162* wh = reinterpret_cast<const __nv_bfloat162*>(&w[i]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float2 xf = __bfloat1622float2(xh[j]), wf = __bfloat1622float2(wh[j]);
+                acc = fmaf(wf.x, xf.x, acc);
+                acc = fmaf(wf.y, xf.y, acc);
+            }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
@@ -506,7 +632,7 @@ void launch_pdl(Kern k, dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool
     GFX_CUDA(cudaLaunchKernelEx(&cfg, k, args...));
 }
 
-template <int kEpi, int kBN>
+template <int kEpi, int kBN, bool kPair>
 void gemm_bn(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_off, const __nv_bfloat16* x,
              __nv_bfloat16* y, const __nv_bfloat16* resid, int T, int K, int N, cudaStream_t s, bool pdl) {
     CUtensorMap tm;
@@ -530,7 +656,7 @@ void gemm_bn(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_
     const size_t smem = kGSmem + 4 * 8192 + 1024;
     static int sms = 0;
     if (!attr_set) {
-        GFX_CUDA(cudaFuncSetAttribute(gemm_bf16_kernel<kEpi, kBN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        GFX_CUDA(cudaFuncSetAttribute(gemm_bf16_kernel<kEpi, kBN, kPair>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       static_cast<int>(smem)));
         int dev = 0;
         GFX_CUDA(cudaGetDevice(&dev));
@@ -538,14 +664,33 @@ void gemm_bn(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_
         attr_set = true;
     }
     const int tiles = (T / kGM) * (N / kBN);
-    const int grid = tiles < sms ? tiles : sms;
+    int grid = tiles < sms ? tiles : sms;
+    if (kPair) grid &= ~1;
     if (trace_on) {
-        GFX_CUDA(cudaMalloc(&a.trace, sizeof(unsigned long long) * 16 * grid));
-        GFX_CUDA(cudaMemset(a.trace, 0, sizeof(unsigned long long) * 16 * grid));
+        GFX_CUDA(cudaMalloc(&a.trace, sizeof(unsigned long long) * (16 * grid + 512)));
+        GFX_CUDA(cudaMemset(a.trace, 0, sizeof(unsigned long long) * (16 * grid + 512)));
     }
-    launch_pdl(gemm_bf16_kernel<kEpi, kBN>, dim3(grid), dim3(kGThreads), smem, s, pdl, tm, tmy, tmr, a);
+    if (kPair) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kGThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[2];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
+        attr[1].id = cudaLaunchAttributeClusterDimension;
+        attr[1].val.clusterDim.x = 2;
+        attr[1].val.clusterDim.y = 1;
+        attr[1].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 2;
+        GFX_CUDA(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<kEpi, kBN, kPair>, tm, tmy, tmr, a));
+    } else {
+        launch_pdl(gemm_bf16_kernel<kEpi, kBN, kPair>, dim3(grid), dim3(kGThreads), smem, s, pdl, tm, tmy, tmr, a);
+    }
     if (trace_on) {  // debug timeline: µs after the first CTA started, min / median / max over CTAs
-        std::vector<unsigned long long> tr(static_cast<size_t>(16) * grid);
+        std::vector<unsigned long long> tr(static_cast<size_t>(16) * grid + 512);
         GFX_CUDA(cudaStreamSynchronize(s));
         GFX_CUDA(cudaMemcpy(tr.data(), a.trace, tr.size() * 8, cudaMemcpyDeviceToHost));
         GFX_CUDA(cudaFree(a.trace));
@@ -564,6 +709,14 @@ void gemm_bn(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_
             std::fprintf(stderr, "  %-14s n=%3zu %8.2f %8.2f %8.2f\n", nm[ph], v.size(), v.front(), v[v.size() / 2],
                          v.back());
         }
+        std::fprintf(stderr, "  stages (us): CTA0 [TMA issued, full seen, pair seen, MMA issued] | CTA1 [TMA issued, full seen, relayed]\n");
+        auto us = [&](unsigned long long t) { return t ? (t - t0) * 1e-3 : -1.0; };
+        for (int g = 0; g < 24; ++g) {
+            const unsigned long long* c0 = tr.data() + 16 * grid + g * 4;
+            const unsigned long long* c1 = tr.data() + 16 * grid + 256 + g * 4;
+            std::fprintf(stderr, "   %2d %7.2f %7.2f %7.2f %7.2f | %7.2f %7.2f %7.2f\n", g, us(c0[0]), us(c0[1]), us(c0[2]),
+                         us(c0[3]), us(c1[0]), us(c1[1]), us(c1[2]));
+        }
     }
 }
 
@@ -575,10 +728,17 @@ template <int kEpi>
 void gemm(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_off, const __nv_bfloat16* x,
           __nv_bfloat16* y, const __nv_bfloat16* resid, int T, int K, int N, cudaStream_t s, bool pdl) {
     if (T % kGM || N % 128 || K % kGK) throw std::runtime_error("bert gemm: T, N multiple of 128, K of 64");
-    if (N % 256 == 0)
-        gemm_bn<kEpi, 256>(arena, pt, w_off, b_off, x, y, resid, T, K, N, s, pdl);
+    // The 2-SM variant (GFX_GEMM_PAIR=1) is correct but measured slower: with 6
+    // stages of 32 KB in flight per CTA its TMA latency rose to ~3 µs per stage
+    // (1.2 vs 1.6 ms per forward; per-stage trace in GFX_TRACE_GEMM), so the
+    // single-CTA 128 x 256 kernel is the default until that is understood.
+    static const bool pair = std::getenv("GFX_GEMM_PAIR") != nullptr;
+    if (N % 256 == 0 && (T / kGM) % 2 == 0 && pair)
+        gemm_bn<kEpi, 256, true>(arena, pt, w_off, b_off, x, y, resid, T, K, N, s, pdl);
+    else if (N % 256 == 0)
+        gemm_bn<kEpi, 256, false>(arena, pt, w_off, b_off, x, y, resid, T, K, N, s, pdl);
     else
-        gemm_bn<kEpi, 128>(arena, pt, w_off, b_off, x, y, resid, T, K, N, s, pdl);
+        gemm_bn<kEpi, 128, false>(arena, pt, w_off, b_off, x, y, resid, T, K, N, s, pdl);
 }
 
 }  // namespace
@@ -665,11 +825,11 @@ int bert_forward(const char* arena, const PageTable& pt, const BertLayout& lay, 
         launch_pdl(attention_kernel, dim3(batch * lay.heads), dim3(256), 0, s, true,
                    static_cast<const __nv_bfloat16*>(ws.qkv), ws.ctx, lay.heads);
         gemm<kEpiResid>(arena, pt, o.wo, o.bo, ws.ctx, ws.t, x, T, d, d, s, true);
-        launch_pdl(layernorm_kernel<768>, dim3((T + 7) / 8), dim3(256), 0, s, true,
+        launch_pdl(layernorm_kernel<768>, dim3((T + 15) / 16), dim3(256), 0, s, true,
                    static_cast<const __nv_bfloat16*>(ws.t), ws.h, arena, pt, o.ln1_g, o.ln1_b, T);
         gemm<kEpiGelu>(arena, pt, o.w1, o.b1, ws.h, ws.f, nullptr, T, d, lay.ffn, s, true);
         gemm<kEpiResid>(arena, pt, o.w2, o.b2, ws.f, ws.t, ws.h, T, lay.ffn, d, s, true);
-        launch_pdl(layernorm_kernel<768>, dim3((T + 7) / 8), dim3(256), 0, s, true,
+        launch_pdl(layernorm_kernel<768>, dim3((T + 15) / 16), dim3(256), 0, s, true,
                    static_cast<const __nv_bfloat16*>(ws.t), ws.x, arena, pt, o.ln2_g, o.ln2_b, T);
         launches += 7;
         x = ws.x;
@@ -677,7 +837,15 @@ int bert_forward(const char* arena, const PageTable& pt, const BertLayout& lay, 
             GFX_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(hidden) + (l + 1) * hbytes, ws.x, hbytes,
                                      cudaMemcpyDeviceToDevice, s));
     }
-    launch_pdl(pooler_kernel, dim3((d + 7) / 8), dim3(256), 0, s, !hidden, static_cast<const __nv_bfloat16*>(x), out,
+    if (d != 768 || static_cast<size_t>(batch) * d * 2 > 160 * 1024)
+        throw std::runtime_error("bert pooler: d = 768 and at most 106 sequences per request");
+    static bool pool_attr = false;
+    if (!pool_attr) {
+        GFX_CUDA(cudaFuncSetAttribute(pooler_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+        pool_attr = true;
+    }
+    launch_pdl(pooler_kernel, dim3((d + 7) / 8), dim3(256), static_cast<size_t>(batch) * d * 2, s, !hidden,
+               static_cast<const __nv_bfloat16*>(x), out,
                arena, pt, lay.wp, lay.bp, d, lay.seq, batch);
     return launches + 1;
 }
