@@ -111,6 +111,10 @@ __device__ __forceinline__ void wait_count(const unsigned* p, unsigned target) {
     while (ld_acquire(p) < target) {
     }
 }
+// Release/acquire fence at GPU scope (MEMBAR.ALL.GPU), not __threadfence()'s
+// sequentially consistent MEMBAR.SC.GPU: the dataflow flags only need
+// "writes before the flag are visible to whoever acquires it".
+__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;\n" ::: "memory"); }
 __device__ __forceinline__ void fence_proxy_async_global() {
     asm volatile("fence.proxy.async.global;\n" ::: "memory");
 }
@@ -537,7 +541,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 epi_sync();  // CTA-scope ordering; thread 0's gpu fence is cumulative over it
                 if (ct == 0) {
                     if (l == 0) mark(a.trace, 18);
-                    __threadfence();
+                    fence_acq_rel_gpu();
                     if (l == 0) mark(a.trace, 19);
                     atomicAdd(cnt + kCntArrive + l * 64 + u.tile, 1u);
                     if (l == 0) mark(a.trace, 20);
@@ -581,7 +585,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             epi_sync();
             if (ct == 0) {
                 if (l == 0) mark(a.trace, 25);
-                __threadfence();
+                fence_acq_rel_gpu();
                 if (l == 0) mark(a.trace, 30);
                 atomicAdd(cnt + kCntDone + l * 64 + u.tile, 1u);
                 if (last) atomicAdd(cnt + kCntFinal, 1u);
