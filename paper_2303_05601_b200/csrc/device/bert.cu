@@ -3,14 +3,15 @@
 //
 // Kernels:
 //   K2 gemm_bf16_kernel   Y[T x N] = epi(X[T x K] . W^T + b) on tcgen05
-//                         (kind::f16, bf16 -> fp32 in TMEM), 128x128 tiles, X via
-//                         a 2-D TMA tensor map, W tiles (pre-swizzled 16 KB) via
-//                         1-D bulk TMA from the arena; epilogue fused: bias,
-//                         GELU, or residual add; bf16 out. Tensor-core bound.
-//   K3 attention_kernel   softmax(Q K^T / sqrt(64)) V per (sequence, head),
-//                         S = 128: one CTA, 8 warps x 16 query rows, warp-level
-//                         mma.sync (bf16 -> fp32) flash-attention-2 style; 2.7 %
-//                         of the model's flops.
+//                         (kind::f16, bf16 -> fp32 in TMEM), persistent 128 x 256
+//                         tiles, X via a 2-D TMA tensor map, W tiles
+//                         (pre-swizzled 16 KB) via 1-D bulk TMA from the arena,
+//                         double-buffered TMEM accumulators; fused bias / GELU /
+//                         residual epilogue through TMA stores; bf16 out.
+//                         Tensor-core bound. Opt-in 2-SM (cta_group::2) variant.
+//   K3 attention_tc_kernel softmax(Q K^T / sqrt(64)) V per (sequence, head),
+//                         S = 128: one CTA of 4 warps, both products on tcgen05
+//                         (V read MN-major), softmax from TMEM by the row's thread.
 //   K4 layernorm_kernel   one warp per token row, 16-byte vector loads, fp32
 //                         two-pass statistics; HBM bound.
 //   pooler_kernel         tanh(Wp . x_cls + bp) per sequence, fp32 out.
@@ -337,134 +338,158 @@ __global__ void __launch_bounds__(kGThreads, 1)
 }
 
 // ------------------------------------------------------------------ K3 attention
-// One CTA per (sequence, head), S = 128 tokens, d_head = 64. Warp w owns query
-// rows 16w..16w+15; mma.sync m16n8k16 bf16 -> fp32.
 
 constexpr int kS = 128, kDh = 64;
-constexpr int kKPitch = kDh + 8;   // bf16 per K / V row in smem (144 B: conflict-free LDS.32 and ldmatrix)
 
-__device__ __forceinline__ void mma_bf16_16816(float (&c)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-        "{%0,%1,%2,%3};\n"
-        : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
-}
-__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
-    __nv_bfloat162 h = __floats2bfloat162_rn(lo, hi);
-    return *reinterpret_cast<uint32_t*>(&h);
-}
+// One CTA (4 warps) per (sequence, head): S = Q K^T (M = 128 queries, N = 128
+// keys, K = 64: four kind::f16 MMAs into TMEM), row softmax by the thread that
+// owns the row's TMEM lane (P = exp((s - max) / 8) unnormalised, bf16, written
+// as the next MMA's K-major SWIZZLE_128B A operand), O = P V (M = 128, N = 64,
+// K = 128: V is read MN-major straight from its token-major tile), O / sum.
+// Q, K, V arrive by three 2-D TMA boxes (64 dims x 128 tokens) from the fused
+// QKV activation. (The first version used warp-level mma.sync; 2.7 % of the
+// model's flops took 12 % of its time there.) Phase trace: GFX_TRACE_ATTN=1.
+constexpr uint32_t kAttnSmem = 3 * 16384 + 1024;  // Q, K, V; P overlays Q + K once S is computed
 
-__device__ __forceinline__ void ldsm_x4_trans(uint32_t (&r)[4], const void* p) {
-    asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];\n"
-                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-                 : "r"(smem_u32(p)));
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
 }
 
-__global__ void __launch_bounds__(256) attention_kernel(const __nv_bfloat16* __restrict__ qkv,
-                                                        __nv_bfloat16* __restrict__ ctx, int heads) {
-    __shared__ __align__(16) __nv_bfloat16 ks[kS * kKPitch];
-    __shared__ __align__(16) __nv_bfloat16 vs[kS * kKPitch];
+__global__ void __launch_bounds__(128, 4) attention_tc_kernel(const __grid_constant__ CUtensorMap tmap_qkv,
+                                                           __nv_bfloat16* __restrict__ ctx, int heads,
+                                                           unsigned long long* trace) {
+    auto amark = [&](int i) {  // debug timeline (GFX_TRACE_ATTN)
+        if (trace == nullptr || threadIdx.x != 0) return;
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+        trace[blockIdx.x * 8 + i] = t;
+    };
+    amark(0);
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* qs = sm;
+    uint8_t* ks = sm + 16384;
+    uint8_t* vs = sm + 32768;
+    uint8_t* ps = sm;  // P (keys 0-63 block, keys 64-127 block) over Q and K: dead after the S MMAs
+    __shared__ __align__(8) uint64_t ld_bar, s_bar, o_bar;
+    __shared__ uint32_t tmem_s;
     const int seq = blockIdx.x / heads, h = blockIdx.x % heads;
-    const int d = heads * kDh, ld = 3 * d;
-    const size_t tok0 = static_cast<size_t>(seq) * kS;
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    pdl_wait();
-    // K and V rows (128 B each) into padded shared rows, 16-byte cp.async chunks.
-    for (int i = tid; i < kS * (kDh / 8); i += 256) {
-        const int t = i / (kDh / 8), c = (i % (kDh / 8)) * 8;
-        const __nv_bfloat16* src = qkv + (tok0 + t) * ld + h * kDh + c;
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(&ks[t * kKPitch + c])), "l"(src + d));
-        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(&vs[t * kKPitch + c])),
-                     "l"(src + 2 * d));
+    const int d = heads * kDh;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    if (tid == 0) {
+        mbar_init(&ld_bar, 1);
+        mbar_init(&s_bar, 1);
+        mbar_init(&o_bar, 1);
+        mbar_fence_init();
+        tma_prefetch_desc(&tmap_qkv);
     }
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-    const int g = lane >> 2, tq = lane & 3;  // mma fragment coordinates
-    const int r0 = warp * 16 + g;            // this thread's query rows: r0, r0 + 8
-    // Q fragments for the 4 k16 steps of d_head = 64.
-    uint32_t qa[4][4];
-    const __nv_bfloat16* q0 = qkv + (tok0 + r0) * ld + h * kDh;
-    const __nv_bfloat16* q1 = q0 + 8 * static_cast<size_t>(ld);
-#pragma unroll
-    for (int kk = 0; kk < 4; ++kk) {
-        const int c = kk * 16 + 2 * tq;
-        qa[kk][0] = *reinterpret_cast<const uint32_t*>(q0 + c);
-        qa[kk][1] = *reinterpret_cast<const uint32_t*>(q1 + c);
-        qa[kk][2] = *reinterpret_cast<const uint32_t*>(q0 + c + 8);
-        qa[kk][3] = *reinterpret_cast<const uint32_t*>(q1 + c + 8);
-    }
-    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    if (warp == 0) tmem_alloc<128>(&tmem_s);  // S: columns 0-127; O reuses 0-63 after the softmax read S
+    tc_fence_before();
     __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = tmem_s;
+    amark(1);
+    pdl_wait();
+    if (tid == 0) {
+        mbar_arrive_expect_tx(&ld_bar, 3 * 16384);
+        tma_tile2d_g2s(qs, &tmap_qkv, h * kDh, seq * kS, &ld_bar);
+        tma_tile2d_g2s(ks, &tmap_qkv, d + h * kDh, seq * kS, &ld_bar);
+        tma_tile2d_g2s(vs, &tmap_qkv, 2 * d + h * kDh, seq * kS, &ld_bar);
+        mbar_wait(&ld_bar, 0);
+        amark(2);
+        tc_fence_after();
+        constexpr uint32_t idesc_s = umma_idesc<128, 128, 1>();  // bf16 x bf16 -> f32, both K-major
+#pragma unroll
+        for (int kk = 0; kk < kDh / 16; ++kk)
+            umma_f16(tmem, umma_desc_sw128(qs, kk * 32), umma_desc_sw128(ks, kk * 32), idesc_s, kk ? 1u : 0u);
+        umma_commit(&s_bar);
+    }
     pdl_trigger();
-    // S = Q K^T: 16 n8 tiles of keys.
-    float sc[16][4];
+    // Softmax: thread = query row = TMEM lane (warp w owns lanes 32w..32w+31).
+    mbar_wait(&s_bar, 0);
+    amark(3);
+    tc_fence_after();
+    const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
+    // Two passes over the row's 128 TMEM columns in 32-column chunks (row max,
+    // then exp / sum / bf16 P), so a thread holds 32 scores, not 128: registers
+    // for four CTAs per SM.
+    float mx = -INFINITY;
 #pragma unroll
-    for (int nt = 0; nt < 16; ++nt) {
-        sc[nt][0] = sc[nt][1] = sc[nt][2] = sc[nt][3] = 0.f;
+    for (int c = 0; c < kS / 32; ++c) {
+        float part[32];
+        tmem_ld_32x32b_x32(lane_base + static_cast<uint32_t>(c * 32), part);
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-            const __nv_bfloat16* kr = &ks[(nt * 8 + g) * kKPitch + kk * 16 + 2 * tq];
-            const uint32_t b[2] = {*reinterpret_cast<const uint32_t*>(kr), *reinterpret_cast<const uint32_t*>(kr + 8)};
-            mma_bf16_16816(sc[nt], qa[kk], b);
+        for (int j = 0; j < 32; ++j) mx = fmaxf(mx, part[j]);
+    }
+    constexpr float kScaleLog2 = 0.125f * 1.4426950408889634f;  // 1/sqrt(64) * log2(e)
+    const float off = mx * kScaleLog2;
+    float sum = 0.f;
+    const int r = tid;
+#pragma unroll
+    for (int c32 = 0; c32 < kS / 32; ++c32) {
+        float part[32];
+        tmem_ld_32x32b_x32(lane_base + static_cast<uint32_t>(c32 * 32), part);
+#pragma unroll
+        for (int q8 = 0; q8 < 4; ++q8) {  // 16-byte chunks of 8 keys
+            const int c = c32 * 4 + q8;
+            uint4 u;
+            __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const float p0 = ex2_approx(fmaf(part[q8 * 8 + 2 * j], kScaleLog2, -off));
+                const float p1 = ex2_approx(fmaf(part[q8 * 8 + 2 * j + 1], kScaleLog2, -off));
+                sum += p0 + p1;
+                h2[j] = __floats2bfloat162_rn(p0, p1);
+            }
+            const int blk = c >> 3, cc = c & 7;
+            *reinterpret_cast<uint4*>(ps + blk * 16384 + r * 128 + ((cc ^ (r & 7)) << 4)) = u;
         }
     }
-    // Row softmax of S / 8 (rows r0: elements 0,1; r0+8: elements 2,3).
-    const float scale = 0.125f;
-    float m0 = -INFINITY, m1 = -INFINITY;
+    fence_proxy_async_smem();  // P (generic-proxy writes) -> the PV MMA reads
+    tc_fence_before();
+    __syncthreads();
+    amark(4);
+    if (tid == 0) {
+        tc_fence_after();
+        // B = V as an MN-major operand: N = 64 dims contiguous (one 128-byte swizzle
+        // span per key), K = keys in 8-key atoms 1024 B apart (SBO).
+        constexpr uint32_t idesc_o = umma_idesc<128, kDh, 1>() | (1u << 16);  // b_major = MN
 #pragma unroll
-    for (int nt = 0; nt < 16; ++nt) {
-        m0 = fmaxf(m0, fmaxf(sc[nt][0], sc[nt][1]));
-        m1 = fmaxf(m1, fmaxf(sc[nt][2], sc[nt][3]));
+        for (int kk = 0; kk < kS / 16; ++kk)
+            umma_f16(tmem, umma_desc_sw128(ps + (kk >> 2) * 16384, (kk & 3) * 32),
+                     umma_desc_sw128(vs, kk * 2048), idesc_o, kk ? 1u : 0u);
+        umma_commit(&o_bar);
     }
+    mbar_wait(&o_bar, 0);
+    amark(5);
+    tc_fence_after();
+    float o[kDh];
+    {
+        float part[32];
+        tmem_ld_32x32b_x32(lane_base, part);
 #pragma unroll
-    for (int o = 1; o <= 2; o <<= 1) {
-        m0 = fmaxf(m0, __shfl_xor_sync(0xffffffffu, m0, o));
-        m1 = fmaxf(m1, __shfl_xor_sync(0xffffffffu, m1, o));
+        for (int j = 0; j < 32; ++j) o[j] = part[j];
+        tmem_ld_32x32b_x32(lane_base + 32, part);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) o[32 + j] = part[j];
     }
-    float l0 = 0.f, l1 = 0.f;
+    const float inv = 1.0f / sum;
+    uint4* dst = reinterpret_cast<uint4*>(ctx + (static_cast<size_t>(seq) * kS + r) * d + h * kDh);
 #pragma unroll
-    for (int nt = 0; nt < 16; ++nt) {
-        sc[nt][0] = expf((sc[nt][0] - m0) * scale);
-        sc[nt][1] = expf((sc[nt][1] - m0) * scale);
-        sc[nt][2] = expf((sc[nt][2] - m1) * scale);
-        sc[nt][3] = expf((sc[nt][3] - m1) * scale);
-        l0 += sc[nt][0] + sc[nt][1];
-        l1 += sc[nt][2] + sc[nt][3];
+    for (int c = 0; c < kDh / 8; ++c) {
+        uint4 u;
+        __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) h2[j] = __floats2bfloat162_rn(o[c * 8 + 2 * j] * inv, o[c * 8 + 2 * j + 1] * inv);
+        dst[c] = u;
     }
-#pragma unroll
-    for (int o = 1; o <= 2; o <<= 1) {
-        l0 += __shfl_xor_sync(0xffffffffu, l0, o);
-        l1 += __shfl_xor_sync(0xffffffffu, l1, o);
-    }
-    // O = P V: P (bf16) from the S fragments, 8 n8 tiles of d_head.
-    float oc[8][4];
-#pragma unroll
-    for (int dt = 0; dt < 8; ++dt) oc[dt][0] = oc[dt][1] = oc[dt][2] = oc[dt][3] = 0.f;
-#pragma unroll
-    for (int kk = 0; kk < 8; ++kk) {  // 16 keys per step
-        const uint32_t pa[4] = {pack_bf16(sc[2 * kk][0], sc[2 * kk][1]), pack_bf16(sc[2 * kk][2], sc[2 * kk][3]),
-                                pack_bf16(sc[2 * kk + 1][0], sc[2 * kk + 1][1]),
-                                pack_bf16(sc[2 * kk + 1][2], sc[2 * kk + 1][3])};
-        // B fragments of V (keys x dims) for two 8-wide dim tiles per ldmatrix.x4.trans:
-        // lane l addresses row (key) kk*16 + (l&7) + 8*((l>>3)&1), dims + 8*(l>>4).
-#pragma unroll
-        for (int dp = 0; dp < 4; ++dp) {
-            uint32_t bv[4];
-            const int key = kk * 16 + (lane & 7) + (((lane >> 3) & 1) << 3);
-            ldsm_x4_trans(bv, &vs[key * kKPitch + dp * 16 + ((lane >> 4) << 3)]);
-            const uint32_t b0[2] = {bv[0], bv[1]}, b1[2] = {bv[2], bv[3]};
-            mma_bf16_16816(oc[2 * dp], pa, b0);
-            mma_bf16_16816(oc[2 * dp + 1], pa, b1);
-        }
-    }
-    const float i0 = 1.f / l0, i1 = 1.f / l1;
-    __nv_bfloat16* c0 = ctx + (tok0 + r0) * d + h * kDh;
-    __nv_bfloat16* c1 = c0 + 8 * static_cast<size_t>(d);
-#pragma unroll
-    for (int dt = 0; dt < 8; ++dt) {
-        *reinterpret_cast<__nv_bfloat162*>(c0 + dt * 8 + 2 * tq) = __floats2bfloat162_rn(oc[dt][0] * i0, oc[dt][1] * i0);
-        *reinterpret_cast<__nv_bfloat162*>(c1 + dt * 8 + 2 * tq) = __floats2bfloat162_rn(oc[dt][2] * i1, oc[dt][3] * i1);
-    }
+    amark(6);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 0) tmem_dealloc<128>(tmem);
 }
 
 // ------------------------------------------------------------------ K4 LayerNorm
@@ -822,8 +847,43 @@ int bert_forward(const char* arena, const PageTable& pt, const BertLayout& lay, 
     for (int l = 0; l < lay.L; ++l) {
         const BertLayerOffsets& o = lay.layer[static_cast<size_t>(l)];
         gemm<kEpiBias>(arena, pt, o.wqkv, o.bqkv, x, ws.qkv, nullptr, T, d, 3 * d, s, l > 0 && !hidden);
-        launch_pdl(attention_kernel, dim3(batch * lay.heads), dim3(256), 0, s, true,
-                   static_cast<const __nv_bfloat16*>(ws.qkv), ws.ctx, lay.heads);
+        {
+            CUtensorMap tq;
+            if (!encode_tensor_map_2d(&tq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ws.qkv, static_cast<uint64_t>(3 * d),
+                                      static_cast<uint64_t>(T), static_cast<uint64_t>(3 * d) * 2, kDh, kS,
+                                      CU_TENSOR_MAP_SWIZZLE_128B))
+                throw CudaError("cuTensorMapEncodeTiled failed (attention)");
+            static bool attr = false;
+            if (!attr) {
+                GFX_CUDA(cudaFuncSetAttribute(attention_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              static_cast<int>(kAttnSmem)));
+                attr = true;
+            }
+            static const bool atrace = std::getenv("GFX_TRACE_ATTN") != nullptr;
+            unsigned long long* tr = nullptr;
+            const int nblk = batch * lay.heads;
+            if (atrace && l == 0) {
+                GFX_CUDA(cudaMalloc(&tr, sizeof(unsigned long long) * 8 * nblk));
+                GFX_CUDA(cudaMemset(tr, 0, sizeof(unsigned long long) * 8 * nblk));
+                GFX_CUDA(cudaStreamSynchronize(s));
+            }
+            launch_pdl(attention_tc_kernel, dim3(nblk), dim3(128), kAttnSmem, s, true, tq, ws.ctx, lay.heads, tr);
+            if (tr) {  // debug timeline: µs after the first CTA started, min / median / max over CTAs
+                std::vector<unsigned long long> hh(static_cast<size_t>(8) * nblk);
+                GFX_CUDA(cudaStreamSynchronize(s));
+                GFX_CUDA(cudaMemcpy(hh.data(), tr, hh.size() * 8, cudaMemcpyDeviceToHost));
+                GFX_CUDA(cudaFree(tr));
+                unsigned long long t0 = ~0ull;
+                for (int c = 0; c < nblk; ++c) t0 = std::min(t0, hh[c * 8]);
+                static const char* nm[7] = {"start", "setup", "QKV landed", "S ready", "P written", "O ready", "stored"};
+                for (int ph = 0; ph < 7; ++ph) {
+                    std::vector<double> v;
+                    for (int c = 0; c < nblk; ++c) v.push_back((hh[c * 8 + ph] - t0) * 1e-3);
+                    std::sort(v.begin(), v.end());
+                    std::fprintf(stderr, "[attn] %-12s %8.2f %8.2f %8.2f\n", nm[ph], v.front(), v[v.size() / 2], v.back());
+                }
+            }
+        }
         gemm<kEpiResid>(arena, pt, o.wo, o.bo, ws.ctx, ws.t, x, T, d, d, s, true);
         launch_pdl(layernorm_kernel<768>, dim3((T + 15) / 16), dim3(256), 0, s, true,
                    static_cast<const __nv_bfloat16*>(ws.t), ws.h, arena, pt, o.ln1_g, o.ln1_b, T);
