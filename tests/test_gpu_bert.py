@@ -1,6 +1,6 @@
 """C5 model family on B200: BERT-base encoder (bf16 activations, fp32
 accumulation, post-LN, tanh pooler) — tcgen05 GEMMs with fused bias / GELU /
-residual epilogues, mma.sync attention, LayerNorm — against the oracle's fp64
+residual epilogues, tcgen05 attention, LayerNorm — against the oracle's fp64
 restatement with the same bf16 rounding points. Tolerance (north star, bf16):
 normwise relative error <= 1e-3.
 
@@ -130,3 +130,16 @@ def test_bert_one_layer_end_to_end(gfx, olib):
                                  os.cpu_count() or 1) == 0
     assert np.isfinite(pooled).all()
     assert rel(pooled, want) <= TOL
+
+
+def test_bert_two_sm_gemm_variant():
+    """The opt-in 2-SM (cta_group::2) GEMM path (GFX_GEMM_PAIR=1, read once per
+    process) passes the same teacher-forced parity check in a fresh process."""
+    import subprocess
+    import sys
+    env = dict(os.environ, GFX_GEMM_PAIR="1")
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider",
+                        os.path.join(here, "test_gpu_bert.py") + "::test_bert_base_every_layer_teacher_forced"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
