@@ -49,7 +49,7 @@ __device__ __forceinline__ float gelu(float x) { return 0.5f * x * (1.0f + erff(
 // Persistent: one CTA per SM loops over 128 x kBN output tiles; the TMEM holds
 // two accumulators so the epilogue of tile i overlaps the MMAs of tile i+1.
 
-constexpr int kGM = 128, kGK = 64, kGThreads = 320;  // TMA, MMA, 8 epilogue warps
+constexpr int kGM = 128, kGK = 64, kGThreads = 384;  // A producer, MMA, 8 epilogue warps, 2 B producers
 constexpr uint32_t kGATile = 128 * 128;  // A: 128 rows x 64 bf16 (16 KB)
 constexpr uint32_t kGSmem = 192 * 1024;  // stage ring budget
 
@@ -125,7 +125,11 @@ __global__ void __launch_bounds__(kGThreads, 1)
     for (int i = tid; i < static_cast<int>(a.pt.n); i += kGThreads) pt[i] = a.pt.page[i];
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full_bar[s], 1);
+            // One arrive.expect_tx per producer warp: A (warp 0) and each B tile
+            // (warps 10, 11). TMA requests of one issuing thread are served one
+            // after another (~500 cycles per 16 KB, tools/tma_rate.cu), so the
+            // stage's three 16 KB loads come from three threads in parallel.
+            mbar_init(&full_bar[s], 1 + kBBytes / kGATile);
             mbar_init(&empty_bar[s], 1);
             mbar_init(&pair_full[s], 1);
         }
@@ -153,33 +157,32 @@ __global__ void __launch_bounds__(kGThreads, 1)
     const uint32_t tmem = tmem_s;
     if (tid == 0) mark(1);
 
-    if (warp == 0) {
-        if (lane == 0) {
-            // Producer: one continuous stage ring across this CTA's tiles.
+    constexpr int kBTiles = static_cast<int>(kBBytes / kGATile);  // B tiles per stage and CTA
+    if (warp == 0 || warp >= 10) {
+        // Producers: one continuous stage ring across this CTA's tiles. Warp 0
+        // loads A (X rows, 2-D tensor map, after the previous kernel: PDL);
+        // warp 10 + h loads B tile h (weights: pair -> this CTA's half of the
+        // kBN rows), independent of the previous kernel.
+        const int h = warp - 10;
+        if (lane == 0 && h < kBTiles) {
             int g = 0;
-            bool waited = false;
+            if (warp == 0) pdl_wait();
             for (int t = t_first; t < tiles; t += t_step) {
                 const int m0 = tile_m0(t), nb = t % n_tiles;
                 for (int k = 0; k < nk; ++k, ++g) {
                     const int s = g % kStages;
                     if (g >= kStages) mbar_wait(&empty_bar[s], ((g / kStages) & 1) ^ 1);
                     uint8_t* st = smem + static_cast<size_t>(s) * kStage;
-                    mbar_arrive_expect_tx(&full_bar[s], kStage);
-                    // Weights first (independent of the previous kernel); pair: this
-                    // CTA's half of the kBN rows (blob tiles of 128 rows).
-                    constexpr int kBTiles = static_cast<int>(kBBytes / kGATile);
-#pragma unroll
-                    for (int h = 0; h < kBTiles; ++h) {
+                    if (warp == 0) {
+                        mbar_arrive_expect_tx(&full_bar[s], kGATile);
+                        tma_tile2d_g2s(st, &tmap_x, k * kGK, m0, &full_bar[s]);
+                        smark(g, 0);
+                    } else {
                         const int bt = nb * (kBN / 128) + (kPair ? static_cast<int>(rank) * kBTiles : 0) + h;
                         const uint64_t v = a.w_off + (static_cast<uint64_t>(bt) * ktiles_row + k) * kGATile;
+                        mbar_arrive_expect_tx(&full_bar[s], kGATile);
                         tma_bulk_g2s(st + kGATile + h * kGATile, translate(a.arena, pt, v), kGATile, &full_bar[s]);
                     }
-                    if (!waited) {
-                        pdl_wait();
-                        waited = true;
-                    }
-                    tma_tile2d_g2s(st, &tmap_x, k * kGK, m0, &full_bar[s]);
-                    smark(g, 0);
                 }
             }
         }
