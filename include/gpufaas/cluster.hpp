@@ -195,6 +195,12 @@ public:
     bool held_elsewhere(int model, int gpu_id) const;
     void set_listener(ExecutionListener* listener) { listener_ = listener; }
     ExecutionListener* listener() const { return listener_; }
+    // Live (closed-loop) mode, run_live(): completions come from the device at
+    // real times, so complete() accepts any time and estimate_finish_time()
+    // treats a task running past its predicted end as finishing now. The
+    // default (replay) mode keeps the reference's exact checks.
+    void set_live(bool live) { live_ = live; }
+    bool live() const { return live_; }
 
 private:
     GpuState& gpu_mut(int gpu_id);
@@ -212,6 +218,7 @@ private:
     std::uint64_t tick_ = 0;
     ExecutionListener* listener_ = nullptr;
     std::vector<int> scratch_victims_;
+    bool live_ = false;
 };
 
 }  // namespace gpufaas

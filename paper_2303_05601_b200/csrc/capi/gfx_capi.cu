@@ -395,9 +395,47 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
                                      out_bytes, cudaMemcpyDeviceToHost, b.io_out));
             res.io_d2h_bytes += out_bytes;
         }
+        if (live_mode) {
+            // Live mode: the engine polls this to learn the request finished (output included).
+            cudaEvent_t e = req_timer.next();
+            GFX_CUDA(cudaEventRecord(e, args.host_io ? b.io_out : m.compute_stream()));
+            live_done[static_cast<size_t>(gpu)] = e;
+        }
     }
 
     void on_complete(int, int, gpufaas::SimTime) override {}
+
+    // Live closed-loop serving (gpufaas::run_live): completions are observed
+    // on the device instead of predicted.
+    struct LiveExec : gpufaas::LiveExecutor {
+        gfx_replay_s* r = nullptr;
+        bool done(int gpu) override {
+            cudaEvent_t e = r->live_done[static_cast<size_t>(gpu)];
+            if (!e) return true;
+            const cudaError_t q = cudaEventQuery(e);
+            if (q == cudaErrorNotReady) return false;
+            GFX_CUDA(q);
+            return true;
+        }
+    };
+    bool live_mode = false;
+    double live_scale = 0.0;
+    std::vector<cudaEvent_t> live_done;
+
+    void run_live(double time_scale, gfx_replay_result* out) {
+        if (args.only_gpu >= 0) throw std::invalid_argument("live mode runs every GPU in one process (only_gpu < 0)");
+        if (!(time_scale > 0)) throw std::invalid_argument("live mode needs a positive time_scale");
+        live_mode = true;
+        live_scale = time_scale;
+        live_done.assign(static_cast<size_t>(gpu_count()), nullptr);
+        try {
+            run(out);
+        } catch (...) {
+            live_mode = false;
+            throw;
+        }
+        live_mode = false;
+    }
 
     void run(gfx_replay_result* out) {
         res = gfx_replay_result{};
@@ -425,7 +463,14 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
         }
         gpufaas::SimConfig cfg = gpufaas::capi::to_sim_config(args.cfg);
         const auto s0 = std::chrono::steady_clock::now();
-        gpufaas::SimResult sim = gpufaas::run_stream(cfg, catalog, requests, nullptr, nullptr, this);
+        gpufaas::SimResult sim;
+        if (live_mode) {
+            LiveExec ex;
+            ex.r = this;
+            sim = gpufaas::run_live(cfg, catalog, requests, live_scale, this, ex);
+        } else {
+            sim = gpufaas::run_stream(cfg, catalog, requests, nullptr, nullptr, this);
+        }
         const auto s1 = std::chrono::steady_clock::now();
         for (int g = 0; g < G; ++g) {
             if (!mgrs[g]) continue;
@@ -746,6 +791,9 @@ int gfx_replay_create(const gfx_replay_args* args, gfx_replay_t* out) {
 }
 int gfx_replay_run(gfx_replay_t r, gfx_replay_result* out) {
     return guarded([&] { r->run(out); });
+}
+int gfx_replay_run_live(gfx_replay_t r, double time_scale, gfx_replay_result* out) {
+    return guarded([&] { r->run_live(time_scale, out); });
 }
 int gfx_replay_outputs(gfx_replay_t r, void* host, uint64_t bytes) {
     return guarded([&] {

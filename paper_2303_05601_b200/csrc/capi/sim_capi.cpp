@@ -124,6 +124,43 @@ void* gfx_sim_run_stream(const char* catalog_csv, const gfx_sim_config* c, int n
     }
 }
 
+// Live closed-loop mode on a timed stand-in device: each dispatched task
+// "runs" for its catalog duration / time_scale of real time. Exercises
+// run_live()'s real-time loop and live ClusterState without a GPU.
+void* gfx_sim_run_live_timed(const char* catalog_csv, const char* trace_csv, const gfx_sim_config* c,
+                             double time_scale) {
+    struct Timed : ExecutionListener, LiveExecutor {
+        using clock = std::chrono::steady_clock;
+        std::vector<clock::time_point> due;
+        double scale = 1;
+        void on_begin_execution(int gpu, const Request&, int, bool, const std::vector<int>&, int, SimTime now,
+                                SimTime completion_us) override {
+            due[static_cast<std::size_t>(gpu)] =
+                clock::now() + std::chrono::nanoseconds(static_cast<long long>((completion_us - now) * 1e3 / scale));
+        }
+        void on_complete(int, int, SimTime) override {}
+        bool done(int gpu) override { return clock::now() >= due[static_cast<std::size_t>(gpu)]; }
+    };
+    try {
+        std::istringstream in(catalog_csv);
+        const Catalog cat = parse_catalog_csv(in, "catalog");
+        std::vector<Request> reqs = gpufaas::capi::make_requests(*c, cat, trace_csv);
+        auto* h = new SimHandle();
+        for (const Request& r : reqs) h->model_idx.push_back(cat.index_of(r.model_id));
+        Timed dev;
+        dev.due.assign(static_cast<std::size_t>(std::max(c->gpu_count, 1)), std::chrono::steady_clock::now());
+        dev.scale = time_scale;
+        const auto t0 = std::chrono::steady_clock::now();
+        h->result = run_live(gpufaas::capi::to_sim_config(*c), cat, std::move(reqs), time_scale, &dev, dev);
+        h->run_ns = std::chrono::duration<double, std::nano>(std::chrono::steady_clock::now() - t0).count();
+        h->report_json = report_to_json(h->result.report).dump();
+        return h;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return nullptr;
+    }
+}
+
 int64_t gfx_sim_num_decisions(void* hp) { return static_cast<SimHandle*>(hp)->result.decisions.size(); }
 int64_t gfx_sim_num_requests(void* hp) { return static_cast<SimHandle*>(hp)->result.requests.size(); }
 double gfx_sim_run_ns(void* hp) { return static_cast<SimHandle*>(hp)->run_ns; }

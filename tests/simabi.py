@@ -236,6 +236,15 @@ class SimLib:
                              ar.ctypes.data_as(C.POINTER(C.c_int64)))
         return self._collect(h)
 
+    def run_live_timed(self, catalog_csv: str, cfg: SimConfig, time_scale: float,
+                       trace_csv: str | None = None) -> SimResult:
+        """Product only: run_live() against the timed stand-in device."""
+        f = getattr(self.lib, self.prefix + "run_live_timed")
+        f.restype = C.c_void_p
+        f.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(SimConfig), C.c_double]
+        h = f(catalog_csv.encode(), trace_csv.encode() if trace_csv else None, C.byref(cfg), time_scale)
+        return self._collect(h)
+
 
 def load_ref() -> SimLib:
     return SimLib(REF_SO, "ref_sim_")
