@@ -305,6 +305,7 @@ def main():
     extras = {}
     if rank == 0 and not a.no_extras:
         extras = locality_extras(gfx, world)
+        extras.update(c3c4_extras(gfx, world))
         extras.update(c5_extras(gfx, world, peaks, peak_kind))
     cpu = None
     if rank == 0 and not a.no_extras:
@@ -424,6 +425,56 @@ def locality_extras(gfx, world):
                      "(5-seed mean) are avg-latency speedups of LALB over LB")
     res["locality_vs_lb_12gpu_fleet_emulated"] = fleet
     return res
+
+
+def c3c4_extras(gfx, world):
+    """configs[2] (C3) and configs[3] (C4) with the fleet emulated on this one B200
+    (one GPU manager per simulated GPU, each with its own 128 MiB paged arena; a
+    peer fetch is a D2D copy standing in for NVLink). Schedules are bit-exact with
+    the reference (tests/test_control_plane.py::test_c3_c4_schedules)."""
+    if world > 1:
+        return {}
+    gfx.register_models(gfx.load_model_specs("mlp_c3"))
+    cat = gfx.catalog_text("mlp_c3")
+    c3 = {}
+    for pol in ("lb", "lalb", "lalbo3"):
+        rep = gfx.Replay(cat, gfx.c3_config(gpus=8, policy=pol), n_devices=1, use_p2p=True)
+        r = rep.run()
+        rep.close()
+        c3[pol] = {"sim_avg_latency_s": round(r.sim_avg_latency_s, 3), "sim_p50_s": round(r.sim_p50_s, 3),
+                   "sim_p99_s": round(r.sim_p99_s, 3), "hit_rate": round(r.hits / max(1, r.hits + r.misses), 4),
+                   "false_misses": int(r.false_misses), "p2p_loads": int(r.loads_p2p),
+                   "h2d_loads": int(r.loads_h2d), "replay_device_ms": round(r.device_ms, 1),
+                   "requests": int(r.n_requests)}
+    c3["speedup_avg_latency_lalb"] = round(c3["lb"]["sim_avg_latency_s"] / c3["lalb"]["sim_avg_latency_s"], 2)
+    c3["speedup_avg_latency_lalbo3"] = round(c3["lb"]["sim_avg_latency_s"] / c3["lalbo3"]["sim_avg_latency_s"], 2)
+    c3["note"] = ("8 GPUs x 128 MiB (1 GiB aggregate) < 1294 MB of weights, 20 MLPs 25-100 MB, ws 20, "
+                  f"{gfx.c3_rpm(8)} rpm x 6 min (rho_infer 0.59), Table-I times; managers emulated on one B200")
+    c4 = {}
+    for zipf in (0.7063, 1.0, 1.2):
+        for G in (2, 4, 8):
+            row = {}
+            for p2p in (True, False):
+                rep = gfx.Replay(cat, gfx.c3_config(gpus=G, policy="lalbo3", zipf=zipf), n_devices=1, use_p2p=p2p)
+                rep.run()
+                r = rep.run()
+                rep.close()
+                row[p2p] = r
+            a, b = row[True], row[False]
+            # Pinned-host time of exactly the loads P2P replaced, at the measured link peak
+            # (summed per-load event times overlap across the emulated managers, so they do not subtract).
+            reload_ms = a.p2p_bytes / (H2D_PEAK_GBS * 1e6)
+            c4[f"zipf{zipf}_g{G}"] = {
+                "misses": int(a.misses), "false_misses": int(a.false_misses), "p2p_loads": int(a.loads_p2p),
+                "p2p_bytes": int(a.p2p_bytes), "p2p_ms": round(a.p2p_ms, 3),
+                "reload_ms_at_h2d_peak": round(reload_ms, 3),
+                "p2p_gbs_emulated": round(a.p2p_bytes / (a.p2p_ms * 1e6), 1) if a.p2p_ms else None,
+                "replay_ms_p2p": round(a.device_ms, 1), "replay_ms_reload": round(b.device_ms, 1),
+                "replay_speedup": round(b.device_ms / a.device_ms, 3),
+                "same_schedule": int(a.decision_digest) == int(b.decision_digest)}
+    c4["note"] = ("same lalbo3 decision stream replayed with false misses as peer fetches vs pinned-host reloads; "
+                  "peer fetch here = D2D on one B200 (real NVLink 5 peer rate is bounded by p2p_peak_gbs)")
+    return {"c3_fleet_emulated": c3, "c4_p2p_vs_reload_emulated": c4}
 
 
 def c5_extras(gfx, world, peaks, peak_kind):

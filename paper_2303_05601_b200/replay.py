@@ -33,6 +33,23 @@ def sim_config(gpus=1, capacity_mb=204.0, policy="lalbo3", o3_limit=25, working_
     return c
 
 
+C3_ARENA_MB = 128.0  # per GPU: 8 x 128 MiB < 1294 MB of C3 weights (working set > aggregate cache)
+
+
+def c3_rpm(gpus: int, mean_infer_s: float = 1.315, rho: float = 0.59) -> int:
+    """Request rate putting the fleet at rho_infer = rpm/60 * mean(infer)/G (the
+    reference regime, Appendix B.5). 1.315 s = mean infer_time_s of the mlp_c3 catalog."""
+    return int(round(rho * 60.0 * gpus / mean_infer_s))
+
+
+def c3_config(gpus=8, policy="lalbo3", zipf=0.7063, seed=1, o3_limit=25) -> _ffi.SimConfig:
+    """configs[2] (C3) / configs[3] (C4, zipf in {0.7063, 1.0, 1.2}, G in {2, 4, 8}): the
+    mlp_c3 catalog (20 models, 25-100 MB), working set 20, 6 minutes, synthetic
+    Azure-shaped trace (60 functions, 3000 draws/min, seed 91) at the given Zipf exponent."""
+    return sim_config(gpus=gpus, capacity_mb=C3_ARENA_MB, policy=policy, o3_limit=o3_limit, working_set=20,
+                      rpm=c3_rpm(gpus), minutes=6, seed=seed, syn_zipf=zipf)
+
+
 @dataclass
 class ReplayResult:
     raw: dict

@@ -128,3 +128,27 @@ def test_live_closed_loop_on_timed_device(product, table1, policy):
     hits_live = live.report["hits"] / n
     hits_virt = virt.report["hits"] / n
     assert abs(hits_live - hits_virt) < 0.15, (hits_live, hits_virt)
+
+
+@pytest.mark.parametrize("gpus", [2, 4, 8])
+@pytest.mark.parametrize("zipf", [0.7063, 1.0, 1.2])
+def test_c3_c4_schedules(product, oracle, gpus, zipf):
+    """configs[2] (C3: 8 GPUs, 20 models of 25-100 MB, working set > aggregate
+    cache) and configs[3] (C4: Zipf 0.7063/1.0/1.2 at 2/4/8 GPUs): the product's
+    schedule is bit-exact with the oracle and, where it is built here, with the
+    compiled reference; locality-aware beats load balancing on average latency."""
+    import paper_2303_05601_b200 as gfx
+    cat = gfx.catalog_text("mlp_c3")
+    ref = simabi.load_ref() if os.path.exists(simabi.REF_SO) else None
+    lat = {}
+    for pol in ("lb", "lalb", "lalbo3"):
+        cfg = simabi.make_config(gpus=gpus, capacity_mb=gfx.C3_ARENA_MB, policy=pol, working_set=20,
+                                 rpm=gfx.c3_rpm(gpus), minutes=6, syn_zipf=zipf, log_events=2)
+        b = product.run(cat, cfg)
+        simabi.assert_same(oracle.run(cat, cfg), b, f"oracle {gpus} {zipf} {pol}")
+        if ref is not None:
+            r = ref.run(cat, cfg)
+            simabi.assert_same(r, b, f"reference {gpus} {zipf} {pol}")
+            assert r.log_digest == b.log_digest
+        lat[pol] = b.report["avg_latency_s"]
+    assert lat["lalbo3"] < lat["lalb"] < lat["lb"]

@@ -46,9 +46,33 @@ def main():
     ap.add_argument("--name", default="mlp_c2")
     ap.add_argument("--paper-times", action="store_true",
                     help="keep Table-I load/infer seconds (the paper's regime) instead of B200 times")
+    ap.add_argument("--c3", action="store_true",
+                    help="configs[2]/[3] (C3/C4) catalog: 20 models of 25-100 MB evenly spaced, Table-I times "
+                         "interpolated at size x scale (the paper regime), ids c3-00..c3-19")
     a = ap.parse_args()
     prof = json.load(open(a.profile)) if a.profile else {}
     rows = list(csv.DictReader(open(a.table1)))
+    if a.c3:
+        t1 = sorted(rows, key=lambda r: float(r["occupation_mb"]))
+        occ = [float(r["occupation_mb"]) / a.scale for r in t1]
+
+        def interp(x, key):
+            ys = [float(r[key]) for r in t1]
+            if x <= occ[0]:
+                return ys[0]
+            for i in range(1, len(occ)):
+                if x <= occ[i]:
+                    f = (x - occ[i - 1]) / max(occ[i] - occ[i - 1], 1e-9)
+                    return ys[i - 1] + f * (ys[i] - ys[i - 1])
+            return ys[-1]
+        rows = []
+        for j in range(20):
+            mb = 25.0 + 75.0 * j / 19
+            rows.append({"model_id": f"c3-{j:02d}", "occupation_mb": mb * a.scale,
+                         "load_time_s": round(interp(mb, "load_time_s"), 2),
+                         "infer_time_s": round(interp(mb, "infer_time_s"), 2)})
+        a.paper_times = True
+        a.name = "mlp_c3"
     cat, spec = [], []
     for r in rows:
         target = float(r["occupation_mb"]) / a.scale * (1 << 20)
