@@ -390,17 +390,39 @@ def locality_extras(gfx, world):
     rate = 0.9 * out["lb"]["replay_req_s"]
     scale = rate * 360.0 / n
     live = {"offered_req_s": round(rate, 1), "time_scale": round(scale, 3)}
-    for pol in ("lb", "lalbo3"):
+    for pol, ema in (("lb", 0.0), ("lalbo3", 0.0), ("lalbo3", 0.3)):
         rep = gfx.Replay(cat, gfx.sim_config(gpus=1, capacity_mb=204.0, policy=pol), record_kernels=False)
         rep.run()
-        lr = rep.run_live(scale)
+        lr = rep.run_live(scale, ema)
         rep.close()
-        live[pol] = {"avg_latency_ms": round(lr.sim_avg_latency_s * 1e3, 3), "p50_ms": round(lr.sim_p50_s * 1e3, 3),
-                     "p99_ms": round(lr.sim_p99_s * 1e3, 3), "hit_rate": round(lr.hits / (lr.hits + lr.misses), 4),
-                     "wall_ms": round(lr.host_ms, 1)}
+        live[pol + ("_ema" if ema else "")] = {
+            "avg_latency_ms": round(lr.sim_avg_latency_s * 1e3, 3), "p50_ms": round(lr.sim_p50_s * 1e3, 3),
+            "p99_ms": round(lr.sim_p99_s * 1e3, 3), "hit_rate": round(lr.hits / (lr.hits + lr.misses), 4),
+            "wall_ms": round(lr.host_ms, 1)}
     live["speedup_avg_latency"] = round(live["lb"]["avg_latency_ms"] / live["lalbo3"]["avg_latency_ms"], 3)
     live["note"] = ("gfx_replay_run_live: arrivals / time_scale released in real time, completions observed "
-                    "on the device; real arrival->completion latencies")
+                    "on the device; real arrival->completion latencies; _ema: planned load/infer times follow "
+                    "the event-measured device durations (alpha 0.3)")
+    # 3-GPU fleet emulated on this B200 (3 managers): LALB's wait-vs-load rule and peer
+    # fetches in play, with catalog vs device-measured planned times.
+    fl = {}
+    cfg3 = {pol: gfx.sim_config(gpus=3, capacity_mb=204.0, policy=pol) for pol in ("lb", "lalb", "lalbo3")}
+    rep = gfx.Replay(cat, cfg3["lb"], n_devices=1, use_p2p=True, record_kernels=False)
+    base = rep.run()
+    rep.close()
+    scale3 = 0.9 * int(base.n_requests) / (base.device_ms / 1e3) * 360.0 / int(base.n_requests)
+    fl["offered_req_s"] = round(0.9 * int(base.n_requests) / (base.device_ms / 1e3), 1)
+    for pol in ("lb", "lalb", "lalbo3"):
+        for ema in (0.0, 0.3):
+            rep = gfx.Replay(cat, cfg3[pol], n_devices=1, use_p2p=True, record_kernels=False)
+            rep.run()
+            lr = rep.run_live(scale3, ema)
+            rep.close()
+            fl[pol + ("_ema" if ema else "")] = {
+                "avg_latency_ms": round(lr.sim_avg_latency_s * 1e3, 3), "p99_ms": round(lr.sim_p99_s * 1e3, 3),
+                "hit_rate": round(lr.hits / (lr.hits + lr.misses), 4), "local_enqueues": int(lr.local_enqueues),
+                "false_misses": int(lr.false_misses)}
+    live["fleet3_emulated"] = fl
     res["live_closed_loop_1gpu_paper_regime"] = live
     # The reference's default fleet (12 GPUs x 8192 MB, Table-I times, ws 15, 325 rpm,
     # proj/test_output.txt:9-10: LB 118.02 s -> LALB 1.770 s avg latency) with the

@@ -72,9 +72,10 @@ void* gfx_sim_run_stream(const char* catalog_csv, const gfx_sim_config* cfg, int
                          const int32_t* model_idx, const int64_t* arrival_us);
 /* Extension: run_live() (see gfx_replay_run_live) against a
  * timed stand-in device on which every task takes its catalog duration /
- * time_scale of real time. Request times are real microseconds. */
+ * time_scale of real time and reports those durations as measured (for
+ * ema_alpha > 0). Request times are real microseconds. */
 void* gfx_sim_run_live_timed(const char* catalog_csv, const char* trace_csv, const gfx_sim_config* cfg,
-                             double time_scale);
+                             double time_scale, double ema_alpha);
 int64_t gfx_sim_num_decisions(void* h);
 int64_t gfx_sim_num_requests(void* h);
 double gfx_sim_run_ns(void* h);
@@ -214,9 +215,11 @@ int gfx_replay_run(gfx_replay_t r, gfx_replay_result* out);
  * its inference) and triggers the scheduler, so the schedule follows the
  * device, not the catalog's predicted times. sim_p50_s / sim_p99_s /
  * sim_avg_latency_s then hold REAL request latencies (seconds, arrival to
- * observed completion) and decision_digest is not reproducible. Needs every GPU
- * in this process (only_gpu < 0). */
-int gfx_replay_run_live(gfx_replay_t r, double time_scale, gfx_replay_result* out);
+ * observed completion) and decision_digest is not reproducible. ema_alpha > 0:
+ * each model's planned load/infer times follow the event-measured device
+ * durations (exponential moving average; 0 keeps the catalog's). Needs every
+ * GPU in this process (only_gpu < 0). */
+int gfx_replay_run_live(gfx_replay_t r, double time_scale, double ema_alpha, gfx_replay_result* out);
 /* Per-request outputs of the last run (keep_outputs): [n_requests][out_bytes]. */
 int gfx_replay_outputs(gfx_replay_t r, void* host, uint64_t bytes);
 /* Per-request model row and device service time (ms) of the last run. */

@@ -97,7 +97,8 @@ gfx_input_seed = _sig("gfx_input_seed", C.c_uint64, [C.c_int])
 gfx_host_fill_params = _sig("gfx_host_fill_params", C.c_int, [_vp, C.c_uint64, C.c_uint64, C.c_uint32, C.c_float])
 gfx_replay_create = _sig("gfx_replay_create", C.c_int, [C.POINTER(ReplayArgs), C.POINTER(_vp)])
 gfx_replay_run = _sig("gfx_replay_run", C.c_int, [_vp, C.POINTER(ReplayResultC)])
-gfx_replay_run_live = _sig("gfx_replay_run_live", C.c_int, [_vp, C.c_double, C.POINTER(ReplayResultC)])
+gfx_replay_run_live = _sig("gfx_replay_run_live", C.c_int, [_vp, C.c_double, C.c_double,
+                                                             C.POINTER(ReplayResultC)])
 gfx_replay_outputs = _sig("gfx_replay_outputs", C.c_int, [_vp, _vp, C.c_uint64])
 gfx_replay_requests = _sig("gfx_replay_requests", C.c_int, [_vp, _vp, _vp, C.c_int64])
 gfx_replay_destroy = _sig("gfx_replay_destroy", C.c_int, [_vp])

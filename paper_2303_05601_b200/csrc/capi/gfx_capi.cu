@@ -328,8 +328,14 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
             e0 = req_timer.next();
             req_start[rid] = e0;
         }
+        LiveTask* lt = live_mode ? &live_task[static_cast<size_t>(gpu)] : nullptr;
+        if (lt) *lt = LiveTask{};
         if (!hit) {
             if (e0) GFX_CUDA(cudaEventRecord(e0, m.copy_stream()));
+            if (lt) {
+                lt->ls = req_timer.next();
+                GFX_CUDA(cudaEventRecord(lt->ls, m.copy_stream()));
+            }
             for (int v : evicted) {
                 if (ipc) wait_peer_reads(m, v);
                 m.evict(v);
@@ -364,6 +370,10 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
                 for (int r = 0; r < gpu_count(); ++r)
                     if (r != gpu) m.copy_write(remotes[static_cast<size_t>(r)].flags + fl_loaded(gpu, model),
                                                load_cnt[fl_loaded(gpu, model)]);
+            if (lt) {
+                lt->le = req_timer.next();
+                GFX_CUDA(cudaEventRecord(lt->le, m.copy_stream()));
+            }
         } else if (e0) {
             GFX_CUDA(cudaEventRecord(e0, m.compute_stream()));
         }
@@ -378,7 +388,16 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
             GFX_CUDA(cudaStreamWaitEvent(m.compute_stream(), ein, 0));
             res.io_h2d_bytes += in_bytes;
         }
+        if (lt) {
+            if (lt->le) GFX_CUDA(cudaStreamWaitEvent(m.compute_stream(), lt->le, 0));
+            lt->is = req_timer.next();
+            GFX_CUDA(cudaEventRecord(lt->is, m.compute_stream()));
+        }
         m.infer(model, in, out);
+        if (lt) {
+            lt->ie = req_timer.next();
+            GFX_CUDA(cudaEventRecord(lt->ie, m.compute_stream()));
+        }
         const gfx::ModelBlob& blob = ModelStore::get().at(model);
         res.mlp_flops += blob.flops;
         res.mlp_weight_bytes += blob.alg_bytes;
@@ -407,6 +426,11 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
 
     // Live closed-loop serving (gpufaas::run_live): completions are observed
     // on the device instead of predicted.
+    // Per GPU, the running task's load (copy stream) and inference (compute
+    // stream) events; measured() reports them to the engine's EMA.
+    struct LiveTask {
+        cudaEvent_t ls = nullptr, le = nullptr, is = nullptr, ie = nullptr;
+    };
     struct LiveExec : gpufaas::LiveExecutor {
         gfx_replay_s* r = nullptr;
         bool done(int gpu) override {
@@ -417,17 +441,27 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
             GFX_CUDA(q);
             return true;
         }
+        bool measured(int gpu, gpufaas::SimTime* load_us, gpufaas::SimTime* infer_us) override {
+            const LiveTask& t = r->live_task[static_cast<size_t>(gpu)];
+            if (!t.is) return false;
+            *load_us = t.ls ? std::max<gpufaas::SimTime>(1, std::llround(elapsed_ms(t.ls, t.le) * 1e3)) : 0;
+            *infer_us = std::max<gpufaas::SimTime>(1, std::llround(elapsed_ms(t.is, t.ie) * 1e3));
+            return true;
+        }
     };
     bool live_mode = false;
-    double live_scale = 0.0;
+    double live_scale = 0.0, live_alpha = 0.0;
     std::vector<cudaEvent_t> live_done;
+    std::vector<LiveTask> live_task;
 
-    void run_live(double time_scale, gfx_replay_result* out) {
+    void run_live(double time_scale, double ema_alpha, gfx_replay_result* out) {
         if (args.only_gpu >= 0) throw std::invalid_argument("live mode runs every GPU in one process (only_gpu < 0)");
         if (!(time_scale > 0)) throw std::invalid_argument("live mode needs a positive time_scale");
         live_mode = true;
         live_scale = time_scale;
+        live_alpha = ema_alpha;
         live_done.assign(static_cast<size_t>(gpu_count()), nullptr);
+        live_task.assign(static_cast<size_t>(gpu_count()), LiveTask{});
         try {
             run(out);
         } catch (...) {
@@ -467,7 +501,7 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
         if (live_mode) {
             LiveExec ex;
             ex.r = this;
-            sim = gpufaas::run_live(cfg, catalog, requests, live_scale, this, ex);
+            sim = gpufaas::run_live(cfg, catalog, requests, live_scale, this, ex, nullptr, live_alpha);
         } else {
             sim = gpufaas::run_stream(cfg, catalog, requests, nullptr, nullptr, this);
         }
@@ -792,8 +826,8 @@ int gfx_replay_create(const gfx_replay_args* args, gfx_replay_t* out) {
 int gfx_replay_run(gfx_replay_t r, gfx_replay_result* out) {
     return guarded([&] { r->run(out); });
 }
-int gfx_replay_run_live(gfx_replay_t r, double time_scale, gfx_replay_result* out) {
-    return guarded([&] { r->run_live(time_scale, out); });
+int gfx_replay_run_live(gfx_replay_t r, double time_scale, double ema_alpha, gfx_replay_result* out) {
+    return guarded([&] { r->run_live(time_scale, ema_alpha, out); });
 }
 int gfx_replay_outputs(gfx_replay_t r, void* host, uint64_t bytes) {
     return guarded([&] {

@@ -128,18 +128,28 @@ void* gfx_sim_run_stream(const char* catalog_csv, const gfx_sim_config* c, int n
 // "runs" for its catalog duration / time_scale of real time. Exercises
 // run_live()'s real-time loop and live ClusterState without a GPU.
 void* gfx_sim_run_live_timed(const char* catalog_csv, const char* trace_csv, const gfx_sim_config* c,
-                             double time_scale) {
+                             double time_scale, double ema_alpha) {
     struct Timed : ExecutionListener, LiveExecutor {
         using clock = std::chrono::steady_clock;
+        const Catalog* cat = nullptr;
         std::vector<clock::time_point> due;
+        std::vector<SimTime> load, infer;  // per GPU: the running task's device durations
         double scale = 1;
-        void on_begin_execution(int gpu, const Request&, int, bool, const std::vector<int>&, int, SimTime now,
-                                SimTime completion_us) override {
-            due[static_cast<std::size_t>(gpu)] =
-                clock::now() + std::chrono::nanoseconds(static_cast<long long>((completion_us - now) * 1e3 / scale));
+        void on_begin_execution(int gpu, const Request& r, int, bool hit, const std::vector<int>&, int, SimTime,
+                                SimTime) override {
+            const ModelProfile& p = cat->lookup(r.model_id);
+            const std::size_t g = static_cast<std::size_t>(gpu);
+            load[g] = hit ? 0 : std::max<SimTime>(1, std::llround(p.load_time_us / scale));
+            infer[g] = std::max<SimTime>(1, std::llround(p.infer_time_us / scale));
+            due[g] = clock::now() + std::chrono::microseconds(load[g] + infer[g]);
         }
         void on_complete(int, int, SimTime) override {}
         bool done(int gpu) override { return clock::now() >= due[static_cast<std::size_t>(gpu)]; }
+        bool measured(int gpu, SimTime* l, SimTime* i) override {
+            *l = load[static_cast<std::size_t>(gpu)];
+            *i = infer[static_cast<std::size_t>(gpu)];
+            return true;
+        }
     };
     try {
         std::istringstream in(catalog_csv);
@@ -148,10 +158,15 @@ void* gfx_sim_run_live_timed(const char* catalog_csv, const char* trace_csv, con
         auto* h = new SimHandle();
         for (const Request& r : reqs) h->model_idx.push_back(cat.index_of(r.model_id));
         Timed dev;
-        dev.due.assign(static_cast<std::size_t>(std::max(c->gpu_count, 1)), std::chrono::steady_clock::now());
+        const std::size_t G = static_cast<std::size_t>(std::max(c->gpu_count, 1));
+        dev.cat = &cat;
+        dev.due.assign(G, std::chrono::steady_clock::now());
+        dev.load.assign(G, 0);
+        dev.infer.assign(G, 0);
         dev.scale = time_scale;
         const auto t0 = std::chrono::steady_clock::now();
-        h->result = run_live(gpufaas::capi::to_sim_config(*c), cat, std::move(reqs), time_scale, &dev, dev);
+        h->result = run_live(gpufaas::capi::to_sim_config(*c), cat, std::move(reqs), time_scale, &dev, dev, nullptr,
+                             ema_alpha);
         h->run_ns = std::chrono::duration<double, std::nano>(std::chrono::steady_clock::now() - t0).count();
         h->report_json = report_to_json(h->result.report).dump();
         return h;

@@ -94,14 +94,15 @@ class Replay:
         _ffi.check(_ffi.gfx_replay_run(self.h, C.byref(r)))
         return ReplayResult({k: getattr(r, k) for k, _ in r._fields_})
 
-    def run_live(self, time_scale: float) -> ReplayResult:
+    def run_live(self, time_scale: float, ema_alpha: float = 0.0) -> ReplayResult:
         """Live closed-loop serving of the same trace (extension):
         arrivals compressed by ``time_scale`` and released in real time, every
-        completion observed on the device and fed back to the scheduler. The
-        sim_* latency fields hold real seconds; the schedule is not
-        reproducible run to run (it follows the device)."""
+        completion observed on the device and fed back to the scheduler; with
+        ``ema_alpha`` > 0 the planned load/infer times follow the event-measured
+        device durations. The sim_* latency fields hold real seconds; the
+        schedule is not reproducible run to run (it follows the device)."""
         r = _ffi.ReplayResultC()
-        _ffi.check(_ffi.gfx_replay_run_live(self.h, float(time_scale), C.byref(r)))
+        _ffi.check(_ffi.gfx_replay_run_live(self.h, float(time_scale), float(ema_alpha), C.byref(r)))
         return ReplayResult({k: getattr(r, k) for k, _ in r._fields_})
 
     def outputs(self, n_requests: int, shape=(2, 32, 1000)) -> np.ndarray:

@@ -236,13 +236,13 @@ class SimLib:
                              ar.ctypes.data_as(C.POINTER(C.c_int64)))
         return self._collect(h)
 
-    def run_live_timed(self, catalog_csv: str, cfg: SimConfig, time_scale: float,
+    def run_live_timed(self, catalog_csv: str, cfg: SimConfig, time_scale: float, ema_alpha: float = 0.0,
                        trace_csv: str | None = None) -> SimResult:
         """Product only: run_live() against the timed stand-in device."""
         f = getattr(self.lib, self.prefix + "run_live_timed")
         f.restype = C.c_void_p
-        f.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(SimConfig), C.c_double]
-        h = f(catalog_csv.encode(), trace_csv.encode() if trace_csv else None, C.byref(cfg), time_scale)
+        f.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(SimConfig), C.c_double, C.c_double]
+        h = f(catalog_csv.encode(), trace_csv.encode() if trace_csv else None, C.byref(cfg), time_scale, ema_alpha)
         return self._collect(h)
 
 

@@ -104,16 +104,19 @@ def test_reference_acceptance_suite_on_product():
     assert "98280 enumerated instances" in prod.stdout and "0 decision mismatches" in prod.stdout
 
 
+@pytest.mark.parametrize("ema", [0.0, 0.5])
 @pytest.mark.parametrize("policy", ["lb", "lalbo3"])
-def test_live_closed_loop_on_timed_device(product, table1, policy):
+def test_live_closed_loop_on_timed_device(product, table1, policy, ema):
     """Extension: run_live() — arrivals released in real time,
     completions observed from a stand-in device that runs each task for its
-    catalog duration / time_scale. Not bit-exact by design; checks that every
+    catalog duration / time_scale (and, with ema > 0, reports those durations
+    so the planned times follow it). Not bit-exact by design; checks that every
     request is served exactly once, never before its service time could have
-    elapsed, with a hit ratio close to the virtual-time schedule's."""
+    elapsed, with a hit ratio close to the virtual-time schedule's (the device
+    is the catalog, uniformly scaled)."""
     scale = 400.0
     cfg = simabi.make_config(gpus=4, policy=policy, minutes=1, debug_checks=True)
-    live = product.run_live_timed(table1, cfg, scale)
+    live = product.run_live_timed(table1, cfg, scale, ema)
     virt = product.run(table1, cfg)
     n = len(virt.arrival)
     assert len(live.arrival) == n
@@ -122,9 +125,13 @@ def test_live_closed_loop_on_timed_device(product, table1, policy):
     assert sorted(dispatched.tolist()) == list(range(n)), "each request dispatched exactly once"
     assert np.array_equal(live.arrival, np.floor(virt.arrival / scale + 0.5).astype(np.int64))
     assert (live.dispatched >= live.arrival).all() and (live.completed >= live.dispatched).all()
-    infer_us = live.times[kinds != 2, 2]
-    done_after = live.completed[dispatched] - live.dispatched[dispatched]
-    assert (done_after + 2 >= infer_us / scale).all(), "completion observed before the task could finish"
+    if ema == 0.0:  # planned times are the catalog's
+        infer_us = live.times[kinds != 2, 2]
+        done_after = live.completed[dispatched] - live.dispatched[dispatched]
+        assert (done_after + 2 >= infer_us / scale).all(), "completion observed before the task could finish"
+    else:  # planned times converge to the device's (catalog / scale)
+        last = live.times[kinds != 2][-50:, 2]
+        assert (last < 1.3e6 / scale * 1.5).all() and (last > 0).all()
     hits_live = live.report["hits"] / n
     hits_virt = virt.report["hits"] / n
     assert abs(hits_live - hits_virt) < 0.15, (hits_live, hits_virt)

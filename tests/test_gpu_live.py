@@ -18,8 +18,9 @@ def _digests(outs):
     return [hashlib.sha1(o.tobytes()).hexdigest() for o in outs]
 
 
-@pytest.mark.parametrize("gpus,policy", [(1, "lalbo3"), (3, "lb"), (3, "lalbo3")])
-def test_live_outputs_match_replay(gpus, policy):
+@pytest.mark.parametrize("gpus,policy,ema", [(1, "lalbo3", 0.0), (3, "lb", 0.0), (3, "lalbo3", 0.0),
+                                              (3, "lalbo3", 0.3)])
+def test_live_outputs_match_replay(gpus, policy, ema):
     import paper_2303_05601_b200 as gfx
     gfx.register_models(gfx.load_model_specs("mlp_c2"))
     cat = gfx.catalog_text("mlp_c2_paper")
@@ -32,7 +33,7 @@ def test_live_outputs_match_replay(gpus, policy):
     # Compress one minute of arrivals into ~2x the replay's device time: queues form but drain.
     scale = span_s / max(2 * base.device_ms / 1e3, 1e-3)
     for _ in range(2):
-        live = rep.run_live(scale)
+        live = rep.run_live(scale, ema)
         assert int(live.n_requests) == n
         assert int(live.hits + live.misses) == n
         got = _digests(rep.outputs(n))
