@@ -424,6 +424,28 @@ def locality_extras(gfx, world):
                 "false_misses": int(lr.false_misses)}
     live["fleet3_emulated"] = fl
     res["live_closed_loop_1gpu_paper_regime"] = live
+    # Pipelined GPUs (extension): a running GPU accepts one staged
+    # task whose load overlaps the running inference. Virtual-time latency of the
+    # oracle-checked schedule + the replay's device time, vs the reference semantics.
+    pipe = {}
+    for G in (1, 3):
+        for pol in ("lb", "lalbo3"):
+            row = {}
+            for on in (False, True):
+                rep = gfx.Replay(cat, gfx.sim_config(gpus=G, capacity_mb=204.0, policy=pol, pipeline=on),
+                                 n_devices=1, use_p2p=G > 1, record_kernels=False)
+                rep.run()
+                r = rep.run()
+                rep.close()
+                row["pipelined" if on else "reference"] = {
+                    "sim_avg_latency_s": round(r.sim_avg_latency_s, 3), "sim_p99_s": round(r.sim_p99_s, 3),
+                    "hit_rate": round(r.hits / max(1, r.hits + r.misses), 4), "replay_device_ms": round(r.device_ms, 1)}
+            row["speedup_avg_latency"] = round(row["reference"]["sim_avg_latency_s"] /
+                                               row["pipelined"]["sim_avg_latency_s"], 3)
+            pipe[f"g{G}_{pol}"] = row
+    pipe["note"] = ("mlp_c2_paper catalog (Table-I times), 325 rpm x 6 min; G > 1 = managers emulated on one B200; "
+                    "schedules bit-exact with the oracle's pipelined restatement (tests/test_control_plane.py)")
+    res["pipelined_gpus_paper_regime"] = pipe
     # The reference's default fleet (12 GPUs x 8192 MB, Table-I times, ws 15, 325 rpm,
     # proj/test_output.txt:9-10: LB 118.02 s -> LALB 1.770 s avg latency) with the
     # device work executed: 12 GPU managers (paged arenas scaled /40 like C2) emulated on

@@ -106,6 +106,19 @@ public:
     bool is_busy() const { return running_.has_value(); }
     SimTime busy_until_us() const;  // logic_error when idle
     const std::optional<RunningTask>& running() const { return running_; }
+    // Extension (pipelined GPUs, SchedulerConfig::pipeline): can a dispatch
+    // start here now? Reference mode: when idle. Pipelined: while nothing is
+    // staged behind the running task.
+    // A running GPU stages only while its unpinned memory could take any
+    // catalog model (so the staged load's victim selection cannot fail).
+    bool accepting() const {
+        if (!pipeline_) return !running_.has_value();
+        if (staged_) return false;
+        return !running_ || capacity_mb_ - pinned_mb() >= stage_headroom_mb_;
+    }
+    double pinned_mb() const;  // occupation of models with pins, summed MRU -> LRU
+    const std::optional<RunningTask>& staged() const { return staged_; }
+    SimTime staged_until_us() const { return staged_until_us_; }
 
     // Resident models, most recently used first.
     const std::list<CachedModel>& cache() const { return lru_; }
@@ -153,6 +166,12 @@ private:
     std::optional<RunningTask> running_;
     int running_model_ = -1;
     SimTime busy_until_us_ = 0;
+    std::optional<RunningTask> staged_;  // pipelined mode: next task, behind running_
+    int staged_model_ = -1;
+    SimTime staged_until_us_ = 0;
+    SimTime copy_free_us_ = 0;           // end of the last model load started here
+    bool pipeline_ = false;
+    double stage_headroom_mb_ = 0.0;     // largest catalog model
     int pinned_models_ = 0;         // models with pins > 0
     std::shared_ptr<ModelTable> table_;
 };
@@ -201,6 +220,9 @@ public:
     // default (replay) mode keeps the reference's exact checks.
     void set_live(bool live) { live_ = live; }
     bool live() const { return live_; }
+    // Pipelined GPUs (SchedulerConfig::pipeline); set before the first dispatch.
+    void set_pipeline(bool on, double stage_headroom_mb);
+    bool pipeline() const { return !gpus_.empty() && gpus_.front().pipeline_; }
 
 private:
     GpuState& gpu_mut(int gpu_id);

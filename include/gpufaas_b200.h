@@ -59,7 +59,7 @@ typedef struct {
     int32_t debug_checks;
     int32_t log_events; /* 0 none, 1 events, 2 events + cache contents */
     int32_t use_reference_scheduler; /* unused by the product */
-    int32_t pad_;
+    int32_t pipeline; /* extension: pipelined GPUs (SchedulerConfig::pipeline); 0 = reference semantics */
     double capacity_mb;
     double syn_zipf_exponent;
     uint64_t seed;

@@ -491,6 +491,10 @@ typedef struct {
     int64_t lq_infer_us;
     int running_req, running_model;  /* -1 idle */
     int64_t busy_until;
+    /* Extension (pipelined GPUs; product: SchedulerConfig::pipeline): one task
+     * staged behind the running one; copy_free = end of the last load here. */
+    int staged_req, staged_model;    /* -1 none */
+    int64_t staged_until, copy_free;
     int* pins;  /* per catalog model */
 } orc_gpu;
 
@@ -499,7 +503,22 @@ typedef struct {
     int n;
     uint64_t use_ticks;
     int nmodels;
+    int pipeline;
+    double headroom_mb;  /* largest catalog model */
 } orc_cluster;
+
+/* can a dispatch start on g now? reference: idle. Pipelined: nothing staged,
+ * and while running, unpinned memory for any catalog model (summed MRU -> LRU) */
+static int accepting(const orc_cluster* c, const orc_gpu* g) {
+    if (!c->pipeline) return g->running_req < 0;
+    if (g->staged_req >= 0) return 0;
+    if (g->running_req < 0) return 1;
+    double pinned = 0.0;
+    for (int i = 0; i < g->ncache; ++i)
+        if (g->pins[g->cache[i].model] > 0) pinned += g->cache[i].occupation_mb;
+    return g->capacity_mb - pinned >= c->headroom_mb;
+}
+static int64_t max64(int64_t a, int64_t b) { return a > b ? a : b; }
 
 static int gpu_find(const orc_gpu* g, int model) {
     for (int i = 0; i < g->ncache; ++i) if (g->cache[i].model == model) return i;
@@ -522,7 +541,7 @@ static int64_t estimate_finish(const orc_cluster* c, int gpu, int64_t now) {
     const orc_gpu* g = &c->g[gpu];
     int64_t rem = 0;
     if (g->running_req >= 0) {
-        rem = g->busy_until - now;
+        rem = (g->staged_req >= 0 ? g->staged_until : g->busy_until) - now;
         if (rem < 0) fail("cluster invariant violated: running task finished in the past");
     }
     return rem + g->lq_infer_us;
@@ -645,14 +664,15 @@ typedef struct {
 /* ClusterState::begin_execution: cluster.cpp:150-174; returns completion */
 static int64_t begin_execution(orc_ctx* x, int gpu, int request, int* hit, orc_decision* d) {
     orc_gpu* g = &x->cl->g[gpu];
-    if (g->running_req >= 0) { fail("cluster invariant violated: begin_execution on busy gpu %d", gpu); return 0; }
+    if (!accepting(x->cl, g)) { fail("cluster invariant violated: begin_execution on busy gpu %d", gpu); return 0; }
     int model = x->req[request].model;
     const orc_model* p = &x->cat->m[model];
     int64_t completion;
+    int behind = g->running_req >= 0;  /* pipelined: staged behind the running task */
     *hit = gpu_find(g, model) >= 0;
     if (*hit) {
         touch(x->cl, g, model);
-        completion = x->now + p->infer_us;
+        completion = (behind ? max64(x->now, g->busy_until) : x->now) + p->infer_us;
     } else {
         int* victims = xcalloc((size_t)g->ncache + 1, sizeof(int));
         int nv = select_victims(g, gpu, p->occupation_mb, victims);
@@ -662,11 +682,21 @@ static int64_t begin_execution(orc_ctx* x, int gpu, int request, int* hit, orc_d
         for (int i = 0; i < nv; ++i) { dl_push_ev(x->out, victims[i]); evict_one(g, victims[i]); }
         free(victims);
         insert_model(x->cl, g, model, p->occupation_mb);
-        completion = x->now + p->load_us + p->infer_us;
+        /* load on the copy engine once the previous load here is done; the
+         * inference once the load and the running task are */
+        int64_t load_end = (behind ? max64(x->now, g->copy_free) : x->now) + p->load_us;
+        g->copy_free = load_end;
+        completion = (behind ? max64(load_end, g->busy_until) : load_end) + p->infer_us;
     }
-    g->running_req = request;
-    g->running_model = model;
-    g->busy_until = completion;
+    if (behind) {
+        g->staged_req = request;
+        g->staged_model = model;
+        g->staged_until = completion;
+    } else {
+        g->running_req = request;
+        g->running_model = model;
+        g->busy_until = completion;
+    }
     g->pins[model] += 1;
     return completion;
 }
@@ -699,13 +729,16 @@ static int llb(orc_ctx* x, int gpu, int request) {
     int locs[1024];
     int nl = locations(x->cl, r->model, locs);
     if (nl == 0) { dispatch(x, gpu, request, 0); return 1; }
-    int best_idle = -1;
+    int best_idle = -1, best_running = 0;
     uint64_t best_tick = 0;
     for (int i = 0; i < nl; ++i) {
         const orc_gpu* g = &x->cl->g[locs[i]];
-        if (g->running_req >= 0) continue;
+        if (!accepting(x->cl, g)) continue;
         uint64_t tick = g->cache[gpu_find(g, r->model)].last_use_tick;
-        if (best_idle == -1 || tick > best_tick) { best_idle = locs[i]; best_tick = tick; }
+        int running = g->running_req >= 0;  /* pipelined: idle holders first */
+        if (best_idle == -1 || (running == best_running ? tick > best_tick : !running)) {
+            best_idle = locs[i]; best_tick = tick; best_running = running;
+        }
     }
     if (best_idle != -1) { dispatch(x, best_idle, request, 0); return best_idle == gpu; }
     int best_busy = -1;
@@ -798,7 +831,7 @@ static void on_scheduling_point(orc_ctx* x) {
     int64_t* hot = xcalloc((size_t)G, sizeof(int64_t));
     int ni = 0;
     for (int g = 0; g < G; ++g) {
-        if (x->cl->g[g].running_req >= 0) continue;
+        if (!accepting(x->cl, &x->cl->g[g])) continue;
         int64_t h = 0;
         for (int i = 0; i < x->cl->g[g].ncache; ++i) h += x->cl->g[g].cache[i].uses;
         if (h != x->cl->g[g].hotness) fail("oracle: hotness drift");
@@ -806,17 +839,23 @@ static void on_scheduling_point(orc_ctx* x) {
         hot[ni] = h;
         ni++;
     }
-    /* stable insertion sort: hotness desc, ties keep ascending id */
+    /* stable insertion sort: (pipelined: idle before running), hotness desc,
+     * ties keep ascending id */
     for (int i = 1; i < ni; ++i) {
         int gi = idle[i];
         int64_t hi = hot[i];
+        int ri = x->cl->g[gi].running_req >= 0;
         int j = i - 1;
-        while (j >= 0 && hot[j] < hi) { idle[j + 1] = idle[j]; hot[j + 1] = hot[j]; --j; }
+        while (j >= 0) {
+            int rj = x->cl->g[idle[j]].running_req >= 0;
+            if (!(rj > ri || (rj == ri && hot[j] < hi))) break;
+            idle[j + 1] = idle[j]; hot[j + 1] = hot[j]; --j;
+        }
         idle[j + 1] = gi;
         hot[j + 1] = hi;
     }
     for (int i = 0; i < ni && !g_failed; ++i) {
-        if (x->cl->g[idle[i]].running_req >= 0) continue;
+        if (!accepting(x->cl, &x->cl->g[idle[i]])) continue;
         schedule_idle_gpu(x, idle[i]);
     }
     free(idle);
@@ -952,11 +991,17 @@ static int run_stream(orc_handle* H, const orc_sim_config* c) {
     cl.n = c->gpu_count;
     cl.use_ticks = 0;
     cl.nmodels = cat->n;
+    cl.pipeline = c->pipeline != 0;
+    cl.headroom_mb = 0.0;
+    for (int m = 0; m < cat->n; ++m)
+        if (cat->m[m].occupation_mb > cl.headroom_mb) cl.headroom_mb = cat->m[m].occupation_mb;
     cl.g = xcalloc((size_t)cl.n, sizeof(orc_gpu));
     for (int g = 0; g < cl.n; ++g) {
         cl.g[g].capacity_mb = c->capacity_mb;
         cl.g[g].running_req = -1;
         cl.g[g].running_model = -1;
+        cl.g[g].staged_req = -1;
+        cl.g[g].staged_model = -1;
         cl.g[g].pins = xcalloc((size_t)cat->n, sizeof(int));
     }
     orc_queue q = {0};
@@ -988,6 +1033,14 @@ static int run_stream(orc_handle* H, const orc_sim_config* c) {
             g->running_req = -1;
             g->running_model = -1;
             g->busy_until = 0;
+            if (g->staged_req >= 0) {  /* pipelined: the staged task runs now */
+                g->running_req = g->staged_req;
+                g->running_model = g->staged_model;
+                g->busy_until = g->staged_until;
+                g->staged_req = -1;
+                g->staged_model = -1;
+                g->staged_until = 0;
+            }
             req[rid].completed_at_us = now;
             if (log) {
                 sb_str(&H->log, "{");
@@ -1036,7 +1089,7 @@ static int run_stream(orc_handle* H, const orc_sim_config* c) {
     int ok = !g_failed;
     if (ok && q.n) { fail("engine: requests still queued after the last event"); ok = 0; }
     for (int g = 0; ok && g < cl.n; ++g)
-        if (cl.g[g].running_req >= 0 || cl.g[g].nlq - cl.g[g].lq_head > 0) { fail("engine: cluster not drained"); ok = 0; }
+        if (cl.g[g].running_req >= 0 || cl.g[g].staged_req >= 0 || cl.g[g].nlq - cl.g[g].lq_head > 0) { fail("engine: cluster not drained"); ok = 0; }
     for (int i = 0; ok && i < n; ++i) {
         if (req[i].completed_at_us < 0) { fail("engine: request %d never completed", i); ok = 0; }
         if (req[i].skip_count > x.limit) { fail("engine: request %d bypassed too often", i); ok = 0; }

@@ -47,7 +47,7 @@ typedef struct {
     int32_t debug_checks;
     int32_t log_events; /* 0 none, 1 log, 2 log + caches */
     int32_t use_reference_scheduler; /* ignored: the oracle has one scheduler */
-    int32_t pad_;
+    int32_t pipeline; /* extension: pipelined GPUs (one staged task behind the running one); 0 = reference */
     double capacity_mb;
     double syn_zipf_exponent;
     uint64_t seed;

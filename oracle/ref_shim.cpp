@@ -16,6 +16,7 @@
 #include <cstring>
 #include <exception>
 #include <sstream>
+#include <stdexcept>
 #include <string>
 #include <vector>
 
@@ -42,7 +43,7 @@ struct SimCfg {  // identical layout in oracle/gpufaas_oracle.h and include/gpuf
     int32_t debug_checks;
     int32_t log_events;      // 0 none, 1 log, 2 log + caches
     int32_t use_reference_scheduler;  // plug tests/support ReferenceScheduler in
-    int32_t pad_;
+    int32_t pipeline;                 // product/oracle extension; the reference has no such mode
     double capacity_mb;
     double syn_zipf_exponent;
     uint64_t seed;
@@ -76,6 +77,7 @@ Policy to_policy(int p) {
 }
 
 SimConfig to_config(const SimCfg& c) {
+    if (c.pipeline) throw std::runtime_error("the reference has no pipelined-GPU mode");
     SimConfig cfg;
     cfg.gpu_count = c.gpu_count;
     cfg.capacity_mb = c.capacity_mb;

@@ -27,7 +27,7 @@ class SimConfig(C.Structure):
     _fields_ = [(n, C.c_int32) for n in (
         "gpu_count", "policy", "o3_limit", "working_set", "per_minute_total", "duration_minutes",
         "use_synthetic_trace", "syn_function_count", "syn_minutes", "syn_draws_per_minute",
-        "debug_checks", "log_events", "use_reference_scheduler", "pad_")] + [
+        "debug_checks", "log_events", "use_reference_scheduler", "pipeline")] + [
         ("capacity_mb", C.c_double), ("syn_zipf_exponent", C.c_double),
         ("seed", C.c_uint64), ("syn_seed", C.c_uint64)]
 

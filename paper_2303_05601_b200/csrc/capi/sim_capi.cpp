@@ -59,6 +59,7 @@ SimConfig to_sim_config(const gfx_sim_config& c) {
     cfg.synthetic.zipf_exponent = c.syn_zipf_exponent;
     cfg.synthetic.seed = c.syn_seed;
     cfg.debug_checks = c.debug_checks != 0;
+    cfg.scheduler.pipeline = c.pipeline != 0;
     return cfg;
 }
 

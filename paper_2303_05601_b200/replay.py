@@ -13,8 +13,10 @@ POLICIES = {"lb": 0, "lalb": 1, "lalbo3": 2}
 
 def sim_config(gpus=1, capacity_mb=204.0, policy="lalbo3", o3_limit=25, working_set=15, rpm=325,
                minutes=6, seed=1, syn_functions=60, syn_minutes=6, syn_draws=3000, syn_zipf=0.7063,
-               syn_seed=91) -> _ffi.SimConfig:
-    """Reference SimConfig (proj/include/gpufaas/engine.hpp:20-32) with the C2 arena."""
+               syn_seed=91, pipeline=False) -> _ffi.SimConfig:
+    """Reference SimConfig (proj/include/gpufaas/engine.hpp:20-32) with the C2 arena.
+    pipeline=True: the pipelined-GPU extension (SchedulerConfig::pipeline; not the
+    reference's semantics, checked against the oracle's restatement of it)."""
     c = _ffi.SimConfig()
     c.gpu_count = gpus
     c.policy = POLICIES[policy] if isinstance(policy, str) else int(policy)
@@ -30,6 +32,7 @@ def sim_config(gpus=1, capacity_mb=204.0, policy="lalbo3", o3_limit=25, working_
     c.syn_seed = syn_seed
     c.capacity_mb = capacity_mb
     c.seed = seed
+    c.pipeline = 1 if pipeline else 0
     return c
 
 

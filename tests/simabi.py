@@ -44,7 +44,7 @@ class SimConfig(C.Structure):
         ("debug_checks", C.c_int32),
         ("log_events", C.c_int32),
         ("use_reference_scheduler", C.c_int32),
-        ("pad_", C.c_int32),
+        ("pipeline", C.c_int32),
         ("capacity_mb", C.c_double),
         ("syn_zipf_exponent", C.c_double),
         ("seed", C.c_uint64),
@@ -55,7 +55,7 @@ class SimConfig(C.Structure):
 def make_config(gpus=12, capacity_mb=8192.0, policy="lalbo3", o3_limit=25, working_set=15,
                 rpm=325, minutes=6, seed=1, synthetic=True, syn_functions=60, syn_minutes=6,
                 syn_draws=3000, syn_zipf=0.7063, syn_seed=91, debug_checks=False, log_events=0,
-                reference_scheduler=False) -> SimConfig:
+                reference_scheduler=False, pipeline=False) -> SimConfig:
     """Defaults = the reference SimConfig defaults (proj/include/gpufaas/engine.hpp:20-32)."""
     c = SimConfig()
     c.gpu_count = gpus
@@ -73,6 +73,7 @@ def make_config(gpus=12, capacity_mb=8192.0, policy="lalbo3", o3_limit=25, worki
     c.debug_checks = 1 if debug_checks else 0
     c.log_events = log_events
     c.use_reference_scheduler = 1 if reference_scheduler else 0
+    c.pipeline = 1 if pipeline else 0
     c.capacity_mb = capacity_mb
     c.seed = seed
     return c

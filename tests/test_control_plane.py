@@ -159,3 +159,48 @@ def test_c3_c4_schedules(product, oracle, gpus, zipf):
             assert r.log_digest == b.log_digest
         lat[pol] = b.report["avg_latency_s"]
     assert lat["lalbo3"] < lat["lalb"] < lat["lb"]
+
+
+@pytest.mark.parametrize("policy", ["lb", "lalb", "lalbo3"])
+@pytest.mark.parametrize("case", ["table1-g12", "table1-g1", "c3-g8", "c3-g8-256", "c2paper-g3"])
+def test_pipelined_gpus_vs_oracle(product, oracle, table1, policy, case):
+    """Extension: pipelined GPUs — a running GPU accepts one
+    staged task whose load overlaps the running inference. The product matches
+    the oracle's independent C restatement decision for decision, event log
+    byte for byte; the reference itself has no such mode and refuses it."""
+    import paper_2303_05601_b200 as gfx
+    cat, kw = {
+        "table1-g12": (table1, dict(gpus=12)),
+        "table1-g1": (table1, dict(gpus=1)),
+        "c3-g8": (gfx.catalog_text("mlp_c3"), dict(gpus=8, capacity_mb=128.0, working_set=20, rpm=gfx.c3_rpm(8))),
+        "c3-g8-256": (gfx.catalog_text("mlp_c3"), dict(gpus=8, capacity_mb=256.0, working_set=20,
+                                                      rpm=gfx.c3_rpm(8))),
+        "c2paper-g3": (gfx.catalog_text("mlp_c2_paper"), dict(gpus=3, capacity_mb=204.0)),
+    }[case]
+    cfg = simabi.make_config(policy=policy, pipeline=True, debug_checks=True, log_events=2, **kw)
+    a, b = oracle.run(cat, cfg), product.run(cat, cfg)
+    simabi.assert_same(a, b, f"pipelined {case} {policy}")
+    assert a.log_digest == b.log_digest
+    ref_cfg = simabi.make_config(policy=policy, pipeline=False, **kw)
+    base = product.run(cat, ref_cfg)
+    assert base.decision_digest != b.decision_digest or case == "table1-g1"  # the mode changes the schedule
+    if os.path.exists(simabi.REF_SO):
+        with pytest.raises(simabi.SimError, match="pipelined"):
+            simabi.load_ref().run(cat, cfg)
+
+
+def test_pipelined_random_streams_vs_oracle(product, oracle):
+    """Random bursty streams over a tight cache, pipelined mode (staging
+    headroom, copy-engine ordering and promotion on completion)."""
+    cat = ("model_id,occupation_mb,load_time_s,infer_time_s\n"
+           "a,1000,1.1,0.6\nb,1600,1.7,0.4\nc,2200,2.3,0.9\nd,2600,2.9,0.5\n")
+    rng = np.random.default_rng(29)
+    for it in range(300):
+        n = int(rng.integers(1, 40))
+        arr = np.cumsum(rng.integers(0, 2_000_000, size=n))
+        mi = rng.integers(0, 4, size=n)
+        pol = ["lb", "lalb", "lalbo3"][it % 3]
+        cfg = simabi.make_config(gpus=int(rng.integers(1, 4)), capacity_mb=float(rng.choice([5000.0, 8000.0])),
+                                 policy=pol, o3_limit=int(rng.integers(0, 4)), debug_checks=True, pipeline=True)
+        a, b = oracle.run_stream(cat, cfg, mi, arr), product.run_stream(cat, cfg, mi, arr)
+        simabi.assert_same(a, b, f"iter {it}")

@@ -188,3 +188,24 @@ def test_host_io_replay_equals_device_resident(gfx):
     rep.close()
     assert r2.io_h2d_bytes == n * 32 * 1024 * 4 and r2.io_d2h_bytes == n * 2 * 32 * 1000 * 4
     assert np.array_equal(hout.reshape(dev_out.shape), dev_out)
+
+
+@pytest.mark.parametrize("policy,gpus", [("lb", 3), ("lalbo3", 3), ("lalbo3", 1)])
+def test_pipelined_replay(gfx, policy, gpus):
+    """Pipelined-GPU extension on the device: the replay follows the oracle's
+    pipelined schedule bit for bit (staged loads overlap the running inference
+    on the copy stream), and every request's output equals the reference-mode
+    replay's output for that request."""
+    cat = gfx.catalog_text("mlp_c2_paper")
+    outs, digests = {}, {}
+    for pipe in (False, True):
+        cfg = gfx.sim_config(gpus=gpus, capacity_mb=204.0, policy=policy, minutes=2, pipeline=pipe)
+        rep = gfx.Replay(cat, cfg, n_devices=1, use_p2p=gpus > 1, keep_outputs=True)
+        res = rep.run()
+        outs[pipe] = rep.outputs(int(res.n_requests))
+        digests[pipe] = int(res.decision_digest)
+        rep.close()
+    o = simabi.load_oracle().run(cat, simabi.make_config(gpus=gpus, capacity_mb=204.0, policy=policy, minutes=2,
+                                                         pipeline=True))
+    assert digests[True] == o.decision_digest
+    assert np.array_equal(outs[True], outs[False])
