@@ -76,6 +76,13 @@ void* gfx_sim_run_stream(const char* catalog_csv, const gfx_sim_config* cfg, int
  * ema_alpha > 0). Request times are real microseconds. */
 void* gfx_sim_run_live_timed(const char* catalog_csv, const char* trace_csv, const gfx_sim_config* cfg,
                              double time_scale, double ema_alpha);
+/* Extension: convert an Azure Functions 2019 invocation
+ * file ("HashOwner,HashApp,HashFunction,Trigger,1..1440") into the trace CSV
+ * ("function_id,m1..mN") of its top_k functions by invocations over the first
+ * max_minutes (0 = all), streaming (O(top_k x minutes) memory).
+ * Returns 0, or -1 with gfx_sim_last_error(). */
+int gfx_sim_azure_convert(const char* in_path, const char* out_path, int top_k, int max_minutes,
+                          int64_t* rows_read, int64_t* rows_kept);
 int64_t gfx_sim_num_decisions(void* h);
 int64_t gfx_sim_num_requests(void* h);
 double gfx_sim_run_ns(void* h);

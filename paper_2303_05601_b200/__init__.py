@@ -9,8 +9,9 @@ library raises.
 from ._ffi import lib, GfxError, check  # noqa: F401
 from .models import (ModelSpec, load_model_specs, register_models, model_seed, catalog_text,  # noqa: F401
                      DATA_DIR)
-from .replay import Replay, ReplayResult, sim_config, c3_config, c3_rpm, C3_ARENA_MB  # noqa: F401
+from .replay import (Replay, ReplayResult, sim_config, c3_config, c3_rpm, C3_ARENA_MB,  # noqa: F401
+                     azure_trace_to_csv)
 
 __all__ = ["lib", "GfxError", "ModelSpec", "load_model_specs", "register_models", "model_seed",
-           "catalog_text", "Replay", "ReplayResult", "sim_config", "c3_config", "c3_rpm", "C3_ARENA_MB",
+           "catalog_text", "Replay", "ReplayResult", "sim_config", "c3_config", "c3_rpm", "C3_ARENA_MB", "azure_trace_to_csv",
            "DATA_DIR"]

@@ -66,6 +66,9 @@ def _sig(name, res, args):
 
 _vp = C.c_void_p
 gfx_last_error = _sig("gfx_last_error", C.c_char_p, [])
+gfx_sim_last_error = _sig("gfx_sim_last_error", C.c_char_p, [])
+gfx_sim_azure_convert = _sig("gfx_sim_azure_convert", C.c_int, [C.c_char_p, C.c_char_p, C.c_int, C.c_int,
+                                                                C.POINTER(C.c_int64), C.POINTER(C.c_int64)])
 gfx_device_count = _sig("gfx_device_count", C.c_int, [C.POINTER(C.c_int)])
 gfx_device_init = _sig("gfx_device_init", C.c_int, [C.c_int, C.c_int])
 gfx_model_register = _sig("gfx_model_register", C.c_int, [C.c_int, C.POINTER(ModelDesc)])

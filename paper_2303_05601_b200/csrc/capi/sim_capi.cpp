@@ -5,6 +5,7 @@
 #include <chrono>
 #include <cstdint>
 #include <exception>
+#include <fstream>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -174,6 +175,25 @@ void* gfx_sim_run_live_timed(const char* catalog_csv, const char* trace_csv, con
     } catch (const std::exception& e) {
         g_err = e.what();
         return nullptr;
+    }
+}
+
+int gfx_sim_azure_convert(const char* in_path, const char* out_path, int top_k, int max_minutes,
+                          int64_t* rows_read, int64_t* rows_kept) {
+    try {
+        std::ifstream in(in_path);
+        if (!in) throw std::runtime_error(std::string("cannot open '") + in_path + "'");
+        AzureIngest opts;
+        opts.top_k = top_k;
+        opts.max_minutes = max_minutes;
+        const TraceMatrix t = parse_azure_trace_csv(in, in_path, opts);
+        save_trace(t, out_path);
+        if (rows_read) *rows_read = opts.rows_read;
+        if (rows_kept) *rows_kept = static_cast<int64_t>(t.functions.size());
+        return 0;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return -1;
     }
 }
 

@@ -36,6 +36,17 @@ def sim_config(gpus=1, capacity_mb=204.0, policy="lalbo3", o3_limit=25, working_
     return c
 
 
+def azure_trace_to_csv(in_path: str, out_path: str, top_k: int = 1000, max_minutes: int = 0) -> tuple[int, int]:
+    """Azure Functions 2019 invocation file -> trace CSV of its top_k functions
+    (extension, SURVEY §8f rank 4; streaming, C++). Returns (rows read, rows kept);
+    the output feeds Replay(trace_csv=...) / the simulator like the bundled trace."""
+    read, kept = C.c_int64(), C.c_int64()
+    if _ffi.gfx_sim_azure_convert(in_path.encode(), out_path.encode(), int(top_k), int(max_minutes),
+                                  C.byref(read), C.byref(kept)) != 0:
+        raise _ffi.GfxError(-1, _ffi.gfx_sim_last_error().decode(errors="replace"))
+    return read.value, kept.value
+
+
 C3_ARENA_MB = 128.0  # per GPU: 8 x 128 MiB < 1294 MB of C3 weights (working set > aggregate cache)
 
 

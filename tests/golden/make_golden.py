@@ -4,6 +4,7 @@ Run HERE (needs /root/reference and oracle/_ref built by `make -C oracle ref`):
     python tests/golden/make_golden.py
 Writes:
   tests/golden/table1_models.csv   paper Table I catalog (proj/data/models.csv, data only)
+  tests/golden/trace_zipf.csv      bundled 60 x 6 invocation trace (proj/data/trace_zipf.csv, data only)
   tests/golden/fleet_goldens.json  per-config decision/request/log digests, counts,
                                    report fields and nearest-rank p50/p99 from the
                                    reference's run_stream
@@ -47,6 +48,9 @@ def fleet_cases():
 def main():
     shutil.copyfile(os.path.join(REF_PROJ, "data", "models.csv"),
                     os.path.join(HERE, "table1_models.csv"))
+    # bundled invocation trace (data only): the Azure-ingest round-trip test
+    shutil.copyfile(os.path.join(REF_PROJ, "data", "trace_zipf.csv"),
+                    os.path.join(HERE, "trace_zipf.csv"))
     ref = simabi.load_ref()
     cat = simabi.table1_catalog()
     trace = open(os.path.join(REF_PROJ, "data", "trace_zipf.csv")).read()

@@ -204,3 +204,67 @@ def test_pipelined_random_streams_vs_oracle(product, oracle):
                                  policy=pol, o3_limit=int(rng.integers(0, 4)), debug_checks=True, pipeline=True)
         a, b = oracle.run_stream(cat, cfg, mi, arr), product.run_stream(cat, cfg, mi, arr)
         simabi.assert_same(a, b, f"iter {it}")
+
+
+def _write_azure(path, ids, counts):
+    """Azure Functions 2019 layout: HashOwner,HashApp,HashFunction,Trigger,1..N."""
+    with open(path, "w") as f:
+        f.write("HashOwner,HashApp,HashFunction,Trigger," + ",".join(str(m + 1) for m in range(counts.shape[1])) + "\n")
+        for (o, a, fn), row in zip(ids, counts):
+            f.write(f"{o},{a},{fn},http," + ",".join(map(str, row.tolist())) + "\n")
+
+
+def test_azure_ingest_round_trip_hits_goldens(product, table1, tmp_path):
+    """The bundled trace rewritten in the Azure dataset layout and ingested back
+    (top_k = all 60) reproduces the reference goldens bit for bit."""
+    import paper_2303_05601_b200 as gfx
+    rows = [ln.strip().split(",") for ln in open(os.path.join(simabi.GOLDEN, "trace_zipf.csv")).read().splitlines()[1:]]
+    ids = [("o1", "a1", r[0]) for r in rows]
+    counts = np.array([[int(x) for x in r[1:]] for r in rows], np.int64)
+    az, out = str(tmp_path / "az.csv"), str(tmp_path / "trace.csv")
+    _write_azure(az, ids, counts)
+    read, kept = gfx.azure_trace_to_csv(az, out, top_k=60)
+    assert (read, kept) == (60, 60)
+    trace = open(out).read()
+    case = _cases()[0]
+    cfg = simabi.make_config(gpus=case["gpus"], working_set=case["working_set"], policy=case["policy"],
+                             seed=case["seed"], o3_limit=case["o3_limit"], capacity_mb=case["capacity_mb"],
+                             synthetic=False, log_events=2)
+    res = product.run(table1, cfg, trace_csv=trace)
+    assert f"{res.decision_digest:016x}" == case["decision_digest"]
+    assert f"{res.log_digest:016x}" == case["log_digest"]
+
+
+def test_azure_ingest_at_scale(product, oracle, table1, tmp_path):
+    """A day file of 4000 functions x 1440 minutes with heavy-tailed rates:
+    the streaming top-k equals a numpy restatement (total desc, id asc; kept rows
+    in file order), and the fleet schedule on the ingested trace is bit-exact
+    between product and oracle."""
+    import paper_2303_05601_b200 as gfx
+    rng = np.random.default_rng(5)
+    F, M, K = 4000, 1440, 300
+    rate = rng.pareto(1.2, size=F) * 0.05
+    counts = rng.poisson(rate[:, None] * np.ones((1, M))).astype(np.int64)
+    ids = [(f"{rng.integers(1 << 60):015x}", f"{rng.integers(1 << 60):015x}", f"{i:06x}") for i in range(F)]
+    az, out = str(tmp_path / "day.csv"), str(tmp_path / "trace.csv")
+    _write_azure(az, ids, counts)
+    read, kept = gfx.azure_trace_to_csv(az, out, top_k=K, max_minutes=720)
+    assert (read, kept) == (F, K)
+    tot = counts[:, :720].sum(1)
+    names = [":".join(t) for t in ids]
+    order = sorted(range(F), key=lambda i: (-tot[i], names[i]))[:K]
+    want = sorted(order)
+    lines = open(out).read().splitlines()
+    assert lines[0] == "function_id," + ",".join(f"m{m + 1}" for m in range(720))
+    got_names = [ln.split(",", 1)[0] for ln in lines[1:]]
+    assert got_names == [names[i] for i in want]
+    got = np.array([[int(x) for x in ln.split(",")[1:]] for ln in lines[1:]], np.int64)
+    assert np.array_equal(got, counts[want, :720])
+    trace = open(out).read()
+    cfg = simabi.make_config(gpus=8, working_set=20, policy="lalbo3", rpm=600, minutes=30, synthetic=False,
+                             capacity_mb=8192.0, log_events=2)
+    a, b = oracle.run(table1, cfg, trace_csv=trace), product.run(table1, cfg, trace_csv=trace)
+    simabi.assert_same(a, b, "azure day file")
+    assert a.log_digest == b.log_digest
+    with pytest.raises(gfx.GfxError, match="Azure"):
+        gfx.azure_trace_to_csv(os.path.join(simabi.GOLDEN, "trace_zipf.csv"), out)
