@@ -7,7 +7,7 @@
 //                         tiles, X via a 2-D TMA tensor map, W tiles
 //                         (pre-swizzled 16 KB) via 1-D bulk TMA from the arena,
 //                         double-buffered TMEM accumulators; fused bias / GELU /
-//                         residual epilogue through TMA stores; bf16 out.
+//                         residual epilogue (16 warps) through TMA stores; bf16 out.
 //                         Tensor-core bound. Opt-in 2-SM (cta_group::2) variant.
 //   K3 attention_tc_kernel softmax(Q K^T / sqrt(64)) V per (sequence, head),
 //                         S = 128: one CTA of 4 warps, both products on tcgen05
@@ -49,7 +49,8 @@ __device__ __forceinline__ float gelu(float x) { return 0.5f * x * (1.0f + erff(
 // Persistent: one CTA per SM loops over 128 x kBN output tiles; the TMEM holds
 // two accumulators so the epilogue of tile i overlaps the MMAs of tile i+1.
 
-constexpr int kGM = 128, kGK = 64, kGThreads = 384;  // A producer, MMA, 8 epilogue warps, 2 B producers
+constexpr int kGM = 128, kGK = 64, kGThreads = 640;  // A producer, MMA, 16 epilogue warps, 2 B producers
+constexpr int kGEpiWarps = 16, kGBWarp0 = 2 + kGEpiWarps;
 constexpr uint32_t kGATile = 128 * 128;  // A: 128 rows x 64 bf16 (16 KB)
 constexpr uint32_t kGSmem = 192 * 1024;  // stage ring budget
 
@@ -87,11 +88,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
     constexpr uint32_t kTmemCols = 2 * kBN <= 256 ? 256 : 512;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
-    // Epilogue staging: per epilogue half, two 128 x 32 bf16 boxes (8 KB,
-    // SWIZZLE_64B image) for the coalesced TMA store of each 32-column chunk
-    // (and the residual load).
-    uint8_t* stage_out = smem + kGSmem;
-    __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], tfull_bar[2], tempty_bar[2], res_bar[2][2];
+    __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], tfull_bar[2], tempty_bar[2], res_bar[4];
     __shared__ __align__(8) uint64_t pair_full[kStages];
     __shared__ uint32_t tmem_s;
     __shared__ uint32_t pt[GFX_MAX_PAGES];
@@ -135,10 +132,9 @@ __global__ void __launch_bounds__(kGThreads, 1)
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull_bar[b], 1);
-            mbar_init(&tempty_bar[b], kPair ? 16 : 8);  // epilogue warps (of both CTAs in pair mode)
-            mbar_init(&res_bar[0][b], 1);
-            mbar_init(&res_bar[1][b], 1);
+            mbar_init(&tempty_bar[b], kPair ? 2 * kGEpiWarps : kGEpiWarps);  // epilogue warps (of both CTAs in pair mode)
         }
+        for (int g = 0; g < 4; ++g) mbar_init(&res_bar[g], 1);
         mbar_fence_init();
         tma_prefetch_desc(&tmap_x);
         tma_prefetch_desc(&tmap_y);
@@ -158,12 +154,12 @@ __global__ void __launch_bounds__(kGThreads, 1)
     if (tid == 0) mark(1);
 
     constexpr int kBTiles = static_cast<int>(kBBytes / kGATile);  // B tiles per stage and CTA
-    if (warp == 0 || warp >= 10) {
+    if (warp == 0 || warp >= kGBWarp0) {
         // Producers: one continuous stage ring across this CTA's tiles. Warp 0
         // loads A (X rows, 2-D tensor map, after the previous kernel: PDL);
-        // warp 10 + h loads B tile h (weights: pair -> this CTA's half of the
-        // kBN rows), independent of the previous kernel.
-        const int h = warp - 10;
+        // warp kGBWarp0 + h loads B tile h (weights: pair -> this CTA's half of
+        // the kBN rows), independent of the previous kernel.
+        const int h = warp - kGBWarp0;
         if (lane == 0 && h < kBTiles) {
             int g = 0;
             if (warp == 0) pdl_wait();
@@ -239,45 +235,42 @@ __global__ void __launch_bounds__(kGThreads, 1)
             }
         }
     } else {
-        // Epilogue (8 warps): TMEM lane = token row, column = output feature.
-        // Two warps per TMEM lane quarter; half h takes the even / odd 32-column
-        // chunks, with its own staging boxes, named barrier and store thread.
-        const int q = warp & 3, h = (warp - 2) >> 2, ct = tid - 64, ht = ct & 127;
-        const uint32_t hbar = 1u + static_cast<uint32_t>(h);
-        auto half_sync = [&] { asm volatile("bar.sync %0, 128;\n" ::"r"(hbar) : "memory"); };
+        // Epilogue (16 warps): TMEM lane = token row, column = output feature.
+        // Four warps per TMEM lane quarter; group gp takes the 32-column chunks
+        // c = gp (mod 4) with its own 8 KB staging box (128 x 32 bf16,
+        // SWIZZLE_64B image), named barrier and store thread. FFN1's GELU made
+        // the epilogue the bottleneck with 8 warps (~7 µs per 128 x 256 tile
+        // against ~4 µs of MMAs).
+        const int q = warp & 3, gp = (warp - 2) >> 2, ct = tid - 64, ht = ct & 127;
+        const uint32_t gbar = 4u + static_cast<uint32_t>(gp);
+        auto group_sync = [&] { asm volatile("bar.sync %0, 128;\n" ::"r"(gbar) : "memory"); };
+        uint8_t* box = smem + kGSmem + gp * 8192;
         int i = 0, e = 0;
         for (int t = t_first; t < tiles; t += t_step, ++i) {
             const int m0 = tile_m0(t), n0 = (t % n_tiles) * kBN;
             const int b = i & 1;
-            asm volatile("bar.sync 3, 256;\n" ::: "memory");  // previous tile's bias reads done
-            for (int c = ct; c < kBN; c += 256)
+            asm volatile("bar.sync 3, %0;\n" ::"r"(kGEpiWarps * 32) : "memory");  // previous tile's bias reads done
+            for (int c = ct; c < kBN; c += kGEpiWarps * 32)
                 bias_s[c] = *reinterpret_cast<const float*>(translate(a.arena, pt, a.b_off + 4ull * (n0 + c)));
-            asm volatile("bar.sync 3, 256;\n" ::: "memory");
+            asm volatile("bar.sync 3, %0;\n" ::"r"(kGEpiWarps * 32) : "memory");
             mbar_wait(&tfull_bar[b], (i >> 1) & 1);
             tc_fence_after();
             if (ct == 0 && i < 4) mark(7 + i);  // tile i accumulated
             if (t + t_step >= tiles) pdl_trigger();  // last tile: let the next kernel start
-            // Thread = accumulator row (TMEM lane q*32+lane) = output row m0 + q*32 + lane.
-            // Per 32-column chunk: TMEM -> registers -> bias / GELU / residual ->
-            // bf16 into a staging box (row = 64 B, SWIZZLE_64B: chunk j of row r
-            // at j ^ ((r >> 1) & 3)), then one thread of the half TMA-stores the
-            // box: coalesced, and the store drains while the next chunk computes.
             const int r = q * 32 + lane;
 #pragma unroll 1
-            for (int c = h; c < kBN / 32; c += 2, ++e) {
-                const int sb = e & 1;
-                uint8_t* box = stage_out + (h * 2 + sb) * 8192;
-                if (ht == 0) bulk_wait_group_read<1>();  // the store that last read this box is done
-                half_sync();
+            for (int c = gp; c < kBN / 32; c += kGEpiWarps / 4, ++e) {
+                if (ht == 0) bulk_wait_group_read<0>();  // this group's previous store has read the box
+                group_sync();
                 if (kEpi == kEpiResid && ht == 0) {
-                    mbar_arrive_expect_tx(&res_bar[h][sb], 8192);
-                    tma_tile2d_g2s(box, &tmap_r, n0 + c * 32, m0, &res_bar[h][sb]);
+                    mbar_arrive_expect_tx(&res_bar[gp], 8192);
+                    tma_tile2d_g2s(box, &tmap_r, n0 + c * 32, m0, &res_bar[gp]);
                 }
                 float v[32];
                 tmem_ld_32x32b_x32(tmem + static_cast<uint32_t>(b * kBN + c * 32) + (static_cast<uint32_t>(q * 32) << 16), v);
                 float rs[32];
                 if (kEpi == kEpiResid) {
-                    mbar_wait(&res_bar[h][sb], (e >> 1) & 1);
+                    mbar_wait(&res_bar[gp], e & 1);
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
                         const uint4 w = *reinterpret_cast<const uint4*>(box + r * 64 + ((u ^ ((r >> 1) & 3)) << 4));
@@ -306,11 +299,12 @@ __global__ void __launch_bounds__(kGThreads, 1)
                     }
                     o2[j] = __floats2bfloat162_rn(x0, x1);
                 }
+                if (kEpi == kEpiResid) group_sync();  // every row's residual read before the box is overwritten
 #pragma unroll
                 for (int u = 0; u < 4; ++u)
                     *reinterpret_cast<uint4*>(box + r * 64 + ((u ^ ((r >> 1) & 3)) << 4)) = out[u];
                 fence_proxy_async_smem();  // generic-proxy writes -> the TMA store reads
-                half_sync();
+                group_sync();
                 if (ht == 0) {
                     tma_tile2d_s2g(&tmap_y, n0 + c * 32, m0, box);
                     bulk_commit_group();
