@@ -72,3 +72,28 @@ def test_model_catalog_charges_cover_arena_pages():
             s = specs[r["model_id"]]
             assert float(r["occupation_mb"]) == 2 * s.pages
             assert s.pages == -(-s.bytes // (2 << 20))
+
+
+def test_model_registration_limits_without_gpu():
+    """Shapes the inference path cannot take are refused at registration, with
+    the reason (no GPU needed): width > 8192, more than 16 layers, layer inputs
+    not a multiple of 32, outputs not a multiple of 4, unknown family."""
+    import ctypes as C
+
+    import paper_2303_05601_b200 as gfx
+    from paper_2303_05601_b200 import _ffi
+
+    def reg(dims, n_layers=None, family=None):
+        d = gfx.ModelSpec("edge", "mlp", dims, 0, 0).desc()
+        if n_layers is not None:
+            d.n_layers = n_layers
+        if family is not None:
+            d.family = family
+        rc = _ffi.gfx_model_register(60, C.byref(d))
+        return rc, _ffi.gfx_last_error().decode()
+
+    assert reg([1024, 8224, 1000])[1] == "bad layer width"
+    assert reg([1024] * 16 + [1000], n_layers=17)[1] == "bad layer count"
+    assert "multiples of 32" in reg([1000, 1024])[1]
+    assert "multiples of 32" in reg([1024, 1001])[1]
+    assert "family" in reg([1024, 1000], family=7)[1]

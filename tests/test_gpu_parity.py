@@ -209,3 +209,42 @@ def test_pipelined_replay(gfx, policy, gpus):
                                                          pipeline=True))
     assert digests[True] == o.decision_digest
     assert np.array_equal(outs[True], outs[False])
+
+
+@pytest.mark.parametrize("dims", [
+    [1024, 1000],                      # one layer: no hidden activations, no dataflow boundary
+    [32, 4],                           # smallest legal layer
+    [1024, 64, 1000],                  # one-tile hidden layer, maximum split-K
+    [96, 160, 352, 100],               # widths that are not multiples of 64 / 128
+    [256] * 16 + [1000],               # the maximum of 16 layers
+    [8192, 8192, 1000],                # the maximum width (282 MiB of weights)
+], ids=["L1", "min", "h64", "odd", "L16", "w8192"])
+def test_mlp_edge_shapes(gfx, olib, dims):
+    """Edge shapes of the one-launch forward against the oracle's fp64 forward."""
+    import ctypes as C
+    spec = gfx.ModelSpec("edge-" + "x".join(map(str, dims)), "mlp", dims, 0, 0)
+    idx = 50
+    gfx.check(gfx._ffi.gfx_model_register(idx, C.byref(spec.desc())))
+    pages = C.c_int32()
+    gfx.check(gfx._ffi.gfx_model_pages(idx, C.byref(pages)))
+    a = C.c_void_p()
+    gfx.check(gfx._ffi.gfx_arena_create(0, C.c_uint64((pages.value + 2) << 21), C.byref(a)))
+    try:
+        x, y = C.c_void_p(), C.c_void_p()
+        gfx.check(gfx._ffi.gfx_device_alloc(a, 32 * dims[0] * 4, C.byref(x)))
+        gfx.check(gfx._ffi.gfx_device_alloc(a, 2 * 32 * dims[-1] * 4, C.byref(y)))
+        gfx.check(gfx._ffi.gfx_load_h2d(a, idx, None))
+        rid = 7000 + len(dims)
+        gfx.check(gfx._ffi.gfx_fill_params(a, x, 32 * dims[0], gfx._ffi.gfx_input_seed(rid), 0xFFFFFFFF, 1.0))
+        for _ in range(2):  # the second launch runs on the other counter bank
+            gfx.check(gfx._ffi.gfx_infer(a, idx, x, y, 32, None))
+            got = np.zeros((2, 32, dims[-1]), np.float32)
+            gfx.check(gfx._ffi.gfx_memcpy_d2h(a, got.ctypes.data, y, got.nbytes))
+            _, lo, pr = oracle_forward(olib, gfx, spec, rid)
+            assert rel(got[0], lo) <= TOL
+            assert rel(got[1], pr) <= TOL
+        gfx.check(gfx._ffi.gfx_evict(a, idx))
+        gfx.check(gfx._ffi.gfx_device_free(a, x))
+        gfx.check(gfx._ffi.gfx_device_free(a, y))
+    finally:
+        gfx._ffi.gfx_arena_destroy(a)
