@@ -74,14 +74,19 @@ struct GemmArgs {
 // point: 6 stages (1.6 µs of MMA work) instead of 4 (1.07 µs) cover the TMA
 // latency under load, which bounded the single-CTA MMA phase at ~78 % of
 // issue rate (GFX_TRACE_GEMM; multicasting B alone did not help).
-// Barriers: each CTA's full barrier counts its own bytes; the odd CTA's warp 1
-// relays "stage s landed" to the even CTA's pair_full; the issuer's commits
-// multicast to both CTAs' empty / tfull barriers; both epilogues arrive on the
-// even CTA's tempty.
+// Barriers: every operand load of either CTA is a .cta_group::2 tensor TMA
+// whose bytes complete the EVEN CTA's full barrier (the even CTA's producers
+// expect both halves), so the issuer waits on one barrier — an earlier version
+// relayed the odd CTA's "landed" by a remote arrive, one stage at a time, and
+// that relay set a 0.7 µs stage cadence; weights come through a tensor map
+// over the whole arena (pre-swizzled tiles, SWIZZLE_NONE boxes); the issuer's
+// commits multicast to both CTAs' empty / tfull barriers; both epilogues arrive
+// on the even CTA's tempty.
 template <int kEpi, int kBN, bool kPair>
 __global__ void __launch_bounds__(kGThreads, 1)
     gemm_bf16_kernel(const __grid_constant__ CUtensorMap tmap_x, const __grid_constant__ CUtensorMap tmap_y,
-                     const __grid_constant__ CUtensorMap tmap_r, const __grid_constant__ GemmArgs a) {
+                     const __grid_constant__ CUtensorMap tmap_r, const __grid_constant__ CUtensorMap tmap_w,
+                     const __grid_constant__ GemmArgs a) {
     constexpr uint32_t kBBytes = (kPair ? kBN / 2 : kBN) * 128;  // B: this CTA's rows x 64 bf16
     constexpr uint32_t kStage = kGATile + kBBytes;
     constexpr int kStages = static_cast<int>(kGSmem / kStage);
@@ -89,7 +94,6 @@ __global__ void __launch_bounds__(kGThreads, 1)
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
     __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], tfull_bar[2], tempty_bar[2], res_bar[4];
-    __shared__ __align__(8) uint64_t pair_full[kStages];
     __shared__ uint32_t tmem_s;
     __shared__ uint32_t pt[GFX_MAX_PAGES];
     __shared__ float bias_s[kBN];
@@ -128,7 +132,6 @@ __global__ void __launch_bounds__(kGThreads, 1)
             // stage's three 16 KB loads come from three threads in parallel.
             mbar_init(&full_bar[s], 1 + kBBytes / kGATile);
             mbar_init(&empty_bar[s], 1);
-            mbar_init(&pair_full[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull_bar[b], 1);
@@ -139,6 +142,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
         tma_prefetch_desc(&tmap_x);
         tma_prefetch_desc(&tmap_y);
         if (kEpi == kEpiResid) tma_prefetch_desc(&tmap_r);
+        if (kPair) tma_prefetch_desc(&tmap_w);
     }
     if (warp == 1) {
         if (kPair)
@@ -169,12 +173,24 @@ __global__ void __launch_bounds__(kGThreads, 1)
                     const int s = g % kStages;
                     if (g >= kStages) mbar_wait(&empty_bar[s], ((g / kStages) & 1) ^ 1);
                     uint8_t* st = smem + static_cast<size_t>(s) * kStage;
-                    if (warp == 0) {
+                    if (kPair) {
+                        // Both CTAs load their halves; only the even CTA's barrier counts them.
+                        if (rank == 0) mbar_arrive_expect_tx(&full_bar[s], 2 * kGATile);
+                        if (warp == 0) {
+                            tma_tile2d_g2s_pair(st, &tmap_x, k * kGK, m0, &full_bar[s]);
+                            smark(g, 0);
+                        } else {
+                            const int bt = nb * (kBN / 128) + static_cast<int>(rank) * kBTiles + h;
+                            const uint64_t v = a.w_off + (static_cast<uint64_t>(bt) * ktiles_row + k) * kGATile;
+                            const uint64_t row = static_cast<uint64_t>(translate(a.arena, pt, v) - a.arena) / 128;
+                            tma_tile2d_g2s_pair(st + kGATile + h * kGATile, &tmap_w, 0, static_cast<int>(row), &full_bar[s]);
+                        }
+                    } else if (warp == 0) {
                         mbar_arrive_expect_tx(&full_bar[s], kGATile);
                         tma_tile2d_g2s(st, &tmap_x, k * kGK, m0, &full_bar[s]);
                         smark(g, 0);
                     } else {
-                        const int bt = nb * (kBN / 128) + (kPair ? static_cast<int>(rank) * kBTiles : 0) + h;
+                        const int bt = nb * (kBN / 128) + h;
                         const uint64_t v = a.w_off + (static_cast<uint64_t>(bt) * ktiles_row + k) * kGATile;
                         mbar_arrive_expect_tx(&full_bar[s], kGATile);
                         tma_bulk_g2s(st + kGATile + h * kGATile, translate(a.arena, pt, v), kGATile, &full_bar[s]);
@@ -184,18 +200,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
         }
     } else if (warp == 1) {
         if (kPair && rank == 1) {
-            // Odd CTA of the pair: relay "my half of stage s landed" to the issuer.
-            if (lane == 0) {
-                int g = 0;
-                for (int t = t_first; t < tiles; t += t_step)
-                    for (int k = 0; k < nk; ++k, ++g) {
-                        const int s = g % kStages;
-                        mbar_wait(&full_bar[s], (g / kStages) & 1);
-                        smark(g, 1);
-                        mbar_arrive_remote(&pair_full[s], 0);
-                        smark(g, 2);
-                    }
-            }
+            // Odd CTA of the pair: nothing to issue (its loads complete the even CTA's barrier).
         } else if (lane == 0) {
             constexpr uint32_t idesc = umma_idesc<kPair ? 2 * kGM : kGM, kBN, 1>();  // BF16 x BF16 -> F32
             int g = 0, i = 0;
@@ -208,7 +213,6 @@ __global__ void __launch_bounds__(kGThreads, 1)
                     const int s = g % kStages;
                     mbar_wait(&full_bar[s], (g / kStages) & 1);
                     smark(g, 1);
-                    if (kPair) mbar_wait(&pair_full[s], (g / kStages) & 1);
                     smark(g, 2);
                     tc_fence_after();
                     if (g == 0) mark(2);
@@ -672,6 +676,18 @@ void gemm_bn(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_
                               static_cast<uint64_t>(T), static_cast<uint64_t>(N) * 2, 32, kGM,
                               CU_TENSOR_MAP_SWIZZLE_64B))
         throw CudaError("cuTensorMapEncodeTiled failed (bert gemm residual)");
+    // Pair mode: weight tiles as 16 KB boxes (64 bf16 x 128 rows of 128 B, raw bytes:
+    // the tiles are stored pre-swizzled) of a tensor map over the arena span the
+    // model's pages cover, so the odd CTA's loads can complete the even CTA's barrier.
+    CUtensorMap tmw = tmy;
+    if (kPair) {
+        uint32_t maxp = 0;
+        for (uint32_t i = 0; i < pt.n; ++i) maxp = std::max(maxp, pt.page[i]);
+        const uint64_t rows = (static_cast<uint64_t>(maxp) + 1) * (kPageBytes / 128);
+        if (!encode_tensor_map_2d(&tmw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, arena, 64, rows, 128, 64, 128,
+                                  CU_TENSOR_MAP_SWIZZLE_NONE))
+            throw CudaError("cuTensorMapEncodeTiled failed (bert gemm arena weights)");
+    }
     static const bool trace_on = std::getenv("GFX_TRACE_GEMM") != nullptr;
     GemmArgs a{nullptr, arena, w_off, b_off, y, resid, T, K, N, pt};
     static bool attr_set = false;
@@ -707,9 +723,9 @@ void gemm_bn(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_
         attr[1].val.clusterDim.z = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 2;
-        GFX_CUDA(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<kEpi, kBN, kPair>, tm, tmy, tmr, a));
+        GFX_CUDA(cudaLaunchKernelEx(&cfg, gemm_bf16_kernel<kEpi, kBN, kPair>, tm, tmy, tmr, tmw, a));
     } else {
-        launch_pdl(gemm_bf16_kernel<kEpi, kBN, kPair>, dim3(grid), dim3(kGThreads), smem, s, pdl, tm, tmy, tmr, a);
+        launch_pdl(gemm_bf16_kernel<kEpi, kBN, kPair>, dim3(grid), dim3(kGThreads), smem, s, pdl, tm, tmy, tmr, tmw, a);
     }
     if (trace_on) {  // debug timeline: µs after the first CTA started, min / median / max over CTAs
         std::vector<unsigned long long> tr(static_cast<size_t>(16) * grid + 512);
@@ -750,10 +766,11 @@ template <int kEpi>
 void gemm(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_off, const __nv_bfloat16* x,
           __nv_bfloat16* y, const __nv_bfloat16* resid, int T, int K, int N, cudaStream_t s, bool pdl) {
     if (T % kGM || N % 128 || K % kGK) throw std::runtime_error("bert gemm: T, N multiple of 128, K of 64");
-    // The 2-SM variant (GFX_GEMM_PAIR=1) is correct but measured slower: with 6
-    // stages of 32 KB in flight per CTA its TMA latency rose to ~3 µs per stage
-    // (1.2 vs 1.6 ms per forward; per-stage trace in GFX_TRACE_GEMM), so the
-    // single-CTA 128 x 256 kernel is the default until that is understood.
+    // The 2-SM variant (GFX_GEMM_PAIR=1) is correct; with the relay removed
+    // (.cta_group::2 loads complete the even CTA's barrier) it runs 1.21 ms per
+    // forward vs 1.17-1.18 for the single-CTA kernel (was 1.63 with the relay):
+    // both advance ~0.45 µs per K stage with ~2 µs TMA latency at 192 KB in
+    // flight per SM, so the single-CTA kernel stays the default.
     static const bool pair = std::getenv("GFX_GEMM_PAIR") != nullptr;
     if (N % 256 == 0 && (T / kGM) % 2 == 0 && pair)
         gemm_bn<kEpi, 256, true>(arena, pt, w_off, b_off, x, y, resid, T, K, N, s, pdl);

@@ -55,6 +55,17 @@ __device__ __forceinline__ void tma_tile2d_g2s(void* dst, const CUtensorMap* map
         "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar))
         : "memory");
 }
+// 2-D tensor tile into THIS CTA's smem whose complete_tx lands on the mbarrier at
+// the same offset in the LEADER (even) CTA of the CTA pair (.cta_group::2; bit 24
+// of the shared::cluster address selects the pair rank): both CTAs' operand
+// halves then complete one barrier, the one the 2-SM MMA issuer waits on.
+__device__ __forceinline__ void tma_tile2d_g2s_pair(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+        "%3}], [%4];\n" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(smem_u32(bar) & 0xFEFFFFFFu)
+        : "memory");
+}
 // Bulk prefetch of global memory into L2 (no shared-memory destination).
 __device__ __forceinline__ void prefetch_l2_bulk(const void* src, uint32_t bytes) {
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;\n" ::"l"(src), "r"(bytes) : "memory");
