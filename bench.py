@@ -422,6 +422,15 @@ def locality_extras(gfx, world):
                 "avg_latency_ms": round(lr.sim_avg_latency_s * 1e3, 3), "p99_ms": round(lr.sim_p99_s * 1e3, 3),
                 "hit_rate": round(lr.hits / (lr.hits + lr.misses), 4), "local_enqueues": int(lr.local_enqueues),
                 "false_misses": int(lr.false_misses)}
+    rep = gfx.Replay(cat, gfx.sim_config(gpus=3, capacity_mb=204.0, policy="lalbo3", pipeline=True), n_devices=1,
+                     use_p2p=True, record_kernels=False)
+    rep.run()
+    lr = rep.run_live(scale3, 0.3)
+    rep.close()
+    fl["lalbo3_ema_pipelined"] = {
+        "avg_latency_ms": round(lr.sim_avg_latency_s * 1e3, 3), "p99_ms": round(lr.sim_p99_s * 1e3, 3),
+        "hit_rate": round(lr.hits / (lr.hits + lr.misses), 4), "local_enqueues": int(lr.local_enqueues),
+        "false_misses": int(lr.false_misses)}
     live["fleet3_emulated"] = fl
     res["live_closed_loop_1gpu_paper_regime"] = live
     # Pipelined GPUs (extension): a running GPU accepts one staged

@@ -11,6 +11,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <deque>
 #include <cstring>
 #include <set>
 #include <chrono>
@@ -328,8 +329,8 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
             e0 = req_timer.next();
             req_start[rid] = e0;
         }
-        LiveTask* lt = live_mode ? &live_task[static_cast<size_t>(gpu)] : nullptr;
-        if (lt) *lt = LiveTask{};
+        LiveTask live_t{};
+        LiveTask* lt = live_mode ? &live_t : nullptr;
         if (!hit) {
             if (e0) GFX_CUDA(cudaEventRecord(e0, m.copy_stream()));
             if (lt) {
@@ -416,9 +417,9 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
         }
         if (live_mode) {
             // Live mode: the engine polls this to learn the request finished (output included).
-            cudaEvent_t e = req_timer.next();
-            GFX_CUDA(cudaEventRecord(e, args.host_io ? b.io_out : m.compute_stream()));
-            live_done[static_cast<size_t>(gpu)] = e;
+            lt->done = req_timer.next();
+            GFX_CUDA(cudaEventRecord(lt->done, args.host_io ? b.io_out : m.compute_stream()));
+            live_q[static_cast<size_t>(gpu)].push_back(live_t);
         }
     }
 
@@ -426,23 +427,30 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
 
     // Live closed-loop serving (gpufaas::run_live): completions are observed
     // on the device instead of predicted.
-    // Per GPU, the running task's load (copy stream) and inference (compute
-    // stream) events; measured() reports them to the engine's EMA.
+    // Per GPU, a FIFO of dispatched tasks (two deep with pipelined GPUs): load
+    // (copy stream) and inference (compute stream) events for measured(), and
+    // the completion event done() polls; the engine retires the front.
     struct LiveTask {
-        cudaEvent_t ls = nullptr, le = nullptr, is = nullptr, ie = nullptr;
+        cudaEvent_t ls = nullptr, le = nullptr, is = nullptr, ie = nullptr, done = nullptr;
     };
     struct LiveExec : gpufaas::LiveExecutor {
         gfx_replay_s* r = nullptr;
         bool done(int gpu) override {
-            cudaEvent_t e = r->live_done[static_cast<size_t>(gpu)];
-            if (!e) return true;
-            const cudaError_t q = cudaEventQuery(e);
-            if (q == cudaErrorNotReady) return false;
-            GFX_CUDA(q);
+            const auto& q = r->live_q[static_cast<size_t>(gpu)];
+            if (q.empty()) return true;
+            const cudaError_t st = cudaEventQuery(q.front().done);
+            if (st == cudaErrorNotReady) return false;
+            GFX_CUDA(st);
             return true;
         }
+        void retire(int gpu) override {
+            auto& q = r->live_q[static_cast<size_t>(gpu)];
+            if (!q.empty()) q.pop_front();
+        }
         bool measured(int gpu, gpufaas::SimTime* load_us, gpufaas::SimTime* infer_us) override {
-            const LiveTask& t = r->live_task[static_cast<size_t>(gpu)];
+            const auto& q = r->live_q[static_cast<size_t>(gpu)];
+            if (q.empty()) return false;
+            const LiveTask& t = q.front();
             if (!t.is) return false;
             *load_us = t.ls ? std::max<gpufaas::SimTime>(1, std::llround(elapsed_ms(t.ls, t.le) * 1e3)) : 0;
             *infer_us = std::max<gpufaas::SimTime>(1, std::llround(elapsed_ms(t.is, t.ie) * 1e3));
@@ -451,8 +459,7 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
     };
     bool live_mode = false;
     double live_scale = 0.0, live_alpha = 0.0;
-    std::vector<cudaEvent_t> live_done;
-    std::vector<LiveTask> live_task;
+    std::vector<std::deque<LiveTask>> live_q;
 
     void run_live(double time_scale, double ema_alpha, gfx_replay_result* out) {
         if (args.only_gpu >= 0) throw std::invalid_argument("live mode runs every GPU in one process (only_gpu < 0)");
@@ -460,8 +467,7 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
         live_mode = true;
         live_scale = time_scale;
         live_alpha = ema_alpha;
-        live_done.assign(static_cast<size_t>(gpu_count()), nullptr);
-        live_task.assign(static_cast<size_t>(gpu_count()), LiveTask{});
+        live_q.assign(static_cast<size_t>(gpu_count()), {});
         try {
             run(out);
         } catch (...) {

@@ -4,6 +4,7 @@
 // tests drive all three identically. Declared in include/gpufaas_b200.h.
 #include <chrono>
 #include <cstdint>
+#include <deque>
 #include <exception>
 #include <fstream>
 #include <sstream>
@@ -131,25 +132,48 @@ void* gfx_sim_run_stream(const char* catalog_csv, const gfx_sim_config* c, int n
 // run_live()'s real-time loop and live ClusterState without a GPU.
 void* gfx_sim_run_live_timed(const char* catalog_csv, const char* trace_csv, const gfx_sim_config* c,
                              double time_scale, double ema_alpha) {
+    // Per GPU a FIFO of tasks; a load starts when the copy engine is free, an
+    // inference when its load and the previous inference are done.
     struct Timed : ExecutionListener, LiveExecutor {
         using clock = std::chrono::steady_clock;
+        struct Task {
+            clock::time_point due;
+            SimTime load, infer;
+        };
         const Catalog* cat = nullptr;
-        std::vector<clock::time_point> due;
-        std::vector<SimTime> load, infer;  // per GPU: the running task's device durations
+        std::vector<std::deque<Task>> q;
+        std::vector<clock::time_point> copy_free, compute_free;
         double scale = 1;
         void on_begin_execution(int gpu, const Request& r, int, bool hit, const std::vector<int>&, int, SimTime,
                                 SimTime) override {
             const ModelProfile& p = cat->lookup(r.model_id);
             const std::size_t g = static_cast<std::size_t>(gpu);
-            load[g] = hit ? 0 : std::max<SimTime>(1, std::llround(p.load_time_us / scale));
-            infer[g] = std::max<SimTime>(1, std::llround(p.infer_time_us / scale));
-            due[g] = clock::now() + std::chrono::microseconds(load[g] + infer[g]);
+            Task t{};
+            t.load = hit ? 0 : std::max<SimTime>(1, std::llround(p.load_time_us / scale));
+            t.infer = std::max<SimTime>(1, std::llround(p.infer_time_us / scale));
+            clock::time_point ready = clock::now();
+            if (!hit) {
+                ready = std::max(ready, copy_free[g]) + std::chrono::microseconds(t.load);
+                copy_free[g] = ready;
+            }
+            t.due = std::max(ready, compute_free[g]) + std::chrono::microseconds(t.infer);
+            compute_free[g] = t.due;
+            q[g].push_back(t);
         }
         void on_complete(int, int, SimTime) override {}
-        bool done(int gpu) override { return clock::now() >= due[static_cast<std::size_t>(gpu)]; }
+        bool done(int gpu) override {
+            const auto& d = q[static_cast<std::size_t>(gpu)];
+            return d.empty() || clock::now() >= d.front().due;
+        }
+        void retire(int gpu) override {
+            auto& d = q[static_cast<std::size_t>(gpu)];
+            if (!d.empty()) d.pop_front();
+        }
         bool measured(int gpu, SimTime* l, SimTime* i) override {
-            *l = load[static_cast<std::size_t>(gpu)];
-            *i = infer[static_cast<std::size_t>(gpu)];
+            const auto& d = q[static_cast<std::size_t>(gpu)];
+            if (d.empty()) return false;
+            *l = d.front().load;
+            *i = d.front().infer;
             return true;
         }
     };
@@ -162,9 +186,9 @@ void* gfx_sim_run_live_timed(const char* catalog_csv, const char* trace_csv, con
         Timed dev;
         const std::size_t G = static_cast<std::size_t>(std::max(c->gpu_count, 1));
         dev.cat = &cat;
-        dev.due.assign(G, std::chrono::steady_clock::now());
-        dev.load.assign(G, 0);
-        dev.infer.assign(G, 0);
+        dev.q.assign(G, {});
+        dev.copy_free.assign(G, std::chrono::steady_clock::now());
+        dev.compute_free.assign(G, std::chrono::steady_clock::now());
         dev.scale = time_scale;
         const auto t0 = std::chrono::steady_clock::now();
         h->result = run_live(gpufaas::capi::to_sim_config(*c), cat, std::move(reqs), time_scale, &dev, dev, nullptr,

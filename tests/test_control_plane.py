@@ -104,9 +104,9 @@ def test_reference_acceptance_suite_on_product():
     assert "98280 enumerated instances" in prod.stdout and "0 decision mismatches" in prod.stdout
 
 
-@pytest.mark.parametrize("ema", [0.0, 0.5])
-@pytest.mark.parametrize("policy", ["lb", "lalbo3"])
-def test_live_closed_loop_on_timed_device(product, table1, policy, ema):
+@pytest.mark.parametrize("policy,ema,pipe", [("lb", 0.0, False), ("lalbo3", 0.0, False), ("lb", 0.5, False),
+                                              ("lalbo3", 0.5, False), ("lalbo3", 0.0, True), ("lb", 0.5, True)])
+def test_live_closed_loop_on_timed_device(product, table1, policy, ema, pipe):
     """Extension: run_live() — arrivals released in real time,
     completions observed from a stand-in device that runs each task for its
     catalog duration / time_scale (and, with ema > 0, reports those durations
@@ -115,7 +115,7 @@ def test_live_closed_loop_on_timed_device(product, table1, policy, ema):
     elapsed, with a hit ratio close to the virtual-time schedule's (the device
     is the catalog, uniformly scaled)."""
     scale = 400.0
-    cfg = simabi.make_config(gpus=4, policy=policy, minutes=1, debug_checks=True)
+    cfg = simabi.make_config(gpus=4, policy=policy, minutes=1, debug_checks=True, pipeline=pipe)
     live = product.run_live_timed(table1, cfg, scale, ema)
     virt = product.run(table1, cfg)
     n = len(virt.arrival)
@@ -125,7 +125,7 @@ def test_live_closed_loop_on_timed_device(product, table1, policy, ema):
     assert sorted(dispatched.tolist()) == list(range(n)), "each request dispatched exactly once"
     assert np.array_equal(live.arrival, np.floor(virt.arrival / scale + 0.5).astype(np.int64))
     assert (live.dispatched >= live.arrival).all() and (live.completed >= live.dispatched).all()
-    if ema == 0.0:  # planned times are the catalog's
+    if ema == 0.0:  # planned times are the catalog's (a staged task also waits for the running one)
         infer_us = live.times[kinds != 2, 2]
         done_after = live.completed[dispatched] - live.dispatched[dispatched]
         assert (done_after + 2 >= infer_us / scale).all(), "completion observed before the task could finish"

@@ -18,13 +18,14 @@ def _digests(outs):
     return [hashlib.sha1(o.tobytes()).hexdigest() for o in outs]
 
 
-@pytest.mark.parametrize("gpus,policy,ema", [(1, "lalbo3", 0.0), (3, "lb", 0.0), (3, "lalbo3", 0.0),
-                                              (3, "lalbo3", 0.3)])
-def test_live_outputs_match_replay(gpus, policy, ema):
+@pytest.mark.parametrize("gpus,policy,ema,pipe", [(1, "lalbo3", 0.0, False), (3, "lb", 0.0, False),
+                                                   (3, "lalbo3", 0.0, False), (3, "lalbo3", 0.3, False),
+                                                   (3, "lalbo3", 0.3, True), (1, "lb", 0.0, True)])
+def test_live_outputs_match_replay(gpus, policy, ema, pipe):
     import paper_2303_05601_b200 as gfx
     gfx.register_models(gfx.load_model_specs("mlp_c2"))
     cat = gfx.catalog_text("mlp_c2_paper")
-    cfg = gfx.sim_config(gpus=gpus, capacity_mb=204.0, policy=policy, minutes=1)
+    cfg = gfx.sim_config(gpus=gpus, capacity_mb=204.0, policy=policy, minutes=1, pipeline=pipe)
     rep = gfx.Replay(cat, cfg, n_devices=1, use_p2p=gpus > 1, keep_outputs=True)
     base = rep.run()
     n = int(base.n_requests)
