@@ -23,13 +23,14 @@ def _free_port():
     return p
 
 
-def _worker(rank, world, port, cat, q):
+def _worker(rank, world, port, cat, q, pipeline=False):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         lib = simabi.load_product()
-        cfg = simabi.make_config(gpus=world, capacity_mb=204.0, policy="lalbo3", rpm=325 * world, minutes=3)
+        cfg = simabi.make_config(gpus=world, capacity_mb=204.0, policy="lalbo3", rpm=325 * world, minutes=3,
+                                 pipeline=pipeline)
         res = lib.run(cat, cfg)
         mine = res.ints[:, 2] == rank
         dispatched = res.ints[mine & (res.ints[:, 0] != 2), 1]
@@ -53,12 +54,12 @@ def _worker(rank, world, port, cat, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2])
-def test_ranks_share_one_schedule_and_partition_requests(mlp_catalog, world):
+@pytest.mark.parametrize("world,pipeline", [(2, False), (2, True), (3, False)])
+def test_ranks_share_one_schedule_and_partition_requests(mlp_catalog, world, pipeline):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, world, port, mlp_catalog, q)) for r in range(world)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, mlp_catalog, q, pipeline)) for r in range(world)]
     for p in procs:
         p.start()
     digests, ids, n, sizes = q.get(timeout=300)
