@@ -507,17 +507,75 @@ void GpuManager::infer(int model, const void* in_v, void* out_v, void* debug_hid
             cudaEvent_t e0, e1;
             GFX_CUDA(cudaEventCreate(&e0));
             GFX_CUDA(cudaEventCreate(&e1));
+            // GFX_MLP_REPEAT_MODE: 0 back-to-back; 1 each launch after a compute-stream
+            // wait on an event of the copy stream (the replay's load dependency);
+            // 2 events around every launch (the replay's kernel timer), summed.
+            static const int rmode = std::getenv("GFX_MLP_REPEAT_MODE") ? std::atoi(std::getenv("GFX_MLP_REPEAT_MODE")) : 0;
+            std::vector<cudaEvent_t> ev;
+            if (rmode == 2)
+                for (int r = 0; r < 2 * repeat; ++r) {
+                    cudaEvent_t e;
+                    GFX_CUDA(cudaEventCreate(&e));
+                    ev.push_back(e);
+                }
+            cudaEvent_t cev;
+            GFX_CUDA(cudaEventCreateWithFlags(&cev, cudaEventDisableTiming));
+            // mode 3: back-to-back launches while the copy stream streams pinned host
+            // memory into a scratch buffer (the replay's concurrent model loads).
+            void* hbuf = nullptr;
+            void* dbuf = nullptr;
+            cudaEvent_t kev;  // modes 4/5: the previous forward's completion
+            GFX_CUDA(cudaEventCreateWithFlags(&kev, cudaEventDisableTiming));
+            if (rmode == 4 || rmode == 5) {
+                GFX_CUDA(cudaHostAlloc(&hbuf, 1u << 20, cudaHostAllocDefault));
+                GFX_CUDA(cudaMalloc(&dbuf, 1u << 20));
+            }
+            if (rmode == 3) {
+                GFX_CUDA(cudaHostAlloc(&hbuf, 256ull << 20, cudaHostAllocDefault));
+                GFX_CUDA(cudaMalloc(&dbuf, 256ull << 20));
+                for (int r = 0; r < 8; ++r)
+                    GFX_CUDA(cudaMemcpyAsync(dbuf, hbuf, 256ull << 20, cudaMemcpyHostToDevice, copy_));
+            }
             GFX_CUDA(cudaEventRecord(e0, compute_));
             for (int r = 0; r < repeat; ++r) {
                 f.epoch = fwd_epoch_++;
+                if (rmode == 1) {
+                    GFX_CUDA(cudaEventRecord(cev, copy_));
+                    GFX_CUDA(cudaStreamWaitEvent(compute_, cev, 0));
+                }
+                if (rmode == 4) {  // serial copy -> forward through a cross-stream dependency (a miss)
+                    GFX_CUDA(cudaStreamWaitEvent(copy_, kev, 0));
+                    GFX_CUDA(cudaMemcpyAsync(dbuf, hbuf, 1u << 20, cudaMemcpyHostToDevice, copy_));
+                    GFX_CUDA(cudaEventRecord(cev, copy_));
+                    GFX_CUDA(cudaStreamWaitEvent(compute_, cev, 0));
+                }
+                if (rmode == 5)  // the same copy on the compute stream itself
+                    GFX_CUDA(cudaMemcpyAsync(dbuf, hbuf, 1u << 20, cudaMemcpyHostToDevice, compute_));
+                if (rmode == 2) GFX_CUDA(cudaEventRecord(ev[2 * r], compute_));
                 launch_mlp_forward(f, compute_);
+                if (rmode == 2) GFX_CUDA(cudaEventRecord(ev[2 * r + 1], compute_));
+                if (rmode == 4) GFX_CUDA(cudaEventRecord(kev, compute_));
             }
             GFX_CUDA(cudaEventRecord(e1, compute_));
             GFX_CUDA(cudaEventSynchronize(e1));
             float ms = 0;
             GFX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-            std::fprintf(stderr, "[repeat] model %d: %.2f us per forward (%d back-to-back launches)\n", model,
-                         1e3 * ms / repeat, repeat);
+            double inner = 0;
+            for (int r = 0; rmode == 2 && r < repeat; ++r) {
+                float x = 0;
+                GFX_CUDA(cudaEventElapsedTime(&x, ev[2 * r], ev[2 * r + 1]));
+                inner += x;
+            }
+            for (cudaEvent_t e : ev) cudaEventDestroy(e);
+            cudaEventDestroy(cev);
+            if (hbuf) {
+                GFX_CUDA(cudaStreamSynchronize(copy_));
+                GFX_CUDA(cudaFreeHost(hbuf));
+                GFX_CUDA(cudaFree(dbuf));
+            }
+            cudaEventDestroy(kev);
+            std::fprintf(stderr, "[repeat] model %d mode %d: %.2f us per forward (%d launches), bracketed %.2f us\n",
+                         model, rmode, 1e3 * ms / repeat, repeat, 1e3 * inner / repeat);
             GFX_CUDA(cudaEventDestroy(e0));
             GFX_CUDA(cudaEventDestroy(e1));
         }
