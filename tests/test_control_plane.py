@@ -268,3 +268,36 @@ def test_azure_ingest_at_scale(product, oracle, table1, tmp_path):
     assert a.log_digest == b.log_digest
     with pytest.raises(gfx.GfxError, match="Azure"):
         gfx.azure_trace_to_csv(os.path.join(simabi.GOLDEN, "trace_zipf.csv"), out)
+
+
+def test_scheduler_edge_cases_vs_oracle_and_reference(product, oracle):
+    """Edge cases of the request stream and cache: an empty stream,
+    one request, every request at the same instant (ties broken by id), a model
+    that exactly fills the cache, and a cache one model wide (every miss evicts
+    everything) — product, oracle and (where built) the compiled reference agree
+    decision for decision; a model larger than the cache is refused by all."""
+    cat = ("model_id,occupation_mb,load_time_s,infer_time_s\n"
+           "a,1000,1.1,0.6\nb,3000,1.7,0.4\nc,2000,2.3,0.9\n")
+    ref = simabi.load_ref() if os.path.exists(simabi.REF_SO) else None
+    cases = [
+        (np.zeros(0, np.int64), np.zeros(0, np.int32), 3000.0),                    # empty
+        (np.array([5], np.int64), np.array([1], np.int32), 3000.0),                # one request
+        (np.zeros(12, np.int64), np.array([0, 1, 2] * 4, np.int32), 3000.0),       # simultaneous
+        (np.arange(9, dtype=np.int64) * 100, np.array([1, 1, 0, 1, 2, 1, 0, 0, 1], np.int32), 3000.0),  # b fills it
+        (np.arange(10, dtype=np.int64) * 7, np.array([0, 1, 2, 1, 0, 2, 2, 1, 0, 1], np.int32), 3000.0),
+    ]
+    for arr, mi, cap in cases:
+        for pol in ("lb", "lalb", "lalbo3"):
+            for gpus in (1, 2):
+                cfg = simabi.make_config(gpus=gpus, capacity_mb=cap, policy=pol, o3_limit=2, debug_checks=True,
+                                         log_events=2)
+                a, b = oracle.run_stream(cat, cfg, mi, arr), product.run_stream(cat, cfg, mi, arr)
+                simabi.assert_same(a, b, f"{len(arr)} {pol} {gpus}")
+                assert a.log_digest == b.log_digest
+                if ref is not None:
+                    r = ref.run_stream(cat, cfg, mi, arr)
+                    simabi.assert_same(r, b, f"ref {len(arr)} {pol} {gpus}")
+    big = simabi.make_config(gpus=1, capacity_mb=2999.0)
+    for lib in [product, oracle] + ([ref] if ref is not None else []):
+        with pytest.raises(simabi.SimError, match="cannot fit"):
+            lib.run_stream(cat, big, np.array([1], np.int32), np.array([0], np.int64))
