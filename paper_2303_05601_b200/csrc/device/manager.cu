@@ -484,7 +484,10 @@ void GpuManager::infer(int model, const void* in_v, void* out_v, void* debug_hid
         f.opnd = fwd_opnd_;
         f.part = fwd_part_;
         f.cnt = fwd_cnt_;
-        f.grid = sm_count_;
+        static const bool use_cluster = std::getenv("GFX_MLP_CLUSTER") != nullptr;
+        static const int cluster_grid = use_cluster ? mlp_fwd_cluster_grid(8) : 0;
+        f.cluster = use_cluster ? 8 : 0;
+        f.grid = use_cluster ? cluster_grid : sm_count_;
         static const int ablate = std::getenv("GFX_MLP_ABLATE") ? std::atoi(std::getenv("GFX_MLP_ABLATE")) : 0;
         f.ablate = ablate;
         for (int l = 0; l < f.L; ++l) {
@@ -494,7 +497,7 @@ void GpuManager::infer(int model, const void* in_v, void* out_v, void* debug_hid
             ly.K = blob.desc.dims[l];
             ly.N = blob.desc.dims[l + 1];
             ly.tiles = (ly.N + kWTileRows - 1) / kWTileRows;
-            ly.splits = mlp_fwd_splits(ly.K, ly.N, f.grid);
+            ly.splits = mlp_fwd_splits(ly.K, ly.N, f.grid, f.cluster);
         }
         static const bool trace_on = std::getenv("GFX_TRACE_MLP") != nullptr;
         if (trace_on) {

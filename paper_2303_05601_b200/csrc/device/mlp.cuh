@@ -38,13 +38,15 @@ struct MlpFwdArgs {
     unsigned epoch;         // launch sequence number on this workspace (stream-ordered)
     int L;
     int grid;
+    int cluster;            // 0, or 8: split-K reduced through cluster DSMEM (GFX_MLP_CLUSTER=1)
     int ablate;             // debug bitmask (0 in production): 1 = W_hi taken as rn_tf32 instead of trunc
     unsigned long long* trace;  // debug (GFX_TRACE_MLP): [grid][32] %globaltimer marks, else nullptr
     MlpFwdLayer layer[GFX_MAX_LAYERS];
     PageTable pt;
 };
 
-int mlp_fwd_splits(int K, int N, int grid);
+int mlp_fwd_splits(int K, int N, int grid, int cluster = 0);
+int mlp_fwd_cluster_grid(int cluster);
 size_t mlp_fwd_smem();
 void launch_mlp_forward(MlpFwdArgs& a, cudaStream_t stream);
 // Debug timeline (GFX_TRACE_MLP): buffer size in 64-bit words and the stderr report.

@@ -165,13 +165,22 @@ struct Unit {
     bool valid;
     int tile, split, kt0, nkt, kt_total;
 };
-__device__ __forceinline__ Unit unit_of(const MlpFwdLayer& ly, int cta) {
+__device__ __forceinline__ Unit unit_of(const MlpFwdLayer& ly, int cta, int cluster) {
     Unit u{};
-    const int units = ly.tiles * ly.splits;
-    u.valid = cta < units;
+    if (cluster) {
+        // Cluster mode: the S splits of a tile are adjacent ranks of one cluster
+        // (S divides the cluster size), cluster c holds tiles c * (cluster / S) + ...
+        const int per = cluster / ly.splits, rank = cta % cluster, lt = rank / ly.splits;
+        u.tile = (cta / cluster) * per + lt;
+        u.split = rank % ly.splits;
+        u.valid = u.tile < ly.tiles;
+    } else {
+        const int units = ly.tiles * ly.splits;
+        u.valid = cta < units;
+        u.tile = cta % ly.tiles;
+        u.split = cta / ly.tiles;
+    }
     if (!u.valid) return u;
-    u.tile = cta % ly.tiles;
-    u.split = cta / ly.tiles;
     u.kt_total = ly.K / kTileK;
     u.kt0 = static_cast<int>((static_cast<long long>(u.kt_total) * u.split) / ly.splits);
     const int kt1 = static_cast<int>((static_cast<long long>(u.kt_total) * (u.split + 1)) / ly.splits);
@@ -186,7 +195,7 @@ struct WIter {
 };
 __device__ __forceinline__ bool witer_seek(const MlpFwdArgs& a, int cta, WIter& w) {
     for (; w.l < a.L; ++w.l) {
-        w.u = unit_of(a.layer[w.l], cta);
+        w.u = unit_of(a.layer[w.l], cta, a.cluster);
         if (w.u.valid) {
             w.it = 0;
             return true;
@@ -216,6 +225,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     __shared__ uint32_t tmem_base_s;
     __shared__ uint32_t pt[GFX_MAX_PAGES];
     __shared__ float red[2][4];
+    // Cluster mode: split-K partials arrive by st.async into the gather area
+    // (two 16 KB parities), completing rbar[parity]; consumed[parity] = the last
+    // layer whose partials this CTA has read from that parity (senders poll it).
+    __shared__ __align__(8) uint64_t rbar[2];
+    __shared__ int consumed[2];
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
@@ -241,12 +255,17 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&tfull[b], 1);
             mbar_init(&tempty[b], 4);  // one arrival per drain warp
         }
+        mbar_init(&rbar[0], 1);
+        mbar_init(&rbar[1], 1);
+        consumed[0] = -2;
+        consumed[1] = -1;
         mbar_fence_init();
         tma_prefetch_desc(&a.tmap_in);
     }
     if (warp == 1) tmem_alloc<kTmemCols>(&tmem_base_s);
     tc_fence_before();
     __syncthreads();
+    if (a.cluster) cluster_sync();  // every CTA's barriers exist before any remote access
     tc_fence_after();
     const uint32_t tmem = tmem_base_s;
     if (tid == 0) mark(a.trace, 1);
@@ -286,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         Prof pr;
         for (int l = 0; l < L; ++l) {
             const MlpFwdLayer& ly = a.layer[l];
-            const Unit u = unit_of(ly, cta);
+            const Unit u = unit_of(ly, cta, a.cluster);
             if (!u.valid) continue;
             if (l == 0 && lane == 0) {
                 const int pre = u.nkt < kSlots ? u.nkt : kSlots;
@@ -371,7 +390,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         Prof pr;
         pr.start();
         for (int l = 0; l < L; ++l) {
-            const Unit u = unit_of(a.layer[l], cta);
+            const Unit u = unit_of(a.layer[l], cta, a.cluster);
             if (!u.valid) continue;
             for (int c0 = 0; c0 < u.nkt; c0 += kChunk, ++chunk) {
                 const int len = u.nkt - c0 < kChunk ? u.nkt - c0 : kChunk;
@@ -425,7 +444,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         Prof pr;
         pr.start();
         for (int l = 0; l < L; ++l) {
-            const Unit u = unit_of(a.layer[l], cta);
+            const Unit u = unit_of(a.layer[l], cta, a.cluster);
             if (!u.valid) continue;
             for (int it = 0; it < u.nkt; ++it, ++step) {
                 if ((step & 1) != group) continue;
@@ -477,11 +496,19 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int i = cta * 128 + ct; i < kCntBank; i += gridDim.x * 128) other[i] = 0;
         }
         int chunk = 0;
+        uint32_t rph = 0;  // rbar phase bits (cluster mode)
         long long pd[2] = {0, 0};
         Prof pr;
+        auto mark_consumed = [&](int l) {  // cluster mode: parity l & 1 of this CTA's buffer is free again
+            if (a.cluster && ct == 0) {
+                asm volatile("fence.acq_rel.cluster;\n" ::: "memory");
+                *reinterpret_cast<volatile int*>(&consumed[l & 1]) = l;
+            }
+        };
         for (int l = 0; l < L; ++l) {
             const MlpFwdLayer& ly = a.layer[l];
-            const Unit u = unit_of(ly, cta);
+            const Unit u = unit_of(ly, cta, a.cluster);
+            if (!u.valid || ly.splits == 1) mark_consumed(l);  // nobody sends this CTA partials of layer l
             if (!u.valid) continue;
             pr.start();
             const bool last = l == L - 1;
@@ -529,6 +556,46 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (S == 1) {
 #pragma unroll
                 for (int b = 0; b < kRows; ++b) emit(b, acc[b]);
+            } else if (a.cluster) {
+                // The tile's S splits are cluster ranks base .. base + S - 1; split o
+                // owns rows b = o (mod S). Every split st.asyncs its partial rows into
+                // the owner's receive buffer [src split][row / S][feature] (a warp's
+                // 32 features of a row = 128 contiguous bytes), completing the
+                // owner's rbar; the owner sums in split order. No global round trip.
+                const int par = l & 1, per = kRows / S;
+                const int base = cta % a.cluster - u.split;
+                float* rb = reinterpret_cast<float*>(smem + kSlots * kSlotBytes) + par * (kRows * kTileM);
+                if (ct < S) {  // the destination's parity buffer was read for layer l - 2
+                    const uint32_t ra = mapa_u32(&consumed[par], static_cast<uint32_t>(base + ct));
+                    while (ld_acquire_cluster_s32(ra) < l - 2) {
+                    }
+                }
+                epi_sync();
+                if (ct == 0) {
+                    if (l == 0) mark(a.trace, 18);
+                    mbar_arrive_expect_tx(&rbar[par], kRows * kTileM * 4);
+                }
+                const uint32_t rb_mine = smem_u32(rb) + static_cast<uint32_t>((u.split * per * kTileM + fl) * 4);
+#pragma unroll
+                for (int b = 0; b < kRows; ++b) {
+                    const int o = b % S, jj = b / S;
+                    const uint32_t rank = static_cast<uint32_t>(base + o);
+                    uint32_t dst, mb;
+                    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(dst) : "r"(rb_mine + jj * kTileM * 4), "r"(rank));
+                    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(mb) : "r"(smem_u32(&rbar[par])), "r"(rank));
+                    st_async_f32(dst, acc[b], mb);
+                }
+                mbar_wait(&rbar[par], (rph >> par) & 1u);
+                rph ^= 1u << par;
+                if (ct == 0 && l < 2) mark(a.trace, 26 + 2 * l);
+                for (int jj = 0; jj < per; ++jj) {
+                    float v = 0.f;
+                    for (int sp = 0; sp < S; ++sp) v += rb[(sp * per + jj) * kTileM + fl];
+                    emit(u.split + jj * S, v);
+                }
+                epi_sync();  // every thread has read the buffer
+                mark_consumed(l);
+                if (ct == 0 && l < 2) mark(a.trace, 27 + 2 * l);
             } else {
                 // Publish this unit's partial [32][128], wait for the tile's
                 // siblings (co-resident: cooperative launch), reduce rows
@@ -642,6 +709,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     tc_fence_before();
     __syncthreads();
+    if (a.cluster) cluster_sync();  // no CTA leaves while a peer may still write into its smem
     tc_fence_after();
     if (tid == 0) mark(a.trace, 31);
     if (warp == 1) tmem_dealloc<kTmemCols>(tmem);
@@ -649,13 +717,38 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 }  // namespace
 
-int mlp_fwd_splits(int K, int N, int grid) {
+int mlp_fwd_splits(int K, int N, int grid, int cluster) {
     const int tiles = (N + kTileM - 1) / kTileM;
     const int kt = K / kTileK;
+    if (cluster) {  // the largest S dividing the cluster whose tiles fit the co-resident clusters
+        for (int s = cluster; s > 1; s >>= 1)
+            if (s <= kt && (tiles + cluster / s - 1) / (cluster / s) <= grid / cluster) return s;
+        return 1;
+    }
     int s = grid / tiles;
     if (s > kt) s = kt;
     if (s > kRows) s = kRows;
     return s < 1 ? 1 : s;
+}
+
+int mlp_fwd_cluster_grid(int cluster) {
+    // Co-resident CTAs when launched in clusters of `cluster` (one CTA per SM).
+    const size_t smem = mlp_fwd_smem();
+    GFX_CUDA(cudaFuncSetAttribute(mlp_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(cluster));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = static_cast<unsigned>(cluster);
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    GFX_CUDA(cudaOccupancyMaxActiveClusters(&n, mlp_forward_kernel, &cfg));
+    return n * cluster;
 }
 
 size_t mlp_trace_words(int grid) { return static_cast<size_t>(48) * grid + 576; }
@@ -728,6 +821,9 @@ void launch_mlp_forward(MlpFwdArgs& a, cudaStream_t stream) {
         const MlpFwdLayer& ly = a.layer[l];
         if (ly.K % kTileK || ly.K > kMlpMaxDim || ly.N > kMlpMaxDim || ly.tiles > 64 || ly.tiles * ly.splits > a.grid)
             throw std::runtime_error("mlp forward: unsupported layer shape");
+        if (a.cluster && (a.cluster % ly.splits || (ly.tiles + a.cluster / ly.splits - 1) / (a.cluster / ly.splits) >
+                                                        a.grid / a.cluster))
+            throw std::runtime_error("mlp forward: layer does not fit the cluster map");
         if (l > 0 && a.layer[l - 1].N != ly.K) throw std::runtime_error("mlp forward: layer widths do not chain");
     }
     if (a.layer[a.L - 1].N > 2048 || a.grid < kRows) throw std::runtime_error("mlp forward: at most 2048 classes, grid >= 32");
@@ -747,12 +843,16 @@ void launch_mlp_forward(MlpFwdArgs& a, cudaStream_t stream) {
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeCooperative;  // every CTA co-resident: the dataflow waits need it
     attr[0].val.cooperative = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = static_cast<unsigned>(a.cluster ? a.cluster : 1);
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
     static const bool no_coop = std::getenv("GFX_MLP_NOCOOP") != nullptr;  // debug A/B
-    cfg.numAttrs = no_coop ? 0 : 1;
+    cfg.numAttrs = a.cluster ? 2 : (no_coop ? 0 : 1);
     GFX_CUDA(cudaLaunchKernelEx(&cfg, mlp_forward_kernel, a));
 }
 

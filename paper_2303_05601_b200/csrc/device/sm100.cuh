@@ -130,6 +130,23 @@ __device__ __forceinline__ void mbar_arrive_remote(uint64_t* bar, uint32_t rank)
         "r"(rank)
         : "memory");
 }
+// Address of `p`'s shared-memory offset in cluster CTA `rank` (shared::cluster window).
+__device__ __forceinline__ uint32_t mapa_u32(const void* p, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(smem_u32(p)), "r"(rank));
+    return r;
+}
+// 4-byte store into another cluster CTA's smem whose bytes complete_tx on that CTA's mbarrier.
+__device__ __forceinline__ void st_async_f32(uint32_t remote_addr, float v, uint32_t remote_mbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];\n" ::"r"(remote_addr),
+                 "r"(__float_as_uint(v)), "r"(remote_mbar)
+                 : "memory");
+}
+__device__ __forceinline__ int ld_acquire_cluster_s32(uint32_t remote_addr) {
+    int v;
+    asm volatile("ld.acquire.cluster.shared::cluster.b32 %0, [%1];\n" : "=r"(v) : "r"(remote_addr) : "memory");
+    return v;
+}
 __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
