@@ -512,7 +512,9 @@ void GpuManager::infer(int model, const void* in_v, void* out_v, void* debug_hid
             GFX_CUDA(cudaEventCreate(&e1));
             // GFX_MLP_REPEAT_MODE: 0 back-to-back; 1 each launch after a compute-stream
             // wait on an event of the copy stream (the replay's load dependency);
-            // 2 events around every launch (the replay's kernel timer), summed.
+            // 2 events around every launch (the replay's kernel timer), summed;
+            // 3 back-to-back under concurrent H2D; 4 / 5 a 1 MB H2D copy before
+            // every launch (cross-stream / same stream); 6 the copies alone.
             static const int rmode = std::getenv("GFX_MLP_REPEAT_MODE") ? std::atoi(std::getenv("GFX_MLP_REPEAT_MODE")) : 0;
             std::vector<cudaEvent_t> ev;
             if (rmode == 2)
@@ -529,7 +531,7 @@ void GpuManager::infer(int model, const void* in_v, void* out_v, void* debug_hid
             void* dbuf = nullptr;
             cudaEvent_t kev;  // modes 4/5: the previous forward's completion
             GFX_CUDA(cudaEventCreateWithFlags(&kev, cudaEventDisableTiming));
-            if (rmode == 4 || rmode == 5) {
+            if (rmode == 4 || rmode == 5 || rmode == 6) {
                 GFX_CUDA(cudaHostAlloc(&hbuf, 1u << 20, cudaHostAllocDefault));
                 GFX_CUDA(cudaMalloc(&dbuf, 1u << 20));
             }
@@ -552,8 +554,9 @@ void GpuManager::infer(int model, const void* in_v, void* out_v, void* debug_hid
                     GFX_CUDA(cudaEventRecord(cev, copy_));
                     GFX_CUDA(cudaStreamWaitEvent(compute_, cev, 0));
                 }
-                if (rmode == 5)  // the same copy on the compute stream itself
+                if (rmode == 5 || rmode == 6)  // the same copy on the compute stream itself (6: copy only)
                     GFX_CUDA(cudaMemcpyAsync(dbuf, hbuf, 1u << 20, cudaMemcpyHostToDevice, compute_));
+                if (rmode == 6) continue;
                 if (rmode == 2) GFX_CUDA(cudaEventRecord(ev[2 * r], compute_));
                 launch_mlp_forward(f, compute_);
                 if (rmode == 2) GFX_CUDA(cudaEventRecord(ev[2 * r + 1], compute_));
