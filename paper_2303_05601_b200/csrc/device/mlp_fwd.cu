@@ -315,7 +315,35 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tma_tile2d_g2s(xs + kXBytes / 2, &a.tmap_in, (u.kt0 + it) * kTileK, 0, &raw_full[it]);
                 }
             }
-            int ready_src = -1;  // last source tile known complete
+            if (l > 0) {
+                // Two lanes issue alternate steps, each its own loop (a thread's TMA
+                // requests are served one after another, ~500 cycles each: one lane
+                // alone capped the post-boundary step rate at ~0.43 µs). Each lane
+                // polls the dataflow counter of a source tile the first time one of
+                // its steps needs it.
+                const int step0 = step;
+                if (lane < 2) {
+                    int ready_src = -1;  // last source tile this lane knows complete
+                    for (int it = lane; it < u.nkt; it += 2) {
+                        const int st = step0 + it, s = st % kSlots, kt = u.kt0 + it;
+                        if (st >= kSlots) mbar_wait(&step_done[s], ((st / kSlots) & 1) ^ 1);
+                        const int src = kt >> 2;  // the previous layer's feature tile holding these 32 inputs
+                        if (src != ready_src) {
+                            wait_count(cnt + kCntDone + (l - 1) * 64 + src, static_cast<unsigned>(a.layer[l - 1].splits));
+                            fence_proxy_async_global();
+                            ready_src = src;
+                        }
+                        smark(a.trace, st, 1);
+                        mbar_arrive_expect_tx(&ready[s], kXBytes);
+                        tma_bulk_g2s(smem + s * kSlotBytes + kWBytes,
+                                     a.opnd + static_cast<size_t>(l) * kMlpOpndLayerBytes + static_cast<size_t>(kt) * kXBytes,
+                                     kXBytes, &ready[s]);
+                    }
+                }
+                __syncwarp();
+                step = step0 + u.nkt;
+                continue;
+            }
             for (int it = 0; it < u.nkt; ++it, ++step) {
                 const int s = step % kSlots;
                 const int kt = u.kt0 + it;
@@ -354,20 +382,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     continue;
                 }
-                if (lane == 0) {
-                    const int src = kt >> 2;  // the previous layer's feature tile holding these 32 inputs
-                    if (src != ready_src) {
-                        wait_count(cnt + kCntDone + (l - 1) * 64 + src, static_cast<unsigned>(a.layer[l - 1].splits));
-                        fence_proxy_async_global();
-                        ready_src = src;
-                        pr.stop(px[1]);
-                    }
-                    smark(a.trace, step, 1);
-                    mbar_arrive_expect_tx(&ready[s], kXBytes);
-                    tma_bulk_g2s(xs, a.opnd + static_cast<size_t>(l) * kMlpOpndLayerBytes + static_cast<size_t>(kt) * kXBytes,
-                                 kXBytes, &ready[s]);
-                }
-                __syncwarp();
             }
         }
         if (lane == 0) {
