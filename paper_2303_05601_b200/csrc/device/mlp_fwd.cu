@@ -307,14 +307,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             const MlpFwdLayer& ly = a.layer[l];
             const Unit u = unit_of(ly, cta, a.cluster);
             if (!u.valid) continue;
-            if (l == 0 && lane == 0) {
-                const int pre = u.nkt < kSlots ? u.nkt : kSlots;
-                for (int it = 0; it < pre; ++it) {
-                    uint8_t* xs = smem + it * kSlotBytes + kWBytes;
-                    mbar_arrive_expect_tx(&raw_full[it], kXBytes / 2);
-                    tma_tile2d_g2s(xs + kXBytes / 2, &a.tmap_in, (u.kt0 + it) * kTileK, 0, &raw_full[it]);
-                }
+            if (l == 0 && lane < (u.nkt < kSlots ? u.nkt : kSlots)) {
+                // one lane per tile: a thread's TMA requests are served one after another
+                const int it = lane;
+                uint8_t* xs = smem + it * kSlotBytes + kWBytes;
+                mbar_arrive_expect_tx(&raw_full[it], kXBytes / 2);
+                tma_tile2d_g2s(xs + kXBytes / 2, &a.tmap_in, (u.kt0 + it) * kTileK, 0, &raw_full[it]);
             }
+            __syncwarp();
             if (l > 0) {
                 // Two lanes issue alternate steps, each its own loop (a thread's TMA
                 // requests are served one after another, ~500 cycles each: one lane
