@@ -358,6 +358,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     __syncwarp();
                     mbar_wait(&raw_full[s], (it / kSlots) & 1);
+                    if (lane == 0) smark(a.trace, step, 6);
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
                         float4* p = reinterpret_cast<float4*>(xs + sw128(kRows + lane, 4 * j));
@@ -799,13 +800,13 @@ void mlp_trace_report(const std::vector<unsigned long long>& tr, int grid, int L
         std::fprintf(stderr, "  %-16s n=%3zu %8.2f %8.2f %8.2f\n", nm, v.size(), v.front(), v[v.size() / 2],
                      v.back());
     }
-    std::fprintf(stderr, "  CTA 0 steps (us): Wreq Xreq Wlanded WloDone xFull mmaIssued\n");
+    std::fprintf(stderr, "  CTA 0 steps (us): Wreq Xreq Wlanded WloDone xFull mmaIssued rawLanded\n");
     for (int st = 0; st < 64; ++st) {
         const unsigned long long* p = tr.data() + nct + st * 8;
         if (!p[0] && !p[5]) break;
         auto us = [&](unsigned long long t) { return t ? (t - t0) * 1e-3 : -1.0; };
-        std::fprintf(stderr, "   %2d %7.2f %7.2f %7.2f %7.2f %7.2f %7.2f\n", st, us(p[0]), us(p[1]), us(p[2]),
-                     us(p[3]), us(p[4]), us(p[5]));
+        std::fprintf(stderr, "   %2d %7.2f %7.2f %7.2f %7.2f %7.2f %7.2f %7.2f\n", st, us(p[0]), us(p[1]), us(p[2]),
+                     us(p[3]), us(p[4]), us(p[5]), us(p[6]));
     }
     static const char* pn[16] = {"mma: wait tempty", "mma: wait ready", "", "",
                                  "mma: commits+rest", "conv: wait w_full", "", "conv: work",
