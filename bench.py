@@ -562,7 +562,27 @@ def c5_extras(gfx, world, peaks, peak_kind):
                       "infer_ms_per_request": round(r.kernel_ms / max(1, r.n_requests), 4),
                       "tensor_tflops": round(tf, 1), "tensor_frac": round(tf / peak, 4),
                       "tensor_frac_sustained": round(tf / peak_sus, 4)})
-    return {"c5_bert_base_arena_sweep": {
+    # configs[4] at 8 GPUs, schedule level: the product's control plane (bit-exact
+    # with the reference) over the BERT catalog's B200-profiled times at rho_infer
+    # 0.6 (403k requests/min), per arena size: hit rate, false misses, latency.
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import simabi
+    plib = simabi.load_product()
+    rpm8 = int(round(0.6 * 60 * 8 / 0.000715))
+    fleet8 = {"gpus": 8, "rpm": rpm8, "note": "control plane only (no device work): 8 simulated GPUs, ws 20, 1 min, "
+                                              "catalog load 3.44 ms / infer 0.715 ms per request"}
+    for arena in (256, 512, 1024, 2048, 4096):
+        row = {}
+        for pol in ("lb", "lalbo3"):
+            r = plib.run(cat, simabi.make_config(gpus=8, capacity_mb=float(arena), policy=pol, working_set=20, rpm=rpm8,
+                                                 minutes=1))
+            c, n = r.counts(), len(r.arrival)
+            row[pol] = {"hit_rate": round(c["hits"] / n, 4), "false_misses": int(c["false_misses"]),
+                        "avg_latency_ms": round(r.report["avg_latency_s"] * 1e3, 3),
+                        "p99_latency_ms": round(r.percentile_s(99) * 1e3, 3)}
+        fleet8[f"arena_{arena}"] = row
+    out_c5 = {"c5_fleet8_schedule_sweep": fleet8}
+    return {**out_c5, "c5_bert_base_arena_sweep": {
         "workload": "C5: 20 BERT-base bf16 encoders (12x768, ffn 3072), 32x128 tokens/request, ws 20, "
                     "325 rpm x 1 min, LALBO3, 1 GPU", "requests": int(rs[-1].n_requests),
         "tensor_peak_tflops": peak, "tensor_peak_sustained_tflops": peak_sus,

@@ -301,3 +301,27 @@ def test_scheduler_edge_cases_vs_oracle_and_reference(product, oracle):
     for lib in [product, oracle] + ([ref] if ref is not None else []):
         with pytest.raises(simabi.SimError, match="cannot fit"):
             lib.run_stream(cat, big, np.array([1], np.int32), np.array([0], np.int64))
+
+
+def test_c5_fleet8_arena_sweep_schedule(product, oracle):
+    """configs[4] (C5) at 8 GPUs, schedule level, on the BERT catalog: product
+    and oracle agree at a reduced rate; at the full rho = 0.6 rate the hit rate
+    of LALBO3 rises with the arena and stays above LB's at every size."""
+    import paper_2303_05601_b200 as gfx
+    cat = gfx.catalog_text("bert_c5")
+    cfg = simabi.make_config(gpus=8, capacity_mb=512.0, policy="lalbo3", working_set=20, rpm=20000, minutes=1,
+                             log_events=2)
+    a, b = oracle.run(cat, cfg), product.run(cat, cfg)
+    simabi.assert_same(a, b, "c5 fleet8")
+    assert a.log_digest == b.log_digest
+    rpm8 = int(round(0.6 * 60 * 8 / 0.000715))
+    prev = -1.0
+    for arena in (256, 512, 1024, 2048):
+        hr = {}
+        for pol in ("lb", "lalbo3"):
+            r = product.run(cat, simabi.make_config(gpus=8, capacity_mb=float(arena), policy=pol, working_set=20,
+                                                    rpm=rpm8, minutes=1))
+            hr[pol] = r.counts()["hits"] / len(r.arrival)
+        assert hr["lalbo3"] > hr["lb"]
+        assert hr["lalbo3"] >= prev
+        prev = hr["lalbo3"]
