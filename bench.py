@@ -237,6 +237,12 @@ def main():
     cfg = gfx.sim_config(gpus=G, capacity_mb=204.0, policy=a.policy, rpm=325 * G)
     only = rank if world > 1 else -1
     ndev = 1 if world == 1 and G == 1 else G
+    emulated = False
+    if world > 1:
+        n = C.c_int(0)
+        gfx.check(gfx._ffi.gfx_device_count(C.byref(n)))
+        if n.value < G:  # fewer devices than ranks: every rank on device 0 (CUDA IPC still crosses processes)
+            ndev, emulated = 1, True
     if world == 1 and G > 1:
         ndev = G  # single process driving G devices
     p2p = G > 1  # false misses fetch from the lowest-id holder over NVLink (in-process or CUDA IPC)
@@ -323,7 +329,7 @@ def main():
                                "working set 15, 325 req/min x 6 min x N GPUs), 22 Table-I ids as fp32 MLPs "
                                "1024-h-h-h-1000 (32-99 MiB), 204 MiB paged HBM arena per GPU",
                    "policy": a.policy, "o3_limit": 25, "requests_per_step": n, "batch": 32,
-                   "parallelism": f"request-dp{G}", "l2": "inputs larger than L2 (250 MB of request inputs, "
+                   "parallelism": f"request-dp{G}" + (" (ranks emulated on one device)" if emulated else ""), "l2": "inputs larger than L2 (250 MB of request inputs, "
                    f"{r.h2d_bytes / 1e9:.0f} GB of model weights streamed per step; arena starts empty each step)"},
         "p50_latency_ms": round(r.sim_p50_s * 1e3, 4), "p99_latency_ms": round(r.sim_p99_s * 1e3, 4),
         "latency_note": "virtual-time latency of the bit-exact schedule under the B200-profiled catalog at the "
