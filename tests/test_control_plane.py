@@ -325,3 +325,38 @@ def test_c5_fleet8_arena_sweep_schedule(product, oracle):
         assert hr["lalbo3"] > hr["lb"]
         assert hr["lalbo3"] >= prev
         prev = hr["lalbo3"]
+
+
+def test_random_catalogs_and_configs_vs_oracle_and_reference(product, oracle):
+    """Property check over random catalogs (3-8 models, random footprints and
+    service times), fleets (1-5 GPUs, capacities from one model to all of them),
+    policies, O3 limits, the pipelined mode and bursty streams: product ==
+    oracle decision for decision (and == the compiled reference where built, for
+    the reference semantics)."""
+    from hypothesis import HealthCheck, given, settings
+    from hypothesis import strategies as st
+
+    ref = simabi.load_ref() if os.path.exists(simabi.REF_SO) else None
+
+    @settings(max_examples=150, deadline=None, derandomize=True, suppress_health_check=list(HealthCheck))
+    @given(st.data())
+    def check(data):
+        n_models = data.draw(st.integers(3, 8))
+        occ = [data.draw(st.integers(100, 4000)) for _ in range(n_models)]
+        rows = [f"m{i},{occ[i]},{data.draw(st.integers(1, 500)) / 100:.2f},{data.draw(st.integers(1, 300)) / 100:.2f}"
+                for i in range(n_models)]
+        cat = "model_id,occupation_mb,load_time_s,infer_time_s\n" + "\n".join(rows) + "\n"
+        cap = float(data.draw(st.integers(max(occ), sum(occ) + 1)))
+        n = data.draw(st.integers(0, 60))
+        arr = np.cumsum(np.array([data.draw(st.integers(0, 3_000_000)) for _ in range(n)], np.int64))
+        mi = np.array([data.draw(st.integers(0, n_models - 1)) for _ in range(n)], np.int32)
+        pol = data.draw(st.sampled_from(["lb", "lalb", "lalbo3"]))
+        pipe = data.draw(st.booleans())
+        cfg = simabi.make_config(gpus=data.draw(st.integers(1, 5)), capacity_mb=cap, policy=pol,
+                                 o3_limit=data.draw(st.integers(0, 5)), debug_checks=True, pipeline=pipe)
+        a, b = oracle.run_stream(cat, cfg, mi, arr), product.run_stream(cat, cfg, mi, arr)
+        simabi.assert_same(a, b, "random")
+        if ref is not None and not pipe:
+            simabi.assert_same(ref.run_stream(cat, cfg, mi, arr), b, "random vs reference")
+
+    check()
