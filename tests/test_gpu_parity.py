@@ -264,3 +264,36 @@ def test_cluster_dsmem_variant():
     r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider"] + tests,
                        env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+def test_mlp_random_shapes(gfx, olib):
+    """Twelve seeded random MLPs (1-6 layers, widths 32-4096 in steps of 32, any
+    number of classes divisible by 4): every tile / split / boundary pattern the
+    one-launch forward derives from them matches the oracle's fp64 forward."""
+    import ctypes as C
+    rng = np.random.default_rng(2303)
+    for case in range(12):
+        L = int(rng.integers(1, 7))
+        dims = [int(rng.integers(1, 129)) * 32 for _ in range(L)] + [int(rng.integers(1, 513)) * 4]
+        spec = gfx.ModelSpec(f"rand-{case}-" + "x".join(map(str, dims)), "mlp", dims, 0, 0)
+        idx = 51
+        gfx.check(gfx._ffi.gfx_model_register(idx, C.byref(spec.desc())))
+        pages = C.c_int32()
+        gfx.check(gfx._ffi.gfx_model_pages(idx, C.byref(pages)))
+        a = C.c_void_p()
+        gfx.check(gfx._ffi.gfx_arena_create(0, C.c_uint64((pages.value + 2) << 21), C.byref(a)))
+        try:
+            x, y = C.c_void_p(), C.c_void_p()
+            gfx.check(gfx._ffi.gfx_device_alloc(a, 32 * dims[0] * 4, C.byref(x)))
+            gfx.check(gfx._ffi.gfx_device_alloc(a, 2 * 32 * dims[-1] * 4, C.byref(y)))
+            gfx.check(gfx._ffi.gfx_load_h2d(a, idx, None))
+            rid = 9000 + case
+            gfx.check(gfx._ffi.gfx_fill_params(a, x, 32 * dims[0], gfx._ffi.gfx_input_seed(rid), 0xFFFFFFFF, 1.0))
+            gfx.check(gfx._ffi.gfx_infer(a, idx, x, y, 32, None))
+            got = np.zeros((2, 32, dims[-1]), np.float32)
+            gfx.check(gfx._ffi.gfx_memcpy_d2h(a, got.ctypes.data, y, got.nbytes))
+            _, lo, pr = oracle_forward(olib, gfx, spec, rid)
+            assert rel(got[0], lo) <= TOL, dims
+            assert rel(got[1], pr) <= TOL, dims
+        finally:
+            gfx._ffi.gfx_arena_destroy(a)
