@@ -18,21 +18,30 @@ CXXFLAGS := -std=c++20 -O2 -fPIC -ffp-contract=off -Wall -Wextra $(INC) -I$(CUDA
 NVFLAGS  := -std=c++20 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -ffp-contract=off \
             --expt-relaxed-constexpr -Xptxas -v $(INC)
 
+ifeq ($(K1_DEBUG),1)
+NVFLAGS += -DGFX_K1_DEBUG $(K1_EXTRA)   # K1 wait watchdogs + phase marks (debug only, never shipped)
+endif
+
 HOST_SRCS := $(wildcard $(PKG)/csrc/host/*.cpp) $(wildcard $(PKG)/csrc/capi/*.cpp)
 CU_SRCS   := $(wildcard $(PKG)/csrc/device/*.cu) $(wildcard $(PKG)/csrc/capi/*.cu)
 HOST_OBJS := $(patsubst $(PKG)/csrc/%.cpp,$(OBJ)/%.o,$(HOST_SRCS))
 CU_OBJS   := $(patsubst $(PKG)/csrc/%.cu,$(OBJ)/%.cu.o,$(CU_SRCS))
 HDRS      := $(wildcard include/*.h include/gpufaas/*.hpp $(PKG)/csrc/*/*.hpp $(PKG)/csrc/*/*.cuh)
 
-.PHONY: all product oracle ref clean
+.PHONY: all product oracle ref clean FORCE
 all: product
 product: $(OUT)/libgpufaas_b200.so
 
-$(OBJ)/%.o: $(PKG)/csrc/%.cpp $(HDRS)
+# Rebuild everything when the compiler flags change (e.g. K1_DEBUG=1 <-> release).
+$(OBJ)/.flags: FORCE
+	@mkdir -p $(OBJ)
+	@echo '$(NVFLAGS) $(CXXFLAGS)' | cmp -s - $@ || echo '$(NVFLAGS) $(CXXFLAGS)' > $@
+
+$(OBJ)/%.o: $(PKG)/csrc/%.cpp $(HDRS) $(OBJ)/.flags
 	@mkdir -p $(dir $@)
 	$(CXX) $(CXXFLAGS) -c $< -o $@
 
-$(OBJ)/%.cu.o: $(PKG)/csrc/%.cu $(HDRS)
+$(OBJ)/%.cu.o: $(PKG)/csrc/%.cu $(HDRS) $(OBJ)/.flags
 	@mkdir -p $(dir $@)
 	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $@.ptxas.txt || (cat $@.ptxas.txt; false)
 

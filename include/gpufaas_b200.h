@@ -133,6 +133,9 @@ int gfx_arena_create(int dev, uint64_t capacity_bytes, gfx_arena_t* out);
 int gfx_arena_destroy(gfx_arena_t a);
 int gfx_arena_reset(gfx_arena_t a); /* synchronise, evict everything */
 int gfx_arena_free_pages(gfx_arena_t a, int32_t* out);
+/* Explicit manager options (no environment switches on the product path). */
+#define GFX_OPT_GEMM_PAIR 1 /* BERT GEMMs on 2-SM (cta_group::2) tiles where the shape allows; default 0 */
+int gfx_arena_set_option(gfx_arena_t a, int32_t option, int32_t value);
 int gfx_arena_resident(gfx_arena_t a, int model_idx, int32_t* out);
 
 /* Cache operations. Each is asynchronous on the manager's streams; `done`
@@ -148,6 +151,13 @@ int gfx_infer(gfx_arena_t a, int model_idx, const void* in, void* out, int batch
 /* Test/debug: BERT inference that also copies every layer's hidden state into
  * hidden ([L+1][batch*seq][d] bf16, device) for teacher-forced parity checks. */
 int gfx_infer_debug(gfx_arena_t a, int model_idx, const void* in, void* out, int batch, void* hidden);
+
+/* Test/debug: one encoder GEMM of a resident BERT model with its fused epilogue,
+ * on `tokens` rows (bf16, device pointers). op 0: QKV (+bias) [tokens x 3d];
+ * 1: attention output (+bias, +resid) [tokens x d]; 2: FFN1 (+bias, GELU)
+ * [tokens x ffn]; 3: FFN2 (+bias, +resid) [tokens x d]. Synchronous. */
+int gfx_bert_gemm(gfx_arena_t a, int model_idx, int layer, int op, const void* x, const void* resid, void* y,
+                  int tokens);
 
 int gfx_event_query(gfx_event_t e); /* 0 done, 1 pending */
 int gfx_event_sync(gfx_event_t e);

@@ -694,6 +694,13 @@ int gfx_arena_reset(gfx_arena_t a) {
 int gfx_arena_free_pages(gfx_arena_t a, int32_t* out) {
     return guarded([&] { *out = static_cast<int32_t>(a->mgr->free_pages()); });
 }
+int gfx_arena_set_option(gfx_arena_t a, int32_t option, int32_t value) {
+    return guarded([&] {
+        if (option != GFX_OPT_GEMM_PAIR || (value != 0 && value != 1))
+            throw std::invalid_argument("unknown arena option or value");
+        a->mgr->set_gemm_pair(value != 0);
+    });
+}
 int gfx_arena_resident(gfx_arena_t a, int model_idx, int32_t* out) {
     return guarded([&] { *out = a->mgr->resident(model_idx) ? 1 : 0; });
 }
@@ -738,6 +745,14 @@ int gfx_infer_debug(gfx_arena_t a, int model_idx, const void* in, void* out, int
         if (b.desc.family != GFX_MODEL_BERT) throw std::invalid_argument("gfx_infer_debug: BERT models only");
         if (batch != b.desc.batch) throw std::invalid_argument("batch does not match the registered model");
         a->mgr->infer(model_idx, in, out, hidden);
+        GFX_CUDA(cudaStreamSynchronize(a->mgr->compute_stream()));
+    });
+}
+
+int gfx_bert_gemm(gfx_arena_t a, int model_idx, int layer, int op, const void* x, const void* resid, void* y,
+                  int tokens) {
+    return guarded([&] {
+        a->mgr->bert_gemm(model_idx, layer, op, x, resid, y, tokens);
         GFX_CUDA(cudaStreamSynchronize(a->mgr->compute_stream()));
     });
 }

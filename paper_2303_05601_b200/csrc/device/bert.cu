@@ -57,7 +57,6 @@ constexpr uint32_t kGSmem = 192 * 1024;  // stage ring budget
 enum Epi : int { kEpiBias = 0, kEpiGelu = 1, kEpiResid = 2 };
 
 struct GemmArgs {
-    unsigned long long* trace;    // debug (GFX_TRACE_GEMM): [grid][16] %globaltimer marks, else nullptr
     const char* arena;
     uint64_t w_off, b_off;        // weight tiles, fp32 bias
     __nv_bfloat16* y;             // [T x N]
@@ -73,7 +72,7 @@ struct GemmArgs {
 // its own 128 rows of D for its own epilogue. Halving the per-CTA stage is the
 // point: 6 stages (1.6 µs of MMA work) instead of 4 (1.07 µs) cover the TMA
 // latency under load, which bounded the single-CTA MMA phase at ~78 % of
-// issue rate (GFX_TRACE_GEMM; multicasting B alone did not help).
+// issue rate (multicasting B alone did not help).
 // Barriers: every operand load of either CTA is a .cta_group::2 tensor TMA
 // whose bytes complete the EVEN CTA's full barrier (the even CTA's producers
 // expect both halves), so the issuer waits on one barrier — an earlier version
@@ -99,19 +98,6 @@ __global__ void __launch_bounds__(kGThreads, 1)
     __shared__ float bias_s[kBN];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    auto mark = [&](int i) {
-        if (a.trace == nullptr) return;
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-        a.trace[blockIdx.x * 16 + i] = t;
-    };
-    if (tid == 0) mark(0);
-    auto smark = [&](int g, int i) {  // per-stage timeline of CTAs 0 and 1 (GFX_TRACE_GEMM)
-        if (a.trace == nullptr || blockIdx.x > 1 || g >= 64) return;
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-        a.trace[static_cast<size_t>(gridDim.x) * 16 + blockIdx.x * 256 + g * 4 + i] = t;
-    };
     const int n_tiles = a.N / kBN, m_tiles = a.T / kGM;
     // Tile sequence of this CTA: single -> tiles t = blockIdx.x (step grid);
     // pair -> pair tiles t = cluster id (step clusters), rows 2*(t / n) + rank.
@@ -155,7 +141,6 @@ __global__ void __launch_bounds__(kGThreads, 1)
     if (kPair) cluster_sync();  // the peer's barriers exist before any remote arrive reaches them
     tc_fence_after();
     const uint32_t tmem = tmem_s;
-    if (tid == 0) mark(1);
 
     constexpr int kBTiles = static_cast<int>(kBBytes / kGATile);  // B tiles per stage and CTA
     if (warp == 0 || warp >= kGBWarp0) {
@@ -178,7 +163,6 @@ __global__ void __launch_bounds__(kGThreads, 1)
                         if (rank == 0) mbar_arrive_expect_tx(&full_bar[s], 2 * kGATile);
                         if (warp == 0) {
                             tma_tile2d_g2s_pair(st, &tmap_x, k * kGK, m0, &full_bar[s]);
-                            smark(g, 0);
                         } else {
                             const int bt = nb * (kBN / 128) + static_cast<int>(rank) * kBTiles + h;
                             const uint64_t v = a.w_off + (static_cast<uint64_t>(bt) * ktiles_row + k) * kGATile;
@@ -188,7 +172,6 @@ __global__ void __launch_bounds__(kGThreads, 1)
                     } else if (warp == 0) {
                         mbar_arrive_expect_tx(&full_bar[s], kGATile);
                         tma_tile2d_g2s(st, &tmap_x, k * kGK, m0, &full_bar[s]);
-                        smark(g, 0);
                     } else {
                         const int bt = nb * (kBN / 128) + h;
                         const uint64_t v = a.w_off + (static_cast<uint64_t>(bt) * ktiles_row + k) * kGATile;
@@ -212,10 +195,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
                 for (int k = 0; k < nk; ++k, ++g) {
                     const int s = g % kStages;
                     mbar_wait(&full_bar[s], (g / kStages) & 1);
-                    smark(g, 1);
-                    smark(g, 2);
                     tc_fence_after();
-                    if (g == 0) mark(2);
                     uint8_t* st = smem + static_cast<size_t>(s) * kStage;
 #pragma unroll
                     for (int kk = 0; kk < kGK / 16; ++kk) {  // K = 16 bf16 = 32 bytes per MMA
@@ -225,7 +205,6 @@ __global__ void __launch_bounds__(kGThreads, 1)
                         else
                             umma_f16(acc, ad, bd, idesc, (k | kk) ? 1u : 0u);
                     }
-                    smark(g, 3);
                     if (kPair)
                         umma_commit_pair_multicast(&empty_bar[s], 0x3);
                     else
@@ -235,7 +214,6 @@ __global__ void __launch_bounds__(kGThreads, 1)
                     umma_commit_pair_multicast(&tfull_bar[b], 0x3);
                 else
                     umma_commit(&tfull_bar[b]);
-                if (i < 4) mark(3 + i);  // last MMA of tile i issued
             }
         }
     } else {
@@ -259,7 +237,6 @@ __global__ void __launch_bounds__(kGThreads, 1)
             asm volatile("bar.sync 3, %0;\n" ::"r"(kGEpiWarps * 32) : "memory");
             mbar_wait(&tfull_bar[b], (i >> 1) & 1);
             tc_fence_after();
-            if (ct == 0 && i < 4) mark(7 + i);  // tile i accumulated
             if (t + t_step >= tiles) pdl_trigger();  // last tile: let the next kernel start
             const int r = q * 32 + lane;
 #pragma unroll 1
@@ -322,7 +299,6 @@ __global__ void __launch_bounds__(kGThreads, 1)
                 else
                     mbar_arrive(&tempty_bar[b]);
             }
-            if (ct == 0 && i < 4) mark(11 + i);  // tile i stored
         }
         if (ht == 0) bulk_wait_group<0>();  // every output box written before the CTA exits
     }
@@ -349,7 +325,7 @@ constexpr int kS = 128, kDh = 64;
 // K = 128: V is read MN-major straight from its token-major tile), O / sum.
 // Q, K, V arrive by three 2-D TMA boxes (64 dims x 128 tokens) from the fused
 // QKV activation. (The first version used warp-level mma.sync; 2.7 % of the
-// model's flops took 12 % of its time there.) Phase trace: GFX_TRACE_ATTN=1.
+// model's flops took 12 % of its time there.)
 constexpr uint32_t kAttnSmem = 3 * 16384 + 1024;  // Q, K, V; P overlays Q + K once S is computed
 
 __device__ __forceinline__ float ex2_approx(float x) {
@@ -359,15 +335,7 @@ __device__ __forceinline__ float ex2_approx(float x) {
 }
 
 __global__ void __launch_bounds__(128, 4) attention_tc_kernel(const __grid_constant__ CUtensorMap tmap_qkv,
-                                                           __nv_bfloat16* __restrict__ ctx, int heads,
-                                                           unsigned long long* trace) {
-    auto amark = [&](int i) {  // debug timeline (GFX_TRACE_ATTN)
-        if (trace == nullptr || threadIdx.x != 0) return;
-        unsigned long long t;
-        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-        trace[blockIdx.x * 8 + i] = t;
-    };
-    amark(0);
+                                                           __nv_bfloat16* __restrict__ ctx, int heads) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* qs = sm;
@@ -391,7 +359,6 @@ __global__ void __launch_bounds__(128, 4) attention_tc_kernel(const __grid_const
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_s;
-    amark(1);
     pdl_wait();
     if (tid == 0) {
         mbar_arrive_expect_tx(&ld_bar, 3 * 16384);
@@ -399,7 +366,6 @@ __global__ void __launch_bounds__(128, 4) attention_tc_kernel(const __grid_const
         tma_tile2d_g2s(ks, &tmap_qkv, d + h * kDh, seq * kS, &ld_bar);
         tma_tile2d_g2s(vs, &tmap_qkv, 2 * d + h * kDh, seq * kS, &ld_bar);
         mbar_wait(&ld_bar, 0);
-        amark(2);
         tc_fence_after();
         constexpr uint32_t idesc_s = umma_idesc<128, 128, 1>();  // bf16 x bf16 -> f32, both K-major
 #pragma unroll
@@ -410,7 +376,6 @@ __global__ void __launch_bounds__(128, 4) attention_tc_kernel(const __grid_const
     pdl_trigger();
     // Softmax: thread = query row = TMEM lane (warp w owns lanes 32w..32w+31).
     mbar_wait(&s_bar, 0);
-    amark(3);
     tc_fence_after();
     const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
     // Two passes over the row's 128 TMEM columns in 32-column chunks (row max,
@@ -451,7 +416,6 @@ __global__ void __launch_bounds__(128, 4) attention_tc_kernel(const __grid_const
     fence_proxy_async_smem();  // P (generic-proxy writes) -> the PV MMA reads
     tc_fence_before();
     __syncthreads();
-    amark(4);
     if (tid == 0) {
         tc_fence_after();
         // B = V as an MN-major operand: N = 64 dims contiguous (one 128-byte swizzle
@@ -464,7 +428,6 @@ __global__ void __launch_bounds__(128, 4) attention_tc_kernel(const __grid_const
         umma_commit(&o_bar);
     }
     mbar_wait(&o_bar, 0);
-    amark(5);
     tc_fence_after();
     float o[kDh];
     {
@@ -486,7 +449,6 @@ __global__ void __launch_bounds__(128, 4) attention_tc_kernel(const __grid_const
         for (int j = 0; j < 4; ++j) h2[j] = __floats2bfloat162_rn(o[c * 8 + 2 * j] * inv, o[c * 8 + 2 * j + 1] * inv);
         dst[c] = u;
     }
-    amark(6);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -688,26 +650,13 @@ void gemm_bn(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_
                                   CU_TENSOR_MAP_SWIZZLE_NONE))
             throw CudaError("cuTensorMapEncodeTiled failed (bert gemm arena weights)");
     }
-    static const bool trace_on = std::getenv("GFX_TRACE_GEMM") != nullptr;
-    GemmArgs a{nullptr, arena, w_off, b_off, y, resid, T, K, N, pt};
-    static bool attr_set = false;
+    GemmArgs a{arena, w_off, b_off, y, resid, T, K, N, pt};
     const size_t smem = kGSmem + 4 * 8192 + 1024;
-    static int sms = 0;
-    if (!attr_set) {
-        GFX_CUDA(cudaFuncSetAttribute(gemm_bf16_kernel<kEpi, kBN, kPair>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
-        int dev = 0;
-        GFX_CUDA(cudaGetDevice(&dev));
-        GFX_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-        attr_set = true;
-    }
+    ensure_max_dynamic_smem(reinterpret_cast<const void*>(gemm_bf16_kernel<kEpi, kBN, kPair>), static_cast<int>(smem));
+    const int sms = device_sm_count(current_device());
     const int tiles = (T / kGM) * (N / kBN);
     int grid = tiles < sms ? tiles : sms;
     if (kPair) grid &= ~1;
-    if (trace_on) {
-        GFX_CUDA(cudaMalloc(&a.trace, sizeof(unsigned long long) * (16 * grid + 512)));
-        GFX_CUDA(cudaMemset(a.trace, 0, sizeof(unsigned long long) * (16 * grid + 512)));
-    }
     if (kPair) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(grid);
@@ -727,35 +676,6 @@ void gemm_bn(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_
     } else {
         launch_pdl(gemm_bf16_kernel<kEpi, kBN, kPair>, dim3(grid), dim3(kGThreads), smem, s, pdl, tm, tmy, tmr, tmw, a);
     }
-    if (trace_on) {  // debug timeline: µs after the first CTA started, min / median / max over CTAs
-        std::vector<unsigned long long> tr(static_cast<size_t>(16) * grid + 512);
-        GFX_CUDA(cudaStreamSynchronize(s));
-        GFX_CUDA(cudaMemcpy(tr.data(), a.trace, tr.size() * 8, cudaMemcpyDeviceToHost));
-        GFX_CUDA(cudaFree(a.trace));
-        unsigned long long t0 = ~0ull;
-        for (int c = 0; c < grid; ++c) t0 = std::min(t0, tr[c * 16]);
-        static const char* nm[16] = {"start", "setup", "first stage", "mma0 issued", "mma1 issued", "mma2 issued",
-                                     "mma3 issued", "acc0 ready", "acc1 ready", "acc2 ready", "acc3 ready",
-                                     "tile0 stored", "tile1 stored", "tile2 stored", "tile3 stored", ""};
-        std::fprintf(stderr, "[gemm trace] T %d K %d N %d tile 128x%d grid %d tiles %d\n", T, K, N, kBN, grid, tiles);
-        for (int ph = 0; ph < 15; ++ph) {
-            std::vector<double> v;
-            for (int c = 0; c < grid; ++c)
-                if (tr[c * 16 + ph]) v.push_back((tr[c * 16 + ph] - t0) * 1e-3);
-            if (v.empty()) continue;
-            std::sort(v.begin(), v.end());
-            std::fprintf(stderr, "  %-14s n=%3zu %8.2f %8.2f %8.2f\n", nm[ph], v.size(), v.front(), v[v.size() / 2],
-                         v.back());
-        }
-        std::fprintf(stderr, "  stages (us): CTA0 [TMA issued, full seen, pair seen, MMA issued] | CTA1 [TMA issued, full seen, relayed]\n");
-        auto us = [&](unsigned long long t) { return t ? (t - t0) * 1e-3 : -1.0; };
-        for (int g = 0; g < 24; ++g) {
-            const unsigned long long* c0 = tr.data() + 16 * grid + g * 4;
-            const unsigned long long* c1 = tr.data() + 16 * grid + 256 + g * 4;
-            std::fprintf(stderr, "   %2d %7.2f %7.2f %7.2f %7.2f | %7.2f %7.2f %7.2f\n", g, us(c0[0]), us(c0[1]), us(c0[2]),
-                         us(c0[3]), us(c1[0]), us(c1[1]), us(c1[2]));
-        }
-    }
 }
 
 // 128 x 256 tiles: a tcgen05.mma with smem operands costs >= ~119 cycles
@@ -764,14 +684,13 @@ void gemm_bn(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_
 // 96 tiles). 128 x 192 was measured at ~210 cycles per MMA.
 template <int kEpi>
 void gemm(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_off, const __nv_bfloat16* x,
-          __nv_bfloat16* y, const __nv_bfloat16* resid, int T, int K, int N, cudaStream_t s, bool pdl) {
+          __nv_bfloat16* y, const __nv_bfloat16* resid, int T, int K, int N, cudaStream_t s, bool pdl, bool pair) {
     if (T % kGM || N % 128 || K % kGK) throw std::runtime_error("bert gemm: T, N multiple of 128, K of 64");
-    // The 2-SM variant (GFX_GEMM_PAIR=1) is correct; with the relay removed
+    // The 2-SM variant (BertWorkspace::gemm_pair) is correct; with the relay removed
     // (.cta_group::2 loads complete the even CTA's barrier) it runs 1.21 ms per
     // forward vs 1.17-1.18 for the single-CTA kernel (was 1.63 with the relay):
     // both advance ~0.45 µs per K stage with ~2 µs TMA latency at 192 KB in
     // flight per SM, so the single-CTA kernel stays the default.
-    static const bool pair = std::getenv("GFX_GEMM_PAIR") != nullptr;
     if (N % 256 == 0 && (T / kGM) % 2 == 0 && pair)
         gemm_bn<kEpi, 256, true>(arena, pt, w_off, b_off, x, y, resid, T, K, N, s, pdl);
     else if (N % 256 == 0)
@@ -860,49 +779,21 @@ int bert_forward(const char* arena, const PageTable& pt, const BertLayout& lay, 
     if (hidden) GFX_CUDA(cudaMemcpyAsync(hidden, in, hbytes, cudaMemcpyDeviceToDevice, s));
     for (int l = 0; l < lay.L; ++l) {
         const BertLayerOffsets& o = lay.layer[static_cast<size_t>(l)];
-        gemm<kEpiBias>(arena, pt, o.wqkv, o.bqkv, x, ws.qkv, nullptr, T, d, 3 * d, s, l > 0 && !hidden);
+        gemm<kEpiBias>(arena, pt, o.wqkv, o.bqkv, x, ws.qkv, nullptr, T, d, 3 * d, s, l > 0 && !hidden, ws.gemm_pair);
         {
             CUtensorMap tq;
             if (!encode_tensor_map_2d(&tq, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, ws.qkv, static_cast<uint64_t>(3 * d),
                                       static_cast<uint64_t>(T), static_cast<uint64_t>(3 * d) * 2, kDh, kS,
                                       CU_TENSOR_MAP_SWIZZLE_128B))
                 throw CudaError("cuTensorMapEncodeTiled failed (attention)");
-            static bool attr = false;
-            if (!attr) {
-                GFX_CUDA(cudaFuncSetAttribute(attention_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              static_cast<int>(kAttnSmem)));
-                attr = true;
-            }
-            static const bool atrace = std::getenv("GFX_TRACE_ATTN") != nullptr;
-            unsigned long long* tr = nullptr;
-            const int nblk = batch * lay.heads;
-            if (atrace && l == 0) {
-                GFX_CUDA(cudaMalloc(&tr, sizeof(unsigned long long) * 8 * nblk));
-                GFX_CUDA(cudaMemset(tr, 0, sizeof(unsigned long long) * 8 * nblk));
-                GFX_CUDA(cudaStreamSynchronize(s));
-            }
-            launch_pdl(attention_tc_kernel, dim3(nblk), dim3(128), kAttnSmem, s, true, tq, ws.ctx, lay.heads, tr);
-            if (tr) {  // debug timeline: µs after the first CTA started, min / median / max over CTAs
-                std::vector<unsigned long long> hh(static_cast<size_t>(8) * nblk);
-                GFX_CUDA(cudaStreamSynchronize(s));
-                GFX_CUDA(cudaMemcpy(hh.data(), tr, hh.size() * 8, cudaMemcpyDeviceToHost));
-                GFX_CUDA(cudaFree(tr));
-                unsigned long long t0 = ~0ull;
-                for (int c = 0; c < nblk; ++c) t0 = std::min(t0, hh[c * 8]);
-                static const char* nm[7] = {"start", "setup", "QKV landed", "S ready", "P written", "O ready", "stored"};
-                for (int ph = 0; ph < 7; ++ph) {
-                    std::vector<double> v;
-                    for (int c = 0; c < nblk; ++c) v.push_back((hh[c * 8 + ph] - t0) * 1e-3);
-                    std::sort(v.begin(), v.end());
-                    std::fprintf(stderr, "[attn] %-12s %8.2f %8.2f %8.2f\n", nm[ph], v.front(), v[v.size() / 2], v.back());
-                }
-            }
+            ensure_max_dynamic_smem(reinterpret_cast<const void*>(attention_tc_kernel), static_cast<int>(kAttnSmem));
+            launch_pdl(attention_tc_kernel, dim3(batch * lay.heads), dim3(128), kAttnSmem, s, true, tq, ws.ctx, lay.heads);
         }
-        gemm<kEpiResid>(arena, pt, o.wo, o.bo, ws.ctx, ws.t, x, T, d, d, s, true);
+        gemm<kEpiResid>(arena, pt, o.wo, o.bo, ws.ctx, ws.t, x, T, d, d, s, true, ws.gemm_pair);
         launch_pdl(layernorm_kernel<768>, dim3((T + 15) / 16), dim3(256), 0, s, true,
                    static_cast<const __nv_bfloat16*>(ws.t), ws.h, arena, pt, o.ln1_g, o.ln1_b, T);
-        gemm<kEpiGelu>(arena, pt, o.w1, o.b1, ws.h, ws.f, nullptr, T, d, lay.ffn, s, true);
-        gemm<kEpiResid>(arena, pt, o.w2, o.b2, ws.f, ws.t, ws.h, T, lay.ffn, d, s, true);
+        gemm<kEpiGelu>(arena, pt, o.w1, o.b1, ws.h, ws.f, nullptr, T, d, lay.ffn, s, true, ws.gemm_pair);
+        gemm<kEpiResid>(arena, pt, o.w2, o.b2, ws.f, ws.t, ws.h, T, lay.ffn, d, s, true, ws.gemm_pair);
         launch_pdl(layernorm_kernel<768>, dim3((T + 15) / 16), dim3(256), 0, s, true,
                    static_cast<const __nv_bfloat16*>(ws.t), ws.x, arena, pt, o.ln2_g, o.ln2_b, T);
         launches += 7;
@@ -913,15 +804,26 @@ int bert_forward(const char* arena, const PageTable& pt, const BertLayout& lay, 
     }
     if (d != 768 || static_cast<size_t>(batch) * d * 2 > 160 * 1024)
         throw std::runtime_error("bert pooler: d = 768 and at most 106 sequences per request");
-    static bool pool_attr = false;
-    if (!pool_attr) {
-        GFX_CUDA(cudaFuncSetAttribute(pooler_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-        pool_attr = true;
-    }
+    ensure_max_dynamic_smem(reinterpret_cast<const void*>(pooler_kernel), 160 * 1024);
     launch_pdl(pooler_kernel, dim3((d + 7) / 8), dim3(256), static_cast<size_t>(batch) * d * 2, s, !hidden,
                static_cast<const __nv_bfloat16*>(x), out,
                arena, pt, lay.wp, lay.bp, d, lay.seq, batch);
     return launches + 1;
+}
+
+void bert_gemm_op(const char* arena, const PageTable& pt, const BertLayout& lay, int l, int op,
+                  const __nv_bfloat16* x, const __nv_bfloat16* resid, __nv_bfloat16* y, int T, bool pair,
+                  cudaStream_t s) {
+    if (l < 0 || l >= lay.L) throw std::invalid_argument("bert gemm: bad layer");
+    const BertLayerOffsets& o = lay.layer[static_cast<size_t>(l)];
+    const int d = lay.d;
+    switch (op) {
+        case 0: gemm<kEpiBias>(arena, pt, o.wqkv, o.bqkv, x, y, nullptr, T, d, 3 * d, s, false, pair); break;
+        case 1: gemm<kEpiResid>(arena, pt, o.wo, o.bo, x, y, resid, T, d, d, s, false, pair); break;
+        case 2: gemm<kEpiGelu>(arena, pt, o.w1, o.b1, x, y, nullptr, T, d, lay.ffn, s, false, pair); break;
+        case 3: gemm<kEpiResid>(arena, pt, o.w2, o.b2, x, y, resid, T, lay.ffn, d, s, false, pair); break;
+        default: throw std::invalid_argument("bert gemm: op must be 0..3");
+    }
 }
 
 void launch_fill_bf16(__nv_bfloat16* dst, uint64_t n, uint64_t seed, uint32_t tensor, float scale, cudaStream_t s,

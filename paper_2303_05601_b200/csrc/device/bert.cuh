@@ -55,6 +55,7 @@ __host__ __device__ inline uint16_t bf16_bits(float f) {
 
 struct BertWorkspace {
     int tokens = 0;
+    bool gemm_pair = false;  // 2-SM (cta_group::2) GEMMs where the shape allows (gfx_arena_set_option)
     __nv_bfloat16 *x = nullptr, *qkv = nullptr, *ctx = nullptr, *h = nullptr, *f = nullptr, *t = nullptr;
     void ensure(int tokens, int d, int ffn);
     void release();
@@ -65,6 +66,12 @@ struct BertWorkspace {
 int bert_forward(const char* arena, const PageTable& pt, const BertLayout& lay, int batch,
                  const __nv_bfloat16* in, float* out, BertWorkspace& ws, cudaStream_t s,
                  __nv_bfloat16* hidden = nullptr);  // debug: [L+1][T][d] hidden states
+
+// Test hook: one K2 GEMM of layer l with its fused epilogue. op 0: QKV (+bias),
+// 1: attention output (+bias +resid), 2: FFN1 (+bias, GELU), 3: FFN2 (+bias +resid).
+void bert_gemm_op(const char* arena, const PageTable& pt, const BertLayout& lay, int l, int op,
+                  const __nv_bfloat16* x, const __nv_bfloat16* resid, __nv_bfloat16* y, int T, bool pair,
+                  cudaStream_t s);
 
 // Fill `count` bf16 tensors of n values from the parameter stream (inputs).
 void launch_fill_bf16(__nv_bfloat16* dst, uint64_t n, uint64_t seed, uint32_t tensor, float scale, cudaStream_t s,

@@ -23,6 +23,13 @@ inline void cuda_check(cudaError_t e, const char* what, const char* file, int li
 }
 #define GFX_CUDA(x) ::gfx::cuda_check((x), #x, __FILE__, __LINE__)
 
+// Per-device launch setup (util.cu). cudaFuncSetAttribute applies to the
+// current device's context only, so one process driving several devices sets
+// it once per (device, kernel); the SM count is cached per device.
+int current_device();
+int device_sm_count(int dev);
+void ensure_max_dynamic_smem(const void* func, int bytes);
+
 constexpr uint32_t kPageShift = 21;  // 2 MiB arena pages
 constexpr uint64_t kPageBytes = uint64_t{1} << kPageShift;
 constexpr uint64_t kPageMask = kPageBytes - 1;

@@ -247,11 +247,9 @@ GpuManager::GpuManager(int device, uint64_t capacity_bytes, int manager_id) : de
     for (uint32_t p = 0; p < npages_; ++p) free_.insert(p);
     GFX_CUDA(cudaStreamCreateWithFlags(&compute_, cudaStreamNonBlocking));
     GFX_CUDA(cudaStreamCreateWithFlags(&copy_, cudaStreamNonBlocking));
-    GFX_CUDA(cudaDeviceGetAttribute(&sm_count_, cudaDevAttrMultiProcessorCount, device_));
-    GFX_CUDA(cudaMalloc(&fwd_opnd_, kMlpOpndLayerBytes * GFX_MAX_LAYERS));
-    GFX_CUDA(cudaMalloc(&fwd_part_, sizeof(float) * kMlpPartLayerFloats * GFX_MAX_LAYERS));
-    GFX_CUDA(cudaMalloc(&fwd_cnt_, sizeof(unsigned) * kMlpCounters));
-    GFX_CUDA(cudaMemset(fwd_cnt_, 0, sizeof(unsigned) * kMlpCounters));
+    sm_count_ = device_sm_count(device_);
+    GFX_CUDA(cudaMalloc(&fwd_act_, sizeof(unsigned long long) * 2 * kMlpActWords));
+    GFX_CUDA(cudaMemset(fwd_act_, 0, sizeof(unsigned long long) * 2 * kMlpActWords));
     GFX_CUDA(cudaDeviceSynchronize());
 }
 
@@ -264,9 +262,7 @@ GpuManager::~GpuManager() {
         if (s.last_use) cudaEventDestroy(s.last_use);
     }
     cudaFree(arena_);
-    cudaFree(fwd_opnd_);
-    cudaFree(fwd_part_);
-    cudaFree(fwd_cnt_);
+    cudaFree(fwd_act_);
     bert_ws_.release();
     cudaStreamDestroy(compute_);
     cudaStreamDestroy(copy_);
@@ -299,7 +295,12 @@ const std::vector<uint32_t>& GpuManager::pages_of(int model) const {
     return slots_[static_cast<size_t>(model)].pages;
 }
 
-void GpuManager::add_reader(int model, cudaEvent_t e) { slot(model).readers.push_back(e); }
+void GpuManager::add_reader(int model, cudaEvent_t e) {
+    // One entry per reader event: a re-fetch by the same manager re-records the
+    // same event, and waiting on its latest record covers every earlier one.
+    std::vector<cudaEvent_t>& r = slot(model).readers;
+    if (std::find(r.begin(), r.end(), e) == r.end()) r.push_back(e);
+}
 
 // ClusterState::evict_one (proj/src/cluster.cpp:117-129) on device: the pages
 // return to the pool at once (host bookkeeping), and the copy stream — the
@@ -471,134 +472,66 @@ void GpuManager::infer(int model, const void* in_v, void* out_v, void* debug_hid
         GFX_CUDA(cudaEventRecord(s.last_use, compute_));
         return;
     }
-    const float* in = static_cast<const float*>(in_v);
-    float* out = static_cast<float*>(out_v);
-    {
-        MlpFwdArgs f{};
-        f.arena = arena_;
-        build_page_table(s, f.pt);
-        f.in = in;
-        f.L = blob.desc.n_layers;
-        f.logits = out;
-        f.probs = out + static_cast<size_t>(kBatch) * blob.desc.dims[f.L];
-        f.opnd = fwd_opnd_;
-        f.part = fwd_part_;
-        f.cnt = fwd_cnt_;
-        static const bool use_cluster = std::getenv("GFX_MLP_CLUSTER") != nullptr;
-        static const int cluster_grid = use_cluster ? mlp_fwd_cluster_grid(8) : 0;
-        f.cluster = use_cluster ? 8 : 0;
-        f.grid = use_cluster ? cluster_grid : sm_count_;
-        static const int ablate = std::getenv("GFX_MLP_ABLATE") ? std::atoi(std::getenv("GFX_MLP_ABLATE")) : 0;
-        f.ablate = ablate;
-        for (int l = 0; l < f.L; ++l) {
-            MlpFwdLayer& ly = f.layer[l];
-            ly.w_off = blob.w_off[l];
-            ly.b_off = blob.b_off[l];
-            ly.K = blob.desc.dims[l];
-            ly.N = blob.desc.dims[l + 1];
-            ly.tiles = (ly.N + kWTileRows - 1) / kWTileRows;
-            ly.splits = mlp_fwd_splits(ly.K, ly.N, f.grid, f.cluster);
-        }
-        static const bool trace_on = std::getenv("GFX_TRACE_MLP") != nullptr;
-        if (trace_on) {
-            GFX_CUDA(cudaMalloc(&f.trace, sizeof(unsigned long long) * mlp_trace_words(f.grid)));
-            GFX_CUDA(cudaMemset(f.trace, 0, sizeof(unsigned long long) * mlp_trace_words(f.grid)));
-        }
-        if (layer_timer) GFX_CUDA(cudaEventRecord(layer_timer->next(), compute_));
-        static const int repeat = std::getenv("GFX_MLP_REPEAT") ? std::atoi(std::getenv("GFX_MLP_REPEAT")) : 0;
-        if (repeat > 0) {  // debug: device time of back-to-back forwards of this model (CUDA events)
-            cudaEvent_t e0, e1;
-            GFX_CUDA(cudaEventCreate(&e0));
-            GFX_CUDA(cudaEventCreate(&e1));
-            // GFX_MLP_REPEAT_MODE: 0 back-to-back; 1 each launch after a compute-stream
-            // wait on an event of the copy stream (the replay's load dependency);
-            // 2 events around every launch (the replay's kernel timer), summed;
-            // 3 back-to-back under concurrent H2D; 4 / 5 a 1 MB H2D copy before
-            // every launch (cross-stream / same stream); 6 the copies alone.
-            static const int rmode = std::getenv("GFX_MLP_REPEAT_MODE") ? std::atoi(std::getenv("GFX_MLP_REPEAT_MODE")) : 0;
-            std::vector<cudaEvent_t> ev;
-            if (rmode == 2)
-                for (int r = 0; r < 2 * repeat; ++r) {
-                    cudaEvent_t e;
-                    GFX_CUDA(cudaEventCreate(&e));
-                    ev.push_back(e);
-                }
-            cudaEvent_t cev;
-            GFX_CUDA(cudaEventCreateWithFlags(&cev, cudaEventDisableTiming));
-            // mode 3: back-to-back launches while the copy stream streams pinned host
-            // memory into a scratch buffer (the replay's concurrent model loads).
-            void* hbuf = nullptr;
-            void* dbuf = nullptr;
-            cudaEvent_t kev;  // modes 4/5: the previous forward's completion
-            GFX_CUDA(cudaEventCreateWithFlags(&kev, cudaEventDisableTiming));
-            if (rmode == 4 || rmode == 5 || rmode == 6) {
-                GFX_CUDA(cudaHostAlloc(&hbuf, 1u << 20, cudaHostAllocDefault));
-                GFX_CUDA(cudaMalloc(&dbuf, 1u << 20));
-            }
-            if (rmode == 3) {
-                GFX_CUDA(cudaHostAlloc(&hbuf, 256ull << 20, cudaHostAllocDefault));
-                GFX_CUDA(cudaMalloc(&dbuf, 256ull << 20));
-                for (int r = 0; r < 8; ++r)
-                    GFX_CUDA(cudaMemcpyAsync(dbuf, hbuf, 256ull << 20, cudaMemcpyHostToDevice, copy_));
-            }
-            GFX_CUDA(cudaEventRecord(e0, compute_));
-            for (int r = 0; r < repeat; ++r) {
-                f.epoch = fwd_epoch_++;
-                if (rmode == 1) {
-                    GFX_CUDA(cudaEventRecord(cev, copy_));
-                    GFX_CUDA(cudaStreamWaitEvent(compute_, cev, 0));
-                }
-                if (rmode == 4) {  // serial copy -> forward through a cross-stream dependency (a miss)
-                    GFX_CUDA(cudaStreamWaitEvent(copy_, kev, 0));
-                    GFX_CUDA(cudaMemcpyAsync(dbuf, hbuf, 1u << 20, cudaMemcpyHostToDevice, copy_));
-                    GFX_CUDA(cudaEventRecord(cev, copy_));
-                    GFX_CUDA(cudaStreamWaitEvent(compute_, cev, 0));
-                }
-                if (rmode == 5 || rmode == 6)  // the same copy on the compute stream itself (6: copy only)
-                    GFX_CUDA(cudaMemcpyAsync(dbuf, hbuf, 1u << 20, cudaMemcpyHostToDevice, compute_));
-                if (rmode == 6) continue;
-                if (rmode == 2) GFX_CUDA(cudaEventRecord(ev[2 * r], compute_));
-                launch_mlp_forward(f, compute_);
-                if (rmode == 2) GFX_CUDA(cudaEventRecord(ev[2 * r + 1], compute_));
-                if (rmode == 4) GFX_CUDA(cudaEventRecord(kev, compute_));
-            }
-            GFX_CUDA(cudaEventRecord(e1, compute_));
-            GFX_CUDA(cudaEventSynchronize(e1));
-            float ms = 0;
-            GFX_CUDA(cudaEventElapsedTime(&ms, e0, e1));
-            double inner = 0;
-            for (int r = 0; rmode == 2 && r < repeat; ++r) {
-                float x = 0;
-                GFX_CUDA(cudaEventElapsedTime(&x, ev[2 * r], ev[2 * r + 1]));
-                inner += x;
-            }
-            for (cudaEvent_t e : ev) cudaEventDestroy(e);
-            cudaEventDestroy(cev);
-            if (hbuf) {
-                GFX_CUDA(cudaStreamSynchronize(copy_));
-                GFX_CUDA(cudaFreeHost(hbuf));
-                GFX_CUDA(cudaFree(dbuf));
-            }
-            cudaEventDestroy(kev);
-            std::fprintf(stderr, "[repeat] model %d mode %d: %.2f us per forward (%d launches), bracketed %.2f us\n",
-                         model, rmode, 1e3 * ms / repeat, repeat, 1e3 * inner / repeat);
-            GFX_CUDA(cudaEventDestroy(e0));
-            GFX_CUDA(cudaEventDestroy(e1));
-        }
-        f.epoch = fwd_epoch_++;
-        launch_mlp_forward(f, compute_);
-        ++kernel_launches;
-        if (trace_on) {  // debug timeline (GFX_TRACE_MLP)
-            std::vector<unsigned long long> tr(mlp_trace_words(f.grid));
-            GFX_CUDA(cudaStreamSynchronize(compute_));
-            GFX_CUDA(cudaMemcpy(tr.data(), f.trace, tr.size() * 8, cudaMemcpyDeviceToHost));
-            GFX_CUDA(cudaFree(f.trace));
-            mlp_trace_report(tr, f.grid, f.L, model);
-        }
-        if (layer_timer) GFX_CUDA(cudaEventRecord(layer_timer->next(), compute_));
-        GFX_CUDA(cudaEventRecord(s.last_use, compute_));
-        return;
+    MlpFwdArgs f{};
+    f.arena = arena_;
+    build_page_table(s, f.pt);
+    f.in = static_cast<const float*>(in_v);
+    f.L = blob.desc.n_layers;
+    f.logits = static_cast<float*>(out_v);
+    f.probs = f.logits + static_cast<size_t>(kBatch) * blob.desc.dims[f.L];
+    f.grid = sm_count_;
+    uint32_t act = 0;
+    for (int l = 0; l < f.L; ++l) {
+        MlpFwdLayer& ly = f.layer[l];
+        ly.w_off = blob.w_off[l];
+        ly.b_off = blob.b_off[l];
+        ly.K = blob.desc.dims[l];
+        ly.N = blob.desc.dims[l + 1];
+        ly.tiles = (ly.N + kWTileRows - 1) / kWTileRows;
+        ly.nkt = ly.K / kWTileK;
+        ly.act_off = act;
+        act += static_cast<uint32_t>(ly.N) * kBatch;
     }
+    // Launch parity p uses act bank p (zeroed by the previous launch) and
+    // clears bank p^1 up to what the previous launch (parity p^1) dirtied.
+    const unsigned p = fwd_epoch_ & 1u;
+    f.act = fwd_act_ + p * kMlpActWords;
+    f.act_clear = reinterpret_cast<uint4*>(fwd_act_ + (p ^ 1u) * kMlpActWords);
+    f.clear_vec = act_dirty_[p ^ 1u] / 2;
+#ifdef GFX_K1_DEBUG
+    static unsigned long long* dbg = nullptr;
+    static unsigned launches = 0;
+    if (!dbg) {
+        GFX_CUDA(cudaMalloc(&dbg, sizeof(unsigned long long) * (32 * 1024 + 96 * 8)));
+        GFX_CUDA(cudaMemset(dbg, 0, sizeof(unsigned long long) * (32 * 1024 + 96 * 8)));
+    }
+    f.dbg = dbg;
+#endif
+    if (layer_timer) GFX_CUDA(cudaEventRecord(layer_timer->next(), compute_));
+    launch_mlp_forward(f, compute_);
+#ifdef GFX_K1_DEBUG
+    if (++launches % 64 == 8) mlp_debug_report(dbg, f.grid, f.L, model, compute_);
+#endif
+    act_dirty_[p ^ 1u] = 0;
+    act_dirty_[p] = act;
+    ++fwd_epoch_;
+    ++kernel_launches;
+    if (layer_timer) GFX_CUDA(cudaEventRecord(layer_timer->next(), compute_));
+    GFX_CUDA(cudaEventRecord(s.last_use, compute_));
+}
+
+void GpuManager::bert_gemm(int model, int layer, int op, const void* x, const void* resid, void* y, int tokens) {
+    const ModelBlob& blob = ModelStore::get().at(model);
+    Slot& s = slot(model);
+    if (!s.live) throw std::logic_error("gemm of non-resident model " + std::to_string(model));
+    if (blob.desc.family != GFX_MODEL_BERT) throw std::invalid_argument("bert_gemm: BERT models only");
+    activate();
+    PageTable pt;
+    build_page_table(s, pt);
+    bert_gemm_op(arena_, pt, blob.bert, layer, op, static_cast<const __nv_bfloat16*>(x),
+                 static_cast<const __nv_bfloat16*>(resid), static_cast<__nv_bfloat16*>(y), tokens, bert_ws_.gemm_pair,
+                 compute_);
+    GFX_CUDA(cudaEventRecord(s.last_use, compute_));
 }
 
 void GpuManager::reset() {
@@ -611,7 +544,11 @@ void GpuManager::reset() {
         s.readers.clear();
         s.live = false;
     }
-    GFX_CUDA(cudaMemset(fwd_cnt_, 0, sizeof(unsigned) * kMlpCounters));
+    // A run may have ended mid-way (an exception after a launch): clear both banks.
+    for (unsigned p = 0; p < 2; ++p)
+        if (act_dirty_[p])
+            GFX_CUDA(cudaMemset(fwd_act_ + p * kMlpActWords, 0, sizeof(unsigned long long) * act_dirty_[p]));
+    act_dirty_[0] = act_dirty_[1] = 0;
     GFX_CUDA(cudaDeviceSynchronize());
 }
 

@@ -82,6 +82,8 @@ public:
     uint64_t load(int model, GpuManager* src);
     void infer(int model, const void* in, void* out, void* debug_hidden = nullptr);
     void reset();  // synchronise and drop every resident model
+    // Test hook: one BERT GEMM (bert_gemm_op) of a resident model on the compute stream.
+    void bert_gemm(int model, int layer, int op, const void* x, const void* resid, void* y, int tokens);
 
     // Cross-process peers (one process per GPU): fetch a model from another
     // rank's arena mapped into this process by CUDA IPC, `src_pages` being that
@@ -100,6 +102,7 @@ public:
     const std::vector<uint32_t>& pages_of(int model) const;
     char* arena() const { return arena_; }
     void activate() const;  // cudaSetDevice
+    void set_gemm_pair(bool on) { bert_ws_.gemm_pair = on; }
 
     // Instrumentation (all optional).
     KernelTimer* layer_timer = nullptr;   // records around every inference
@@ -129,11 +132,10 @@ private:
     int sm_count_ = 148;
     // inference workspaces
     BertWorkspace bert_ws_;
-    // K1 v6 forward workspace
-    char* fwd_opnd_ = nullptr;
-    float* fwd_part_ = nullptr;
-    unsigned* fwd_cnt_ = nullptr;
-    unsigned fwd_epoch_ = 0;  // launches of the forward kernel on this manager's workspace
+    // K1 forward workspace: layer outputs, two banks by launch parity
+    unsigned long long* fwd_act_ = nullptr;
+    unsigned fwd_epoch_ = 0;      // launches of the forward kernel on this manager's workspace
+    uint32_t act_dirty_[2] = {0, 0};  // words of each act bank written and not yet cleared
 };
 
 }  // namespace gfx

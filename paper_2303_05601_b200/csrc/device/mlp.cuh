@@ -14,44 +14,45 @@ namespace gfx {
 void launch_fill_params(float* dst, uint64_t n, uint64_t seed, uint32_t tensor, float scale, cudaStream_t s,
                         uint64_t count = 1);
 
-// K1 v6: whole forward in one persistent cooperative launch (mlp_fwd.cu).
+// K1 v7: whole forward in one persistent cooperative launch (mlp_fwd.cu).
 constexpr int kMlpMaxDim = 8192;
-constexpr size_t kMlpOpndLayerBytes = static_cast<size_t>(kMlpMaxDim / 32) * 8192;  // operand blocks per layer input
-constexpr size_t kMlpPartLayerFloats = static_cast<size_t>(160) * 32 * 128;        // split-K partials per layer
-constexpr int kMlpCounters = 8192;
+constexpr int kMlpMaxClasses = 2048;
+// Layer outputs as 64-bit words (fixed-point value x 2^32 << 9 | completion
+// count), feature-major [N][32], reduced in L2 by the split-K partials
+// (red.add.u64: associative, so the sum is the same whatever order the
+// partials arrive in). One buffer per launch parity; Σ_l N_l x 32 words used.
+constexpr int kMlpFixShift = 32;
+constexpr size_t kMlpActWords = static_cast<size_t>(GFX_MAX_LAYERS) * kMlpMaxDim * 32;
 
 struct MlpFwdLayer {
     uint64_t w_off, b_off;  // model-blob offsets of the weight tiles and the bias
     int K, N;
-    int tiles, splits;      // units = tiles x splits <= grid
+    int tiles, nkt;         // 128-row feature tiles, 32-wide K tiles
+    uint32_t act_off;       // words: this layer's output [N][32] in the act buffer
 };
 
 struct MlpFwdArgs {
     CUtensorMap tmap_in;    // layer-0 input tiles (filled by launch_mlp_forward)
+    CUtensorMap tmap_out[GFX_MAX_LAYERS];  // layer outputs [N][32] u64, 32 x 16 boxes (filled by launch_mlp_forward)
     const char* arena;
     const float* in;        // [32 x K0] request input, row-major
     float* logits;          // [32 x C]
     float* probs;           // [32 x C] softmax rows
-    char* opnd;             // operand blocks, layer l's input at opnd + l * kMlpOpndLayerBytes
-    float* part;            // split-K partials, layer l at part + l * kMlpPartLayerFloats
-    unsigned* cnt;          // kMlpCounters dataflow counters: two banks, bank (epoch & 1) zero at launch
-    unsigned epoch;         // launch sequence number on this workspace (stream-ordered)
+    unsigned long long* act;  // this launch's layer outputs (all zero at launch)
+    uint4* act_clear;         // the other parity's buffer: cleared here for the next launch
+    uint32_t clear_vec;       // 16-byte vectors of act_clear the previous launch dirtied
+    unsigned long long* dbg;  // GFX_K1_DEBUG builds: [grid][32] phase marks (%globaltimer), else unused
     int L;
     int grid;
-    int cluster;            // 0, or 8: split-K reduced through cluster DSMEM (GFX_MLP_CLUSTER=1)
-    int ablate;             // debug bitmask (0 in production): 1 = W_hi taken as rn_tf32 instead of trunc
-    unsigned long long* trace;  // debug (GFX_TRACE_MLP): [grid][32] %globaltimer marks, else nullptr
     MlpFwdLayer layer[GFX_MAX_LAYERS];
     PageTable pt;
 };
 
-int mlp_fwd_splits(int K, int N, int grid, int cluster = 0);
-int mlp_fwd_cluster_grid(int cluster);
 size_t mlp_fwd_smem();
+// GFX_K1_DEBUG builds: phase-mark table of the last launch (stderr).
+void mlp_debug_report(const unsigned long long* dbg, int grid, int L, int model, cudaStream_t s);
+// Validates the shapes, fills the tensor map and launches on `stream`.
 void launch_mlp_forward(MlpFwdArgs& a, cudaStream_t stream);
-// Debug timeline (GFX_TRACE_MLP): buffer size in 64-bit words and the stderr report.
-size_t mlp_trace_words(int grid);
-void mlp_trace_report(const std::vector<unsigned long long>& trace, int grid, int layers, int model);
 
 // Weight tiles of the blob: 128 x 32 fp32, K-major SWIZZLE_128B image (16 KB).
 constexpr int kWTileRows = 128;

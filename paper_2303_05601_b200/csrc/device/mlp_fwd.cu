@@ -1,67 +1,91 @@
-// K1 v6: the whole fp32 MLP forward of one request (batch 32) in ONE persistent
+// K1 v7: the whole fp32 MLP forward of one request (batch 32) in ONE persistent
 // cooperative launch on the 5th-gen tensor cores (tcgen05, kind::tf32, 3xTF32
 // error compensation), weights streamed by TMA straight out of the paged HBM
 // arena. Replaces profile.infer_time_us (proj/src/cluster.cpp:161,167).
 //
 //   layer l: Y_l[32 x N] = act(X_l[32 x K] . W_l^T + b_l)  as  D^T[N x 32] = W_l . X_l^T
 //   (swap AB: 128 weight rows fill the MMA M side, the 32 batch rows are N),
-//   act = ReLU on hidden layers; the last layer's rows also go through softmax.
+//   act = ReLU on hidden layers; the last layer's rows go through softmax.
 //
-// Why one launch (profiles/r1_k1_v5_ncu.md): a layer of a C2 model is 7-13 MB
-// of weights, 1-2 µs of HBM time, but a per-layer launch cost 12-15 µs of
-// prologue, pipeline fill and split-K tail. Here every CTA streams the weight
-// tiles of ALL its layers back to back through one TMA ring — weights do not
-// depend on activations — so the HBM never idles at a layer boundary; only the
-// (small) activation operands wait, on per-tile dataflow flags set by the
-// CTAs that reduced the previous layer's tile. No grid barrier, no relaunch.
+// Work split (stream-K): a layer is tiles x nkt steps, step s = (feature tile
+// s / nkt, K tile s % nkt); the blob stores weight tiles in exactly that order,
+// so step s reads the 16 KB tile at w_off + 16 KB * s. CTA c takes the
+// contiguous steps [c*S/grid, (c+1)*S/grid): every SM streams the same number
+// of weight bytes in every layer (no idle SMs, whatever the layer shape), and a
+// CTA whose range crosses a tile boundary contributes to two tiles. Every CTA
+// streams the weight tiles of ALL its layers back to back through one TMA ring
+// (weights do not depend on activations), so the HBM stays busy across layer
+// boundaries; only the activation operands wait.
 //
-// Work split per layer: unit u = blockIdx.x < tiles x splits -> feature tile
-// u % tiles (128 outputs), K split u / tiles (a contiguous range of 32-wide K
-// tiles). Split-K partials are reduced by the split CTAs of the tile, each
-// owning the batch rows b = split (mod splits), summed in fixed split order
-// (deterministic). The reducer writes the next layer's operand directly in the
-// tensor-core layout (see "operand block" below), so no CTA re-splits inputs.
+// Layer boundary (v6 needed eight dependent global round trips, a counter-
+// based v7 draft five): each CTA adds its partial of a tile straight into the
+// layer's output buffer with red.add.u64 (the reduction happens in L2), and
+// nothing else — no fence, no counter. Every 64-bit word carries its own
+// completion count: word = (fixed-point value << 9) + (K tiles this partial
+// covers), so a word is complete when its low 9 bits reach the layer's nkt.
+// The consumer's X producer waits until one word of the source tile is
+// complete (the tile's contributors reduce all its words at about the same
+// time; lanes share what they have seen through shared memory), then
+// bulk-copies the 8 KB [32 features x 32 rows] block of its K tile; the
+// converter warps check every word's count and re-read any still incomplete
+// word from L2, then apply ReLU and the tf32 split while building the MMA
+// operand. (Issuing the copies before the tile completed made every early
+// ring slot pay its own ~1 µs poll round trip in the converters.) The bias is added once, by the CTA whose range holds the tile's K
+// tile 0. Fixed point: value x 2^32 rounded to an integer; integer addition is
+// associative, so the reduced value does not depend on the order the partials
+// reach L2 and every launch is bit-reproducible; the consumer converts once
+// (int64 -> fp32, one rounding). Range |value| < 2^22, resolution 2^-32 (far
+// inside the 1e-5 fp32 tolerance for these models).
 //
-// Precision (north-star fp32 tolerance 1e-5): the tensor core reads W straight
-// from the landed fp32 tile; kind::tf32 uses only the top 19 bits, i.e.
-// W_hi = trunc_tf32(W) (verified on B200: taking W_hi as the rounded value
-// instead breaks parity, 1.4e-3). Converter warps form W_lo = W - W_hi (exact
-// in fp32, |W_lo| < 2^-10 |W|) into a TMEM ring. Activations are pre-split by
-// their producer: X_hi = rn_tf32(X), X_lo = X - X_hi (exact). Per 8-wide K slice:
+// Precision: the tensor core reads W straight from the landed fp32 tile;
+// kind::tf32 uses only the top 19 bits, i.e. W_hi = trunc_tf32(W) (verified on
+// B200: the rounded interpretation breaks parity, 1.4e-3). Converter warps form
+// W_lo = W - W_hi (exact) into a TMEM ring; activations are split by the
+// converters: X_hi = rn_tf32(X), X_lo = X - X_hi (exact). Per 8-wide K slice:
 //   D += W_hi . [X_hi; X_lo]   (SS, N = 64: both batch planes at once)
-//   D += W_lo . X_hi           (TS, A from TMEM, N = 32; B rows just read)
-// Measured per 32-wide K step (tools/issue_rate.cu, rotating ring slots): this
-// pair costs ~556 cycles, vs ~1081 with W_hi also from TMEM and ~1007 for the
-// two N = 64 TMEM products of K1 v5.
-// i.e. every product but W_lo.X_lo (< 2^-21 relative); the accumulator keeps
-// the X_hi / X_lo columns apart and is drained to fp32 registers every kChunk
-// K tiles (short tensor-core accumulation chains at any K).
+//   D += W_lo . X_hi           (TS, A from TMEM, N = 32)
+// i.e. every product but W_lo.X_lo (< 2^-21 relative); the accumulator is
+// drained to fp32 registers every kChunk K tiles.
 //
-// Operand block (global, per 32-wide K tile of a layer input, 8 KB): 64 rows x
-// 128 B — rows 0-31 = X_hi of batch rows 0-31, rows 32-63 = X_lo — with the
-// SWIZZLE_128B chunk permutation (16-byte chunk j of row r at j ^ (r & 7)), so
-// a 1-D bulk copy into a 1024-aligned smem slot is the MMA's B operand as is.
+// Operand block (smem, per step, 8 KB): 64 rows x 128 B, rows 0-31 = X_hi of
+// batch rows 0-31, rows 32-63 = X_lo, SWIZZLE_128B chunk permutation (16-byte
+// chunk j of row r at j ^ (r & 7)): the MMA's K-major B operand as is. The raw
+// input of the step lands in the same 8 KB (layer 0: 2-D TMA of the 4 KB
+// request-input tile into the upper half, row-major swizzled; later layers:
+// the previous layer's 8 KB fixed-point output block, feature-major) and is
+// converted in place.
 //
-// Roles (16 warps, one CTA per SM, 8-deep ring of 24 KB slots = W 16 KB + X 8 KB):
-//   warp 0        W producer: 1-D bulk TMA of each 16 KB pre-swizzled weight tile
-//   warp 14       X producer: layer 0 splits the request input into the slot;
-//                 later layers wait for the tile's dataflow flag, bulk TMA 8 KB
-//   warps 2-5/6-9 converters (two groups, alternate K tiles): W_lo -> TMEM ring
+// Roles (16 warps, one CTA per SM, 8-deep ring: W [8][16 KB] and X [8][8 KB]):
+//   warp 0        W producer: 1-D bulk TMA of the pre-swizzled weight tiles, one
+//                 32 KB copy per pair of consecutive steps of a layer (half the
+//                 requests of one issuing thread, whose TMA requests are served
+//                 one after another)
+//   warp 14       X producer (one lane: divergent lanes spinning on different
+//                 conditions can starve each other): layer 0 issues the 2-D TMA
+//                 of the raw input tile, later layers wait for the source tile's
+//                 first complete word, then bulk-copy its 8 KB block (16 KB for
+//                 a pair of steps). A paired copy completes the first slot's
+//                 barrier; the producer arrives on the second slot's barrier so
+//                 every barrier still completes once per ring round.
+//   warps 2-5/6-9 converters (two groups, alternate steps): W_lo -> TMEM ring,
+//                 raw X (completion-checked) -> [X_hi; X_lo] operand (ReLU)
 //   warps 1, 15   MMA issuers, alternate accumulator chunks: 8 MMAs per K tile
-//                 and ONE commit per step (slot, operand and W_lo stage share
-//                 a step_done barrier)
-//   warps 10-13   drain (TMEM -> fp32 registers per chunk) and epilogue
-//                 (split-K reduction, bias, ReLU, next-layer operand / logits),
-//                 softmax rows at the end.
+//                 and one commit per step (step_done frees slot + W_lo stage)
+//   warps 10-13   drain (TMEM -> fp32 registers per chunk); per tile partial:
+//                 fixed-point words staged in smem (SWIZZLE_128B boxes of 32
+//                 features x 16 rows), then one TMA add-reduction per box
+//                 (cp.reduce.async.bulk.tensor .add u64, rows >= N clipped by
+//                 the tensor map) — the SM hands 32 KB to the TMA engine;
+//                 softmax rows at the end; at start they clear the other
+//                 parity's buffer for the next launch.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
-#include <cstdint>
-#include <vector>
-#include <cstdio>
 #include <algorithm>
-#include <cstdlib>
+#include <cstdint>
+#include <cstdio>
 #include <stdexcept>
+#include <vector>
 
 #include "common.cuh"
 #include "mlp.cuh"
@@ -74,54 +98,131 @@ namespace {
 using namespace gfx::sm100;
 
 constexpr int kRows = 32;     // batch rows per request
-constexpr int kTileM = 128;   // output features per unit = MMA M
+constexpr int kTileM = 128;   // output features per tile = MMA M
 constexpr int kTileK = 32;    // fp32 K per ring step (one 128-byte swizzle row)
 constexpr int kSlots = 8;     // ring depth: 8 x 16 KB = 128 KB of weights in flight per SM
 constexpr int kChunk = 4;     // K tiles accumulated in TMEM before a drain
 constexpr int kThreads = 16 * 32;
 constexpr uint32_t kWBytes = kTileM * kTileK * 4;      // 16 KB
 constexpr uint32_t kXBytes = 2 * kRows * kTileK * 4;   // 8 KB: [X_hi; X_lo]
-constexpr uint32_t kSlotBytes = kWBytes + kXBytes;     // 24 KB (1024-aligned)
+constexpr uint32_t kRaw0Bytes = kRows * kTileK * 4;    // layer-0 raw input tile: 4 KB (upper half of X)
+constexpr uint32_t kRawBytes = kRows * kTileK * 8;     // later layers: 8 KB fixed-point block (all of X)
+constexpr uint32_t kXRing = kSlots * kWBytes;          // smem: W ring [8][16 KB], then X ring [8][8 KB]
+constexpr uint32_t kStageOff = kXRing + kSlots * kXBytes;  // then the drain's 32 KB staging
 constexpr uint32_t kAccCols = 2 * kRows;               // 64: X_hi products | X_lo products
 constexpr int kAccBufs = 4;                              // accumulator buffers (chunks in flight MMA -> drain)
 constexpr uint32_t kLoBase = kAccBufs * kAccCols;        // W_lo ring (one 32-column stage per slot)
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kGatherBytes = 64 * kTileM * 4;     // split-K gather: <= 63 partial rows of 512 B
 static_assert(kLoBase + kTileK * kSlots <= kTmemCols, "TMEM budget");
-
-// counters (u32), zero between launches (the last CTA out resets them)
-constexpr int kCntArrive = 0;                        // [layer][tile] split partials published
-constexpr int kCntDone = GFX_MAX_LAYERS * 64;         // [layer][tile] split rows reduced + written
-constexpr int kCntFinal = 2 * GFX_MAX_LAYERS * 64;    // last-layer units finished
-// Two banks alternate by launch parity: a launch zeroes the bank the previous
-// (stream-ordered, finished) launch used, off its critical path, so no CTA has
-// to reset counters at the end.
-constexpr int kCntBank = kCntFinal + 64;
-static_assert(2 * kCntBank <= kMlpCounters, "counter banks");
+constexpr uint32_t kStageBytes = kTileM * kRows * 8;    // drain staging: 2 halves x 128 features x 16 rows u64
+constexpr float kFixScale = 4294967296.0f;               // 2^kMlpFixShift
+constexpr float kFixInv = 1.0f / 4294967296.0f;
+static_assert(kMlpFixShift == 32, "fixed-point scale");
+constexpr int kCountBits = 9;                            // per-word completion count (nkt <= 256)
+constexpr unsigned long long kCountMask = (1ull << kCountBits) - 1;
+static_assert(kMlpMaxDim / kTileK < (1 << kCountBits), "count field");
 
 __device__ __forceinline__ const char* translate(const char* arena, const uint32_t* pt, uint64_t v) {
     return arena + (static_cast<uint64_t>(pt[v >> kPageShift]) << kPageShift) + (v & kPageMask);
 }
-__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
-    unsigned v;
-    asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+    unsigned long long v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];\n" : "=l"(v) : "l"(p) : "memory");
     return v;
 }
-__device__ __forceinline__ void wait_count(const unsigned* p, unsigned target) {
-    while (ld_acquire(p) < target) {
+// Debug build (make K1_DEBUG=1 -> -DGFX_K1_DEBUG): every wait has a watchdog
+// that reports the stuck wait (CTA, warp, lane, site, step) and traps.
+#ifdef GFX_K1_DEBUG
+__device__ __forceinline__ void watchdog(long long& spins, int site, int g) {
+    if (++spins == (1ll << 24))
+        printf("K1 watchdog: cta %d warp %d lane %d site %d step %d\n", blockIdx.x, threadIdx.x >> 5, threadIdx.x & 31,
+               site, g);
+    if (spins == (1ll << 26)) __trap();
+}
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
+__device__ __forceinline__ unsigned long long gtime() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+// Phase marks per CTA (K1_MARK: first writer wins; K1_SET: last writer wins),
+// copied to MlpFwdArgs::dbg[cta][32] at exit: 0 start, 1 setup; per layer
+// l < 4 at 2 + 6 l: +0 first W landed, +1 first X word block complete, +2 first
+// MMA issued, +3 last MMA complete (drain), +4 last partial's reds issued,
+// +5 last step's X complete; 26 end.
+#define K1_MARK(i)                                                         \
+    do {                                                                   \
+        if ((i) < 32) atomicCAS(&k1_marks[(i)], 0ull, gtime());            \
+    } while (0)
+#define K1_SET(i)                                \
+    do {                                         \
+        if ((i) < 32) k1_marks[(i)] = gtime();    \
+    } while (0)
+// Per-step marks of CTA 0 (steps < 96): dbg[grid * 32 + g * 8 + i], i = 0 W issued,
+// 1 X issued, 2 W landed, 3 raw landed, 4 operand ready (converter), 5 MMA issued.
+#define K1_STEP(g, i)                                                                         \
+    do {                                                                                      \
+        if (a.dbg && blockIdx.x == 0 && (g) < 96) a.dbg[gridDim.x * 32 + (g) * 8 + (i)] = gtime(); \
+    } while (0)
+#define K1_WAIT(bar, parity, site, g)                          \
+    do {                                                       \
+        long long spins_ = 0;                                  \
+        while (!mbar_try((bar), (parity))) watchdog(spins_, (site), (g)); \
+    } while (0)
+#else
+#define K1_WAIT(bar, parity, site, g) mbar_wait((bar), (parity))
+#define K1_MARK(i) \
+    do {           \
+    } while (0)
+#define K1_SET(i) \
+    do {          \
+    } while (0)
+#define K1_STEP(g, i) \
+    do {              \
+    } while (0)
+#endif
+// Layer-output words once all K tiles of their feature tile are reduced into
+// them: w[i] is the copy at hand (from the bulk copy), p[i] its address; every
+// incomplete word is re-read from L2, all of them in flight at once, until each
+// count equals `need`.
+template <int kN>
+__device__ __forceinline__ void complete_words(unsigned long long (&w)[kN], const unsigned long long* const (&p)[kN],
+                                               unsigned need, int site = 0, int g = 0) {
+#ifdef GFX_K1_DEBUG
+    long long spins = 0;
+#else
+    (void)site;
+    (void)g;
+#endif
+    for (;;) {
+        bool done = true;
+#pragma unroll
+        for (int i = 0; i < kN; ++i) done &= (w[i] & kCountMask) == need;
+        if (done) return;
+        __nanosleep(32);
+#pragma unroll
+        for (int i = 0; i < kN; ++i)
+            if ((w[i] & kCountMask) != need) w[i] = ld_relaxed_u64(p[i]);
+#ifdef GFX_K1_DEBUG
+        watchdog(spins, site, g);
+#endif
     }
 }
-// Release/acquire fence at GPU scope (MEMBAR.ALL.GPU), not __threadfence()'s
-// sequentially consistent MEMBAR.SC.GPU: the dataflow flags only need
-// "writes before the flag are visible to whoever acquires it".
-__device__ __forceinline__ void fence_acq_rel_gpu() { asm volatile("fence.acq_rel.gpu;\n" ::: "memory"); }
-__device__ __forceinline__ void fence_proxy_async_global() {
-    asm volatile("fence.proxy.async.global;\n" ::: "memory");
-}
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(smem)), "l"(gmem) : "memory");
+__device__ __forceinline__ float decode_word(unsigned long long w) {
+    return __ll2float_rn(static_cast<long long>(w) >> kCountBits) * kFixInv;
 }
 __device__ __forceinline__ void epi_sync() { asm volatile("bar.sync 1, 128;\n" ::: "memory"); }
+__device__ __forceinline__ void conv_sync(int group) {
+    asm volatile("bar.sync %0, 128;\n" ::"r"(2 + group) : "memory");
+}
 __device__ __forceinline__ float rn_tf32(float v) {
     return __uint_as_float((__float_as_uint(v) + 0x1000u) & 0xFFFFE000u);
 }
@@ -130,578 +231,389 @@ __device__ __forceinline__ uint32_t sw128(int r, int c) {
     return static_cast<uint32_t>(r * 128 + ((((c >> 2) ^ (r & 7))) << 4) + (c & 3) * 4);
 }
 
-__device__ __forceinline__ unsigned long long gtime() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    return t;
-}
-// Per-step timeline of CTA 0 (GFX_TRACE_MLP): 8 %globaltimer marks per ring step.
-__device__ __forceinline__ void smark(unsigned long long* tr, int step, int i) {
-    if (tr == nullptr || blockIdx.x != 0 || step >= 64) return;
-    tr[static_cast<size_t>(gridDim.x) * 32 + step * 8 + i] = gtime();
-}
-// Per-CTA cycle accounting (GFX_TRACE_MLP): where each role's time goes.
-struct Prof {
-    long long t = 0;
-    __device__ __forceinline__ void start() { t = clock64(); }
-    __device__ __forceinline__ void stop(long long& acc) {
-        const long long n = clock64();
-        acc += n - t;
-        t = n;
-    }
+// This CTA's contiguous step range of a layer (stream-K split).
+struct Range {
+    int s0, s1;
 };
-__device__ __forceinline__ void prof_store(unsigned long long* tr, int i, long long v) {
-    if (tr) tr[static_cast<size_t>(gridDim.x) * 32 + 576 + blockIdx.x * 16 + i] = static_cast<unsigned long long>(v);
+__device__ __forceinline__ Range range_of(const MlpFwdLayer& ly, int cta, int grid) {
+    const long long steps = static_cast<long long>(ly.tiles) * ly.nkt;
+    return {static_cast<int>(steps * cta / grid), static_cast<int>(steps * (cta + 1) / grid)};
 }
-// Debug timeline (GFX_TRACE_MLP): %globaltimer per CTA at phase boundaries.
-__device__ __forceinline__ void mark(unsigned long long* tr, int i) {
-    if (tr == nullptr) return;
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    tr[blockIdx.x * 32 + i] = t;
-}
-
-struct Unit {
-    bool valid;
-    int tile, split, kt0, nkt, kt_total;
-};
-__device__ __forceinline__ Unit unit_of(const MlpFwdLayer& ly, int cta, int cluster) {
-    Unit u{};
-    if (cluster) {
-        // Cluster mode: the S splits of a tile are adjacent ranks of one cluster
-        // (S divides the cluster size), cluster c holds tiles c * (cluster / S) + ...
-        const int per = cluster / ly.splits, rank = cta % cluster, lt = rank / ly.splits;
-        u.tile = (cta / cluster) * per + lt;
-        u.split = rank % ly.splits;
-        u.valid = u.tile < ly.tiles;
-    } else {
-        const int units = ly.tiles * ly.splits;
-        u.valid = cta < units;
-        u.tile = cta % ly.tiles;
-        u.split = cta / ly.tiles;
-    }
-    if (!u.valid) return u;
-    u.kt_total = ly.K / kTileK;
-    u.kt0 = static_cast<int>((static_cast<long long>(u.kt_total) * u.split) / ly.splits);
-    const int kt1 = static_cast<int>((static_cast<long long>(u.kt_total) * (u.split + 1)) / ly.splits);
-    u.nkt = kt1 - u.kt0;
-    return u;
-}
-
-// Walk of one CTA's weight tiles over all layers (the W producer's order).
-struct WIter {
-    int l, it;
-    Unit u;
-};
-__device__ __forceinline__ bool witer_seek(const MlpFwdArgs& a, int cta, WIter& w) {
-    for (; w.l < a.L; ++w.l) {
-        w.u = unit_of(a.layer[w.l], cta, a.cluster);
-        if (w.u.valid) {
-            w.it = 0;
-            return true;
-        }
-    }
-    return false;
-}
-__device__ __forceinline__ bool witer_first(const MlpFwdArgs& a, int cta, WIter& w) {
-    w.l = 0;
-    return witer_seek(a, cta, w);
-}
-__device__ __forceinline__ bool witer_next(const MlpFwdArgs& a, int cta, WIter& w) {
-    if (++w.it < w.u.nkt) return true;
-    ++w.l;
-    return witer_seek(a, cta, w);
-}
-__device__ __forceinline__ uint64_t witer_off(const MlpFwdArgs& a, const WIter& w) {
-    return a.layer[w.l].w_off + (static_cast<uint64_t>(w.u.tile) * w.u.kt_total + w.u.kt0 + w.it) * kWBytes;
+// End of the segment (steps of one feature tile) that starts at s.
+__device__ __forceinline__ int seg_end(const MlpFwdLayer& ly, const Range& r, int s) {
+    const int e = (s / ly.nkt + 1) * ly.nkt;
+    return e < r.s1 ? e : r.s1;
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
     mlp_forward_kernel(const __grid_constant__ MlpFwdArgs a) {
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    __shared__ __align__(8) uint64_t w_full[kSlots], ready[kSlots], step_done[kSlots], raw_full[kSlots];
+    __shared__ __align__(8) uint64_t w_full[kSlots], raw_full[kSlots], ready[kSlots], step_done[kSlots];
     __shared__ __align__(8) uint64_t tfull[kAccBufs], tempty[kAccBufs];
     __shared__ uint32_t tmem_base_s;
     __shared__ uint32_t pt[GFX_MAX_PAGES];
-    __shared__ float red[2][4];
-    // Cluster mode: split-K partials arrive by st.async into the gather area
-    // (two 16 KB parities), completing rbar[parity]; consumed[parity] = the last
-    // layer whose partials this CTA has read from that parity (senders poll it).
-    __shared__ __align__(8) uint64_t rbar[2];
-    __shared__ int consumed[2];
+    __shared__ float red_s[2][4];
+#ifdef GFX_K1_DEBUG
+    __shared__ unsigned long long k1_marks[32];
+    if (threadIdx.x < 32) k1_marks[threadIdx.x] = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) K1_MARK(0);
+#endif
 
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int lane = tid & 31;
     const int cta = blockIdx.x;
+    const int grid = a.grid;
     const int L = a.L;
-    unsigned* const cnt = a.cnt + (a.epoch & 1u) * kCntBank;
 
-    if (tid == 0) mark(a.trace, 0);
     for (int i = tid; i < static_cast<int>(a.pt.n); i += kThreads) pt[i] = a.pt.page[i];
     if (tid == 0) {
         for (int s = 0; s < kSlots; ++s) {
             mbar_init(&w_full[s], 1);
-            // ready: the 4 converter warps (W_lo in TMEM; they saw w_full) + the X
-            // producer's arrive.expect_tx, completed by the X bulk copy's bytes —
-            // the MMA thread waits on ONE barrier per step (a try_wait costs ~90
-            // cycles even when the phase is already complete).
-            mbar_init(&ready[s], 5);
+            mbar_init(&raw_full[s], 1);
+            mbar_init(&ready[s], 4);      // the 4 converter warps of the step's group
             mbar_init(&step_done[s], 1);  // MMA commit: W, X and W_lo of the step consumed
-            mbar_init(&raw_full[s], 1);   // layer-0 raw input tile landed
         }
         for (int b = 0; b < kAccBufs; ++b) {
             mbar_init(&tfull[b], 1);
             mbar_init(&tempty[b], 4);  // one arrival per drain warp
         }
-        mbar_init(&rbar[0], 1);
-        mbar_init(&rbar[1], 1);
-        consumed[0] = -2;
-        consumed[1] = -1;
         mbar_fence_init();
         tma_prefetch_desc(&a.tmap_in);
     }
     if (warp == 1) tmem_alloc<kTmemCols>(&tmem_base_s);
     tc_fence_before();
     __syncthreads();
-    if (a.cluster) cluster_sync();  // every CTA's barriers exist before any remote access
     tc_fence_after();
     const uint32_t tmem = tmem_base_s;
-    if (tid == 0) mark(a.trace, 1);
+    if (tid == 0) K1_MARK(1);
 
     if (warp == 0) {
         // ---------------- W producer: never waits on activations ----------------
         if (lane == 0) {
-            long long pw = 0;
-            Prof pr;
-            WIter cur{};
-            bool have = witer_first(a, cta, cur);
-            for (int step = 0; have; ++step) {
-                const int s = step % kSlots;
-                if (step >= kSlots) {
-                    pr.start();
-                    mbar_wait(&step_done[s], ((step / kSlots) & 1) ^ 1);
-                    pr.stop(pw);
+            int g = 0;
+            for (int l = 0; l < L; ++l) {
+                const MlpFwdLayer& ly = a.layer[l];
+                const Range r = range_of(ly, cta, grid);
+                for (int s = r.s0; s < r.s1;) {
+                    const int slot = g % kSlots;
+                    const bool pair = (g & 1) == 0 && s + 1 < r.s1;  // steps g, g+1 of this layer
+                    if (g >= kSlots) K1_WAIT(&step_done[slot], ((g / kSlots) & 1) ^ 1, 1, g);
+                    if (pair && g + 1 >= kSlots) K1_WAIT(&step_done[slot + 1], (((g + 1) / kSlots) & 1) ^ 1, 1, g + 1);
+                    K1_STEP(g, 0);
+                    const uint64_t v = ly.w_off + static_cast<uint64_t>(s) * kWBytes;
+                    const char* src = translate(a.arena, pt, v);
+                    uint8_t* dst = smem + slot * kWBytes;
+                    mbar_arrive_expect_tx(&w_full[slot], pair ? 2 * kWBytes : kWBytes);
+                    if (pair && translate(a.arena, pt, v + kWBytes) == src + kWBytes) {
+                        tma_bulk_g2s(dst, src, 2 * kWBytes, &w_full[slot]);
+                    } else {
+                        tma_bulk_g2s(dst, src, kWBytes, &w_full[slot]);
+                        if (pair) tma_bulk_g2s(dst + kWBytes, translate(a.arena, pt, v + kWBytes), kWBytes, &w_full[slot]);
+                    }
+                    if (pair) mbar_arrive(&w_full[slot + 1]);
+                    s += pair ? 2 : 1;
+                    g += pair ? 2 : 1;
                 }
-                smark(a.trace, step, 0);
-                mbar_arrive_expect_tx(&w_full[s], kWBytes);
-                tma_bulk_g2s(smem + s * kSlotBytes, translate(a.arena, pt, witer_off(a, cur)), kWBytes, &w_full[s]);
-                have = witer_next(a, cta, cur);
             }
-            prof_store(a.trace, 8, pw);
         }
     } else if (warp == 14) {
-        // ---------------- X producer: the operand block of each step ----------------
-        // Layer 0: a 2-D TMA brings the raw 32 x 32 fp32 input tile into the lower
-        // half of the slot (rows 32-63 of the SWIZZLE_128B block, same chunk
-        // permutation), then the warp splits it in place (lane = batch row):
-        // X_hi to rows 0-31, X_lo over the raw row it read. All of a CTA's
-        // layer-0 tiles are requested up front (they fit the first ring slots).
-        // Later layers: dataflow wait on the previous layer's tile, then one 8 KB
-        // bulk copy of the operand block its reducers wrote.
-        int step = 0;
-        long long px[2] = {0, 0};
-        Prof pr;
-        for (int l = 0; l < L; ++l) {
-            const MlpFwdLayer& ly = a.layer[l];
-            const Unit u = unit_of(ly, cta, a.cluster);
-            if (!u.valid) continue;
-            if (l == 0 && lane < (u.nkt < kSlots ? u.nkt : kSlots)) {
-                // one lane per tile: a thread's TMA requests are served one after another
-                const int it = lane;
-                uint8_t* xs = smem + it * kSlotBytes + kWBytes;
-                mbar_arrive_expect_tx(&raw_full[it], kXBytes / 2);
-                tma_tile2d_g2s(xs + kXBytes / 2, &a.tmap_in, (u.kt0 + it) * kTileK, 0, &raw_full[it]);
-            }
-            __syncwarp();
-            if (l > 0) {
-                // Two lanes issue alternate steps, each its own loop (a thread's TMA
-                // requests are served one after another, ~500 cycles each: one lane
-                // alone capped the post-boundary step rate at ~0.43 µs). Each lane
-                // polls the dataflow counter of a source tile the first time one of
-                // its steps needs it.
-                const int step0 = step;
-                if (lane < 2) {
-                    int ready_src = -1;  // last source tile this lane knows complete
-                    for (int it = lane; it < u.nkt; it += 2) {
-                        const int st = step0 + it, s = st % kSlots, kt = u.kt0 + it;
-                        if (st >= kSlots) mbar_wait(&step_done[s], ((st / kSlots) & 1) ^ 1);
-                        const int src = kt >> 2;  // the previous layer's feature tile holding these 32 inputs
-                        if (src != ready_src) {
-                            wait_count(cnt + kCntDone + (l - 1) * 64 + src, static_cast<unsigned>(a.layer[l - 1].splits));
-                            fence_proxy_async_global();
-                            ready_src = src;
-                        }
-                        smark(a.trace, st, 1);
-                        mbar_arrive_expect_tx(&ready[s], kXBytes);
-                        tma_bulk_g2s(smem + s * kSlotBytes + kWBytes,
-                                     a.opnd + static_cast<size_t>(l) * kMlpOpndLayerBytes + static_cast<size_t>(kt) * kXBytes,
-                                     kXBytes, &ready[s]);
-                    }
-                }
-                __syncwarp();
-                step = step0 + u.nkt;
-                continue;
-            }
-            for (int it = 0; it < u.nkt; ++it, ++step) {
-                const int s = step % kSlots;
-                const int kt = u.kt0 + it;
-                uint8_t* xs = smem + s * kSlotBytes + kWBytes;
-                pr.start();
-                if (step >= kSlots) mbar_wait(&step_done[s], ((step / kSlots) & 1) ^ 1);
-                pr.stop(px[0]);
-                if (l == 0) {
-                    if (it >= kSlots && lane == 0) {  // wider than the ring: request this tile now
-                        mbar_arrive_expect_tx(&raw_full[s], kXBytes / 2);
-                        tma_tile2d_g2s(xs + kXBytes / 2, &a.tmap_in, kt * kTileK, 0, &raw_full[s]);
-                    }
-                    __syncwarp();
-                    mbar_wait(&raw_full[s], (it / kSlots) & 1);
-                    if (lane == 0) smark(a.trace, step, 6);
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        float4* p = reinterpret_cast<float4*>(xs + sw128(kRows + lane, 4 * j));
-                        const float4 v = *p;
-                        float4 hi, lo;
-                        hi.x = rn_tf32(v.x);
-                        hi.y = rn_tf32(v.y);
-                        hi.z = rn_tf32(v.z);
-                        hi.w = rn_tf32(v.w);
-                        lo.x = v.x - hi.x;
-                        lo.y = v.y - hi.y;
-                        lo.z = v.z - hi.z;
-                        lo.w = v.w - hi.w;
-                        *reinterpret_cast<float4*>(xs + sw128(lane, 4 * j)) = hi;
-                        *p = lo;
-                    }
-                    fence_proxy_async_smem();  // generic-proxy writes -> tensor core reads
-                    __syncwarp();
-                    if (lane == 0) {
-                        smark(a.trace, step, 1);
-                        mbar_arrive(&ready[s]);
-                    }
-                    continue;
-                }
-            }
-        }
+        // ---------------- X producer: the raw input block of each step ----------------
         if (lane == 0) {
-            prof_store(a.trace, 9, px[0]);
-            prof_store(a.trace, 10, px[1]);
+            int g = 0;
+            for (int l = 0; l < L; ++l) {
+                const MlpFwdLayer& ly = a.layer[l];
+                const Range r = range_of(ly, cta, grid);
+                const unsigned long long* src_act = l > 0 ? a.act + a.layer[l - 1].act_off : nullptr;
+                int seen = -1;  // last source tile seen complete
+                // Wait until source tile kt >> 2 shows a complete word (its partials have landed).
+                auto await_source = [&](int kt, int g_) {
+                    const int src = kt >> 2;  // the previous layer's feature tile holding these 32 inputs
+                    if (src == seen) return;
+                    const unsigned long long* w = src_act + static_cast<size_t>(kt) * (kTileK * kRows) + 32 * 32 - 1;
+                    unsigned long long v[1] = {ld_relaxed_u64(w)};
+                    const unsigned long long* pp[1] = {w};
+                    complete_words(v, pp, static_cast<unsigned>(a.layer[l - 1].nkt), 10, g_);
+                    seen = src;
+                };
+                for (int s = r.s0; s < r.s1;) {
+                    const int slot = g % kSlots, kt = s % ly.nkt;
+                    const bool pair = l > 0 && (g & 1) == 0 && s + 1 < r.s1;
+                    if (g >= kSlots) K1_WAIT(&step_done[slot], ((g / kSlots) & 1) ^ 1, 2, g);
+                    if (pair && g + 1 >= kSlots) K1_WAIT(&step_done[slot + 1], (((g + 1) / kSlots) & 1) ^ 1, 2, g + 1);
+                    uint8_t* xs = smem + kXRing + slot * kXBytes;
+                    K1_STEP(g, 1);
+                    if (l == 0) {
+                        mbar_arrive_expect_tx(&raw_full[slot], kRaw0Bytes);
+                        tma_tile2d_g2s(xs + kRaw0Bytes, &a.tmap_in, kt * kTileK, 0, &raw_full[slot]);
+                    } else {
+                        const int kt1 = (s + 1) % ly.nkt;  // the pair's second K tile
+                        await_source(kt, g);
+                        if (pair) await_source(kt1, g + 1);
+                        mbar_arrive_expect_tx(&raw_full[slot], pair ? 2 * kRawBytes : kRawBytes);
+                        const unsigned long long* b0 = src_act + static_cast<size_t>(kt) * (kTileK * kRows);
+                        if (pair && kt1 == kt + 1) {
+                            tma_bulk_g2s(xs, b0, 2 * kRawBytes, &raw_full[slot]);
+                        } else {
+                            tma_bulk_g2s(xs, b0, kRawBytes, &raw_full[slot]);
+                            if (pair)
+                                tma_bulk_g2s(xs + kRawBytes, src_act + static_cast<size_t>(kt1) * (kTileK * kRows), kRawBytes,
+                                             &raw_full[slot]);
+                        }
+                        if (pair) mbar_arrive(&raw_full[slot + 1]);
+                    }
+                    s += pair ? 2 : 1;
+                    g += pair ? 2 : 1;
+                }
+            }
         }
     } else if (warp == 1 || warp == 15) {
         // ---------------- MMA issuers: two warps take alternate accumulator chunks ----------------
-        // Each issuing warp loops converged (one elected lane issues). One issuer
-        // alone left the tensor pipe idle during its per-step barrier waits and
-        // commits (~0.3 us of every 0.6 us step); with two, one issues while the
-        // other waits. Chunks of one unit accumulate in different TMEM buffers
-        // and are summed by the drain in chunk order, so the result is the same
-        // whichever issuer ran first.
+        // Each issuing warp loops converged (one elected lane issues). With two,
+        // one issues while the other waits on its barriers. Chunks never span
+        // two tiles; chunks of one tile accumulate in different TMEM buffers and
+        // are summed by the drain in chunk order.
         const int issuer = warp == 1 ? 0 : 1;
         constexpr uint32_t idesc64 = umma_idesc<kTileM, 2 * kRows, 2>();  // TF32 x TF32 -> F32, N = 64
         constexpr uint32_t idesc32 = umma_idesc<kTileM, kRows, 2>();      // N = 32
-        int step = 0, chunk = 0;
-        long long pw[6] = {0, 0, 0, 0, 0, 0};
-        Prof pr;
-        pr.start();
+        int g = 0, chunk = 0;
         for (int l = 0; l < L; ++l) {
-            const Unit u = unit_of(a.layer[l], cta, a.cluster);
-            if (!u.valid) continue;
-            for (int c0 = 0; c0 < u.nkt; c0 += kChunk, ++chunk) {
-                const int len = u.nkt - c0 < kChunk ? u.nkt - c0 : kChunk;
-                if ((chunk & 1) != issuer) {
-                    step += len;
-                    continue;
-                }
-                const int buf = chunk % kAccBufs;
-                const uint32_t acc = tmem + static_cast<uint32_t>(buf * kAccCols);
-                if (chunk >= kAccBufs) mbar_wait(&tempty[buf], ((chunk / kAccBufs) & 1) ^ 1);
-                pr.stop(pw[0]);
-                for (int j = 0; j < len; ++j, ++step) {
-                    const int s = step % kSlots;
-                    // W_lo staged (the converters waited on w_full) and X landed.
-                    mbar_wait(&ready[s], (step / kSlots) & 1);
-                    tc_fence_after();
-                    pr.stop(pw[1]);
-                    if (lane == 0) smark(a.trace, step, 4);
-                    if (lane == 0 && c0 + j == 0 && l < 6) mark(a.trace, 2 + 4 * l);
-                    const uint8_t* w = smem + s * kSlotBytes;
-                    const uint64_t bx = umma_desc_sw128(w + kWBytes, 0), aw = umma_desc_sw128(w, 0);
-                    const uint32_t lo = tmem + kLoBase + static_cast<uint32_t>(kTileK * s);
-#pragma unroll
-                    for (int kk = 0; kk < kTileK / 8; ++kk) {
-                        // +kk*32 bytes = +2 in the descriptor's 16-byte address units
-                        umma_tf32_elect(acc, aw + 2 * kk, bx + 2 * kk, idesc64, (j == 0 && kk == 0) ? 0u : 1u);
-                        if (!(a.ablate & 2)) umma_tf32_ts_elect(acc, lo + static_cast<uint32_t>(8 * kk), bx + 2 * kk, idesc32, 1u);
+            const MlpFwdLayer& ly = a.layer[l];
+            const Range r = range_of(ly, cta, grid);
+            for (int s = r.s0; s < r.s1;) {
+                const int e = seg_end(ly, r, s);
+                for (; s < e; ++chunk) {
+                    const int len = e - s < kChunk ? e - s : kChunk;
+                    if ((chunk & 1) != issuer) {
+                        s += len;
+                        g += len;
+                        continue;
                     }
-                    pr.stop(pw[5]);
-                    if (lane == 0) smark(a.trace, step, 5);
-                    umma_commit_elect(&step_done[s]);  // W slot, X slot and W_lo stage s free once these MMAs retire
-                    if (lane == 0 && c0 + j == u.nkt - 1 && l < 6) mark(a.trace, 3 + 4 * l);
-                    pr.stop(pw[4]);
+                    const int buf = chunk % kAccBufs;
+                    const uint32_t acc = tmem + static_cast<uint32_t>(buf * kAccCols);
+                    if (chunk >= kAccBufs) K1_WAIT(&tempty[buf], ((chunk / kAccBufs) & 1) ^ 1, 4, g);
+                    for (int j = 0; j < len; ++j, ++s, ++g) {
+                        const int slot = g % kSlots;
+                        K1_WAIT(&ready[slot], (g / kSlots) & 1, 5, g);  // W landed, W_lo staged, X operand built
+                        tc_fence_after();
+                        if (l < 4 && lane == 0) K1_MARK(4 + 6 * l);
+                        if (l == 1 && lane == 0 && s == r.s0) K1_MARK(29);
+                        const uint64_t bx = umma_desc_sw128(smem + kXRing + slot * kXBytes, 0);
+                        const uint64_t aw = umma_desc_sw128(smem + slot * kWBytes, 0);
+                        const uint32_t lo = tmem + kLoBase + static_cast<uint32_t>(kTileK * slot);
+#pragma unroll
+                        for (int kk = 0; kk < kTileK / 8; ++kk) {
+                            // +kk*32 bytes = +2 in the descriptor's 16-byte address units
+                            umma_tf32_elect(acc, aw + 2 * kk, bx + 2 * kk, idesc64, (j == 0 && kk == 0) ? 0u : 1u);
+                            umma_tf32_ts_elect(acc, lo + static_cast<uint32_t>(8 * kk), bx + 2 * kk, idesc32, 1u);
+                        }
+                        umma_commit_elect(&step_done[slot]);  // slot + W_lo stage free once these MMAs retire
+                        if (lane == 0) K1_STEP(g, 5);
+                    }
+                    umma_commit_elect(&tfull[buf]);
                 }
-                umma_commit_elect(&tfull[buf]);
             }
         }
-        if (lane == 0 && issuer == 0) {
-            for (int i = 0; i < 5; ++i) prof_store(a.trace, i, pw[i]);
-            prof_store(a.trace, 13, pw[5]);
-            prof_store(a.trace, 15, step);
-        }
     } else if (warp < 10) {
-        // ---------------- converters: W_lo = W - trunc_tf32(W) into TMEM stage s ----------------
+        // ---------------- converters: W_lo -> TMEM stage, raw X -> operand ----------------
         const int group = (warp - 2) >> 2;
         const int q = warp & 3;            // TMEM lane quarter of this warp
         const int r = q * 32 + lane;       // weight row of the tile = TMEM lane
-        const uint32_t mask = (a.ablate & 1) ? 0u : 0xFFFFE000u;
-        int step = 0;
-        long long pc[3] = {0, 0, 0};
-        Prof pr;
-        pr.start();
+        int g = 0;
         for (int l = 0; l < L; ++l) {
-            const Unit u = unit_of(a.layer[l], cta, a.cluster);
-            if (!u.valid) continue;
-            for (int it = 0; it < u.nkt; ++it, ++step) {
-                if ((step & 1) != group) continue;
-                const int s = step % kSlots;
-                mbar_wait(&w_full[s], (step / kSlots) & 1);
-                pr.stop(pc[0]);
-                if (lane == 0 && q == 2) smark(a.trace, step, 2);
-                // Stage s of the W_lo ring was last read by the MMAs of step - kSlots,
-                // which also freed the landing slot this tile arrived in: step_done
-                // of that phase is complete already (the producer waited on it).
-                if (a.ablate & 4) {
-                    __syncwarp();
-                    if (lane == 0) mbar_arrive(&ready[s]);
-                    continue;
-                }
-                const float4* wrow = reinterpret_cast<const float4*>(smem + s * kSlotBytes + r * 128);
+            const MlpFwdLayer& ly = a.layer[l];
+            const Range rg = range_of(ly, cta, grid);
+            for (int s = rg.s0; s < rg.s1; ++s, ++g) {
+                if ((g & 1) != group) continue;
+                const int slot = g % kSlots;
+                uint8_t* xs = smem + kXRing + slot * kXBytes;
+                // The second step of a producer pair (odd g, not the layer's first step
+                // here) landed with the first: wait on the first slot's barrier.
+                const bool second = (g & 1) && s > rg.s0;
+                K1_WAIT(&w_full[second ? slot - 1 : slot], (g / kSlots) & 1, 6, g);
+                if (q == 0 && lane == 0) K1_STEP(g, 2);
+                if (l < 4 && lane == 0) K1_MARK(2 + 6 * l);
+                // Stage `slot` of the W_lo ring was last read by the MMAs of step
+                // g - kSlots, which the producer waited on before this tile landed.
+                const float4* wrow = reinterpret_cast<const float4*>(smem + slot * kWBytes + r * 128);
                 float wlo[32];
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const float4 v = wrow[j ^ (r & 7)];
-                    const float e[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const float hi = (a.ablate & 1) ? rn_tf32(e[i]) : __uint_as_float(__float_as_uint(e[i]) & mask);
-                        wlo[4 * j + i] = e[i] - hi;
-                    }
+                    wlo[4 * j + 0] = v.x - __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+                    wlo[4 * j + 1] = v.y - __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+                    wlo[4 * j + 2] = v.z - __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+                    wlo[4 * j + 3] = v.w - __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
                 }
-                pr.stop(pc[2]);
                 tc_fence_after();
-                tmem_st_32x32b_x32(tmem + (static_cast<uint32_t>(q * 32) << 16) + kLoBase + static_cast<uint32_t>(kTileK * s), wlo);
+                tmem_st_32x32b_x32(tmem + (static_cast<uint32_t>(q * 32) << 16) + kLoBase + static_cast<uint32_t>(kTileK * slot), wlo);
+                // X: warp q converts K columns 8q .. 8q+7 (16-byte chunks 2q, 2q+1) of all 32 rows; lane = batch row.
+                K1_WAIT(&raw_full[second && l > 0 ? slot - 1 : slot], (g / kSlots) & 1, 7, g);
+                if (q == 0 && lane == 0) K1_STEP(g, 3);
+                if (l == 0 && lane == 0) {
+                    K1_MARK(3);
+                    K1_SET(7);
+                }
+                float4 xv[2];
+                if (l == 0) {
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) xv[h] = *reinterpret_cast<const float4*>(xs + kRaw0Bytes + sw128(lane, 8 * q + 4 * h));
+                } else {
+                    // Fixed-point feature-major block: raw[f][b] at f * 256 + b * 8; words whose
+                    // count is short are re-read from L2. Hidden inputs get the ReLU here.
+                    const unsigned long long* rawq = reinterpret_cast<const unsigned long long*>(xs);
+                    const unsigned long long* gsrc =
+                        a.act + a.layer[l - 1].act_off + static_cast<size_t>(s % ly.nkt) * (kTileK * kRows);
+                    const unsigned need = static_cast<unsigned>(a.layer[l - 1].nkt);
+                    unsigned long long wv[8];
+                    const unsigned long long* wp[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) {
+                        wv[i] = rawq[(8 * q + i) * 32 + lane];
+                        wp[i] = gsrc + (8 * q + i) * 32 + lane;
+                    }
+                    complete_words(wv, wp, need, 3, g);
+                    float x[8];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i) x[i] = fmaxf(decode_word(wv[i]), 0.f);
+                    if (l < 4 && lane == 0) {
+                        K1_MARK(3 + 6 * l);
+                        K1_SET(7 + 6 * l);
+                    }
+                    xv[0] = make_float4(x[0], x[1], x[2], x[3]);
+                    xv[1] = make_float4(x[4], x[5], x[6], x[7]);
+                    conv_sync(group);  // every warp of the group has read its raw rows before the operand overwrites them
+                    if (l == 1 && lane == 0) K1_MARK(27);
+                }
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    float4 hi, lo;
+                    hi.x = rn_tf32(xv[h].x);
+                    hi.y = rn_tf32(xv[h].y);
+                    hi.z = rn_tf32(xv[h].z);
+                    hi.w = rn_tf32(xv[h].w);
+                    lo.x = xv[h].x - hi.x;
+                    lo.y = xv[h].y - hi.y;
+                    lo.z = xv[h].z - hi.z;
+                    lo.w = xv[h].w - hi.w;
+                    *reinterpret_cast<float4*>(xs + sw128(lane, 8 * q + 4 * h)) = hi;
+                    *reinterpret_cast<float4*>(xs + sw128(kRows + lane, 8 * q + 4 * h)) = lo;
+                }
+                fence_proxy_async_smem();  // generic-proxy writes -> tensor core reads
                 tmem_st_wait();
                 tc_fence_before();
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&ready[s]);
-                pr.stop(pc[2]);
-                if (lane == 0 && q == 2) smark(a.trace, step, 3);
+                if (lane == 0) mbar_arrive(&ready[slot]);
+                if (l == 1 && lane == 0) K1_MARK(28);
+                if (q == 0 && lane == 0) K1_STEP(g, 4);
             }
         }
-        if (warp == 2 && lane == 0)
-            for (int i = 0; i < 3; ++i) prof_store(a.trace, 5 + i, pc[i]);
     } else if (warp < 14) {
         // ---------------- drain + epilogue warps ----------------
         const int ct = tid - 320;          // 0..127
         const int q = warp & 3;            // TMEM lane quarter (warps 10..13 -> 2,3,0,1)
         const int fl = q * 32 + lane;      // feature row within the tile
 
-        {  // the other counter bank, for the next launch (see kCntBank)
-            unsigned* other = a.cnt + ((a.epoch & 1u) ^ 1u) * kCntBank;
-            for (int i = cta * 128 + ct; i < kCntBank; i += gridDim.x * 128) other[i] = 0;
-        }
+        // The other parity's buffer, for the next launch (stream-ordered after this one).
+        for (uint32_t i = static_cast<uint32_t>(cta * 128 + ct); i < a.clear_vec; i += static_cast<uint32_t>(grid * 128))
+            a.act_clear[i] = make_uint4(0u, 0u, 0u, 0u);
+        // Staging (after the ring): half h holds rows 16h..16h+15 as [128 features][128 B], 16-byte chunk j of
+        // feature f at j ^ (f & 7) (the TMA SWIZZLE_128B image); warp q owns features 32q..32q+31 of both halves.
+        uint8_t* const stg = smem + kStageOff;
+
         int chunk = 0;
-        uint32_t rph = 0;  // rbar phase bits (cluster mode)
-        long long pd[2] = {0, 0};
-        Prof pr;
-        auto mark_consumed = [&](int l) {  // cluster mode: parity l & 1 of this CTA's buffer is free again
-            if (a.cluster && ct == 0) {
-                asm volatile("fence.acq_rel.cluster;\n" ::: "memory");
-                *reinterpret_cast<volatile int*>(&consumed[l & 1]) = l;
-            }
-        };
         for (int l = 0; l < L; ++l) {
             const MlpFwdLayer& ly = a.layer[l];
-            const Unit u = unit_of(ly, cta, a.cluster);
-            if (!u.valid || ly.splits == 1) mark_consumed(l);  // nobody sends this CTA partials of layer l
-            if (!u.valid) continue;
-            pr.start();
+            const Range r = range_of(ly, cta, grid);
             const bool last = l == L - 1;
-            const int N = ly.N;
-            const int f = u.tile * kTileM + fl;
-            const bool valid = f < N;  // rows >= N are the zero padding of the last weight tile
-            const float bias = valid ? *reinterpret_cast<const float*>(translate(a.arena, pt, ly.b_off + 4ull * f)) : 0.f;
-            float acc[kRows];
+            for (int s = r.s0; s < r.s1;) {
+                const int e = seg_end(ly, r, s);
+                const int tile = s / ly.nkt;
+                const int f = tile * kTileM + fl;
+                // Bias row fetched before the MMAs finish (off the boundary's critical path).
+                const float bias = (s % ly.nkt) == 0 && f < ly.N
+                                       ? *reinterpret_cast<const float*>(translate(a.arena, pt, ly.b_off + 4ull * f))
+                                       : 0.f;
+                const unsigned long long count = static_cast<unsigned long long>(e - s);  // K tiles of this partial
+                float acc[kRows];
 #pragma unroll
-            for (int b = 0; b < kRows; ++b) acc[b] = 0.f;
-            const int nch = (u.nkt + kChunk - 1) / kChunk;
-            for (int c = 0; c < nch; ++c, ++chunk) {
-                mbar_wait(&tfull[chunk % kAccBufs], (chunk / kAccBufs) & 1);
-                pr.stop(pd[0]);
-                if (ct == 0 && a.trace && cta == 0 && chunk < 32) a.trace[static_cast<size_t>(gridDim.x) * 32 + 512 + chunk] = gtime();
-                tc_fence_after();
-                float ph[kRows], pl[kRows];
-                const uint32_t src = tmem + static_cast<uint32_t>((chunk % kAccBufs) * kAccCols) + (static_cast<uint32_t>(q * 32) << 16);
-                tmem_ld_32x32b_x32(src + kRows, pl);  // products with X_lo (small)
-                tmem_ld_32x32b_x32(src, ph);
+                for (int b = 0; b < kRows; ++b) acc[b] = 0.f;
+                for (; s < e; ++chunk) {
+                    const int len = e - s < kChunk ? e - s : kChunk;
+                    s += len;
+                    K1_WAIT(&tfull[chunk % kAccBufs], (chunk / kAccBufs) & 1, 8, chunk);
+                    tc_fence_after();
+                    float ph[kRows], pl[kRows];
+                    const uint32_t src = tmem + static_cast<uint32_t>((chunk % kAccBufs) * kAccCols) + (static_cast<uint32_t>(q * 32) << 16);
+                    tmem_ld_32x32b_x32(src + kRows, pl);  // products with X_lo (small)
+                    tmem_ld_32x32b_x32(src, ph);
 #pragma unroll
-                for (int b = 0; b < kRows; ++b) acc[b] += ph[b] + pl[b];
-                tc_fence_before();
+                    for (int b = 0; b < kRows; ++b) acc[b] += ph[b] + pl[b];
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&tempty[chunk % kAccBufs]);
+                }
+                if (l < 4 && ct == 0 && e == r.s1) K1_SET(5 + 6 * l);
+                if (lane == 0) bulk_wait_group_read<0>();  // the previous segment's reductions have read the staging
                 __syncwarp();
-                if (lane == 0) mbar_arrive(&tempty[chunk % kAccBufs]);
-            }
-
-            if (ct == 0 && l < 6) mark(a.trace, 4 + 4 * l);
-            // Where row b of feature f goes.
-            char* const nxt = last ? nullptr : a.opnd + static_cast<size_t>(l + 1) * kMlpOpndLayerBytes + static_cast<size_t>(f >> 5) * kXBytes;
-            auto emit = [&](int b, float v) {
-                v += bias;
-                if (!last) {
-                    v = fmaxf(v, 0.f);
-                    if (valid) {
-                        const float hi = rn_tf32(v);
-                        *reinterpret_cast<float*>(nxt + sw128(b, f & 31)) = hi;
-                        *reinterpret_cast<float*>(nxt + sw128(kRows + b, f & 31)) = v - hi;
-                    }
-                } else if (valid) {
-                    a.logits[static_cast<size_t>(b) * N + f] = v;
-                }
-            };
-            const int S = ly.splits;
-            if (S == 1) {
 #pragma unroll
-                for (int b = 0; b < kRows; ++b) emit(b, acc[b]);
-            } else if (a.cluster) {
-                // The tile's S splits are cluster ranks base .. base + S - 1; split o
-                // owns rows b = o (mod S). Every split st.asyncs its partial rows into
-                // the owner's receive buffer [src split][row / S][feature] (a warp's
-                // 32 features of a row = 128 contiguous bytes), completing the
-                // owner's rbar; the owner sums in split order. No global round trip.
-                const int par = l & 1, per = kRows / S;
-                const int base = cta % a.cluster - u.split;
-                float* rb = reinterpret_cast<float*>(smem + kSlots * kSlotBytes) + par * (kRows * kTileM);
-                if (ct < S) {  // the destination's parity buffer was read for layer l - 2
-                    const uint32_t ra = mapa_u32(&consumed[par], static_cast<uint32_t>(base + ct));
-                    while (ld_acquire_cluster_s32(ra) < l - 2) {
-                    }
+                for (int j = 0; j < kRows / 2; ++j) {
+                    const unsigned long long q0 =
+                        (static_cast<unsigned long long>(__float2ll_rn((acc[2 * j] + bias) * kFixScale)) << kCountBits) + count;
+                    const unsigned long long q1 =
+                        (static_cast<unsigned long long>(__float2ll_rn((acc[2 * j + 1] + bias) * kFixScale)) << kCountBits) +
+                        count;
+                    *reinterpret_cast<ulonglong2*>(stg + (j >> 3) * (kStageBytes / 2) + fl * 128 + (((j & 7) ^ (fl & 7)) << 4)) =
+                        make_ulonglong2(q0, q1);
                 }
-                epi_sync();
-                if (ct == 0) {
-                    if (l == 0) mark(a.trace, 18);
-                    mbar_arrive_expect_tx(&rbar[par], kRows * kTileM * 4);
-                }
-                const uint32_t rb_mine = smem_u32(rb) + static_cast<uint32_t>((u.split * per * kTileM + fl) * 4);
+                fence_proxy_async_smem();  // generic-proxy writes -> the TMA engine's reads
+                __syncwarp();
+                if (lane == 0 && tile * kTileM + q * 32 < ly.N) {  // rows >= N: zero padding, clipped by the map
 #pragma unroll
-                for (int b = 0; b < kRows; ++b) {
-                    const int o = b % S, jj = b / S;
-                    const uint32_t rank = static_cast<uint32_t>(base + o);
-                    uint32_t dst, mb;
-                    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(dst) : "r"(rb_mine + jj * kTileM * 4), "r"(rank));
-                    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(mb) : "r"(smem_u32(&rbar[par])), "r"(rank));
-                    st_async_f32(dst, acc[b], mb);
+                    for (int h = 0; h < 2; ++h)
+                        tma_reduce_add_2d(&a.tmap_out[l], 16 * h, tile * kTileM + q * 32, stg + h * (kStageBytes / 2) + q * 4096);
+                    bulk_commit_group();
                 }
-                mbar_wait(&rbar[par], (rph >> par) & 1u);
-                rph ^= 1u << par;
-                if (ct == 0 && l < 2) mark(a.trace, 26 + 2 * l);
-                for (int jj = 0; jj < per; ++jj) {
-                    float v = 0.f;
-                    for (int sp = 0; sp < S; ++sp) v += rb[(sp * per + jj) * kTileM + fl];
-                    emit(u.split + jj * S, v);
-                }
-                epi_sync();  // every thread has read the buffer
-                mark_consumed(l);
-                if (ct == 0 && l < 2) mark(a.trace, 27 + 2 * l);
-            } else {
-                // Publish this unit's partial [32][128], wait for the tile's
-                // siblings (co-resident: cooperative launch), reduce rows
-                // b = split (mod S) in fixed split order.
-                float* tp = a.part + static_cast<size_t>(l) * kMlpPartLayerFloats +
-                            static_cast<size_t>(u.tile) * S * (kRows * kTileM);
-                float* mine = tp + static_cast<size_t>(u.split) * (kRows * kTileM);
-#pragma unroll
-                for (int b = 0; b < kRows; ++b) __stcg(mine + b * kTileM + fl, acc[b]);
-                epi_sync();  // CTA-scope ordering; thread 0's gpu fence is cumulative over it
-                if (ct == 0) {
-                    if (l == 0) mark(a.trace, 18);
-                    fence_acq_rel_gpu();
-                    if (l == 0) mark(a.trace, 19);
-                    atomicAdd(cnt + kCntArrive + l * 64 + u.tile, 1u);
-                    if (l == 0) mark(a.trace, 20);
-                    wait_count(cnt + kCntArrive + l * 64 + u.tile, static_cast<unsigned>(S));  // acquire
-                    if (l == 0) mark(a.trace, 21);
-                }
-                epi_sync();
-                if (ct == 0 && l < 2) mark(a.trace, 26 + 2 * l);
-                // One round of 16-byte cp.async gathers every partial row this
-                // split reduces (ri-th owned row, split sp) into the gather area.
-                const int nrows = (kRows - u.split + S - 1) / S;
-                float* gat = reinterpret_cast<float*>(smem + kSlots * kSlotBytes);
-                // Lane = 16-byte column chunk of a 512-byte partial row; the 4
-                // warps take the (row, split) pairs round robin (no divisions).
-                {
-                    const int w4 = ct >> 5;
-                    int rs = 0;
-                    for (int ri = 0; ri < nrows; ++ri) {
-                        const float* row = tp + (u.split + ri * S) * kTileM + lane * 4;
-                        for (int sp = 0; sp < S; ++sp, ++rs)
-                            if ((rs & 3) == w4)
-                                cp_async16(gat + static_cast<size_t>(rs) * kTileM + lane * 4,
-                                           row + static_cast<size_t>(sp) * (kRows * kTileM));
-                    }
-                }
-                if (ct == 0 && l == 0) mark(a.trace, 22);
-                asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
-                epi_sync();
-                if (ct == 0 && l == 0) mark(a.trace, 23);
-                for (int ri = 0; ri < nrows; ++ri) {
-                    const float* g = gat + static_cast<size_t>(ri * S) * kTileM + fl;
-                    float v = 0.f;
-#pragma unroll 8
-                    for (int sp = 0; sp < S; ++sp) v += g[sp * kTileM];
-                    emit(u.split + ri * S, v);
-                }
-                if (ct == 0 && l < 2) mark(a.trace, 27 + 2 * l);
+                if (l < 4 && ct == 0) K1_SET(6 + 6 * l);
             }
-            fence_proxy_async_global();
-            if (ct == 0 && l == 0) mark(a.trace, 24);
-            epi_sync();
-            if (ct == 0) {
-                if (l == 0) mark(a.trace, 25);
-                fence_acq_rel_gpu();
-                if (l == 0) mark(a.trace, 30);
-                atomicAdd(cnt + kCntDone + l * 64 + u.tile, 1u);
-                if (last) atomicAdd(cnt + kCntFinal, 1u);
-                if (l < 6) mark(a.trace, 5 + 4 * l);
-            }
-            pr.stop(pd[1]);
-        }
-        if (ct == 0) {
-            prof_store(a.trace, 11, pd[0]);
-            prof_store(a.trace, 12, pd[1]);
         }
 
-        // Softmax of the logits: batch row b = cta, after every last-layer unit finished.
+        if (lane == 0) bulk_wait_group<0>();  // every reduction of this CTA issued and complete
+
+        // Softmax rows: batch row b = cta, from the last layer's words once complete.
         if (cta < kRows) {
             const MlpFwdLayer& ly = a.layer[L - 1];
             const int C = ly.N;
-            if (ct == 0) wait_count(cnt + kCntFinal, static_cast<unsigned>(ly.tiles * ly.splits));
-            epi_sync();
-            const float* in = a.logits + static_cast<size_t>(cta) * C;
-            float* out = a.probs + static_cast<size_t>(cta) * C;
-            constexpr int kPer = 2048 / 128;
+            const unsigned need = static_cast<unsigned>(ly.nkt);
+            const unsigned long long* in = a.act + ly.act_off;  // [C][32]
+            float* lg = a.logits + static_cast<size_t>(cta) * C;
+            float* pr = a.probs + static_cast<size_t>(cta) * C;
+            constexpr int kPer = kMlpMaxClasses / 128;
+            unsigned long long wv[kPer];
+            const unsigned long long* wp[kPer];
+#pragma unroll
+            for (int i = 0; i < kPer; ++i) {  // columns past C: a complete dummy word
+                const int c = ct + i * 128;
+                wp[i] = in + static_cast<size_t>(c < C ? c : 0) * kRows + cta;
+                wv[i] = c < C ? ld_relaxed_u64(wp[i]) : need;
+            }
+            complete_words(wv, wp, need, 9, 0);
             float v[kPer];
             float m = -INFINITY;
 #pragma unroll
             for (int i = 0; i < kPer; ++i) {
                 const int c = ct + i * 128;
-                v[i] = c < C ? __ldcg(in + c) : -INFINITY;
+                v[i] = c < C ? decode_word(wv[i]) : -INFINITY;
+                if (c < C) lg[c] = v[i];
                 m = fmaxf(m, v[i]);
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-            if (lane == 0) red[0][q] = m;
+            if (lane == 0) red_s[0][q] = m;
             epi_sync();
-            m = fmaxf(fmaxf(red[0][0], red[0][1]), fmaxf(red[0][2], red[0][3]));
+            m = fmaxf(fmaxf(red_s[0][0], red_s[0][1]), fmaxf(red_s[0][2], red_s[0][3]));
             float sum = 0.f;
 #pragma unroll
             for (int i = 0; i < kPer; ++i) {
@@ -711,163 +623,104 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
 #pragma unroll
             for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
-            if (lane == 0) red[1][q] = sum;
+            if (lane == 0) red_s[1][q] = sum;
             epi_sync();
-            const float inv = 1.0f / (red[1][0] + red[1][1] + red[1][2] + red[1][3]);
+            const float inv = 1.0f / (red_s[1][0] + red_s[1][1] + red_s[1][2] + red_s[1][3]);
 #pragma unroll
             for (int i = 0; i < kPer; ++i) {
                 const int c = ct + i * 128;
-                if (c < C) out[c] = v[i] * inv;
+                if (c < C) pr[c] = v[i] * inv;
             }
         }
     }
 
     tc_fence_before();
     __syncthreads();
-    if (a.cluster) cluster_sync();  // no CTA leaves while a peer may still write into its smem
     tc_fence_after();
-    if (tid == 0) mark(a.trace, 31);
     if (warp == 1) tmem_dealloc<kTmemCols>(tmem);
+#ifdef GFX_K1_DEBUG
+    if (tid == 0) K1_MARK(26);
+    __syncthreads();
+    if (a.dbg && tid < 32) a.dbg[cta * 32 + tid] = k1_marks[tid];
+#endif
 }
 
 }  // namespace
 
-int mlp_fwd_splits(int K, int N, int grid, int cluster) {
-    const int tiles = (N + kTileM - 1) / kTileM;
-    const int kt = K / kTileK;
-    if (cluster) {  // the largest S dividing the cluster whose tiles fit the co-resident clusters
-        for (int s = cluster; s > 1; s >>= 1)
-            if (s <= kt && (tiles + cluster / s - 1) / (cluster / s) <= grid / cluster) return s;
-        return 1;
-    }
-    int s = grid / tiles;
-    if (s > kt) s = kt;
-    if (s > kRows) s = kRows;
-    return s < 1 ? 1 : s;
-}
-
-int mlp_fwd_cluster_grid(int cluster) {
-    // Co-resident CTAs when launched in clusters of `cluster` (one CTA per SM).
-    const size_t smem = mlp_fwd_smem();
-    GFX_CUDA(cudaFuncSetAttribute(mlp_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(static_cast<unsigned>(cluster));
-    cfg.blockDim = dim3(kThreads);
-    cfg.dynamicSmemBytes = smem;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = static_cast<unsigned>(cluster);
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    int n = 0;
-    GFX_CUDA(cudaOccupancyMaxActiveClusters(&n, mlp_forward_kernel, &cfg));
-    return n * cluster;
-}
-
-size_t mlp_trace_words(int grid) { return static_cast<size_t>(48) * grid + 576; }
-
-// Debug report of a traced launch (GFX_TRACE_MLP=1): per-phase %globaltimer marks
-// (µs after the first CTA started; min / median / max over CTAs), CTA 0's
-// per-step timeline and the per-role cycle accounting.
-void mlp_trace_report(const std::vector<unsigned long long>& tr, int grid, int L, int model) {
-    struct {
-        int grid, L;
-    } f{grid, L};
+void mlp_debug_report(const unsigned long long* dbg, int grid, int L, int model, cudaStream_t s) {
+    std::vector<unsigned long long> m(static_cast<size_t>(grid) * 32 + 96 * 8);
+    GFX_CUDA(cudaStreamSynchronize(s));
+    GFX_CUDA(cudaMemcpy(m.data(), dbg, m.size() * 8, cudaMemcpyDeviceToHost));
     unsigned long long t0 = ~0ull;
-    const size_t nct = static_cast<size_t>(f.grid) * 32;
-    for (size_t i = 0; i < nct; i += 32) t0 = std::min(t0, tr[i]);
-    static const char* names[4] = {"mma first", "mma last", "epi start", "tile done"};
-    std::fprintf(stderr, "[trace] model %d grid %d\n", model, f.grid);
-    for (int ph = 0; ph < 32; ++ph) {
+    for (int c = 0; c < grid; ++c) t0 = std::min(t0, m[static_cast<size_t>(c) * 32]);
+    static const char* nm[6] = {"W landed", "X complete", "MMA first", "MMA done", "reds issued", "last X cplt"};
+    std::fprintf(stderr, "[K1 model %d] us after first CTA start: min p10 median p90 max over %d CTAs\n", model, grid);
+    for (int i = 0; i < 30; ++i) {
         std::vector<double> v;
-        for (size_t i = 0; i < nct; i += 32)
-            if (tr[i + static_cast<size_t>(ph)]) v.push_back((tr[i + static_cast<size_t>(ph)] - t0) * 1e-3);
-        if (v.empty()) continue;
+        for (int c = 0; c < grid; ++c)
+            if (m[static_cast<size_t>(c) * 32 + i]) v.push_back((m[static_cast<size_t>(c) * 32 + i] - t0) * 1e-3);
+        if (v.empty() || (i >= 2 && i < 26 && (i - 2) / 6 >= L)) continue;
         std::sort(v.begin(), v.end());
-        char nm[32];
-        if (ph == 0) std::snprintf(nm, sizeof nm, "start");
-        else if (ph == 1) std::snprintf(nm, sizeof nm, "setup");
-        else if (ph == 31) std::snprintf(nm, sizeof nm, "end");
-        else if (ph >= 26 && ph < 30) std::snprintf(nm, sizeof nm, "L%d %s", (ph - 26) / 2, ph % 2 ? "gathered" : "siblings");
-        else if (ph >= 18 && ph <= 30 && f.L <= 4) {
-            static const char* sub[13] = {"L0 part stored", "L0 fenced", "L0 arrived", "L0 sib seen", "L0 cp.async issued",
-                                          "L0 cp.async done", "L0 emitted", "L0 done-sync", "", "", "", "", "L0 done fenced"};
-            std::snprintf(nm, sizeof nm, "%s", sub[ph - 18]);
-        }
-        else std::snprintf(nm, sizeof nm, "L%d %s", (ph - 2) / 4, names[(ph - 2) % 4]);
-        std::fprintf(stderr, "  %-16s n=%3zu %8.2f %8.2f %8.2f\n", nm, v.size(), v.front(), v[v.size() / 2],
-                     v.back());
+        char name[40];
+        if (i == 0) std::snprintf(name, sizeof name, "start");
+        else if (i == 1) std::snprintf(name, sizeof name, "setup");
+        else if (i == 26) std::snprintf(name, sizeof name, "end");
+        else if (i == 27) std::snprintf(name, sizeof name, "L1 grp words cplt");
+        else if (i == 28) std::snprintf(name, sizeof name, "L1 ready arrive");
+        else if (i == 29) std::snprintf(name, sizeof name, "L1 MMA saw step0");
+        else std::snprintf(name, sizeof name, "L%d %s", (i - 2) / 6, nm[(i - 2) % 6]);
+        const size_t n = v.size();
+        std::fprintf(stderr, "  %-18s %7.2f %7.2f %7.2f %7.2f %7.2f\n", name, v[0], v[n / 10], v[n / 2], v[n * 9 / 10],
+                     v[n - 1]);
     }
-    std::fprintf(stderr, "  CTA 0 steps (us): Wreq Xreq Wlanded WloDone xFull mmaIssued rawLanded\n");
-    for (int st = 0; st < 64; ++st) {
-        const unsigned long long* p = tr.data() + nct + st * 8;
-        if (!p[0] && !p[5]) break;
+    std::fprintf(stderr, "  CTA 0 steps (us): W issued, X issued, W landed, raw landed, operand ready, MMA issued\n");
+    for (int g = 0; g < 96; ++g) {
+        const unsigned long long* p = m.data() + static_cast<size_t>(grid) * 32 + g * 8;
+        if (!p[0]) break;
         auto us = [&](unsigned long long t) { return t ? (t - t0) * 1e-3 : -1.0; };
-        std::fprintf(stderr, "   %2d %7.2f %7.2f %7.2f %7.2f %7.2f %7.2f %7.2f\n", st, us(p[0]), us(p[1]), us(p[2]),
-                     us(p[3]), us(p[4]), us(p[5]), us(p[6]));
+        std::fprintf(stderr, "   %2d %7.2f %7.2f %7.2f %7.2f %7.2f %7.2f\n", g, us(p[0]), us(p[1]), us(p[2]), us(p[3]),
+                     us(p[4]), us(p[5]));
     }
-    static const char* pn[16] = {"mma: wait tempty", "mma: wait ready", "", "",
-                                 "mma: commits+rest", "conv: wait w_full", "", "conv: work",
-                                 "wprod: wait slot", "xprod: wait slot", "xprod: wait flag", "drain: wait tfull",
-                                 "drain: epilogue", "mma: MMAs", "", "steps"};
-    std::fprintf(stderr, "  cycles per CTA, mean over CTAs with work (per step in brackets):\n");
-    for (int i = 0; i < 16; ++i) {
-        if (!pn[i][0]) continue;
-        double sum = 0, steps = 0;
-        int n = 0;
-        for (int c = 0; c < f.grid; ++c) {
-            const unsigned long long st = tr[nct + 576 + c * 16 + 15];
-            if (!st) continue;
-            sum += static_cast<double>(tr[nct + 576 + c * 16 + i]);
-            steps += static_cast<double>(st);
-            ++n;
-        }
-        if (n) std::fprintf(stderr, "   %-22s %10.0f  (%7.1f)\n", pn[i], sum / n, sum / steps);
-    }
-    }
+    GFX_CUDA(cudaMemset(const_cast<unsigned long long*>(dbg), 0, m.size() * 8));
+}
 
-size_t mlp_fwd_smem() { return static_cast<size_t>(kSlotBytes) * kSlots + kGatherBytes + 1024; }
+size_t mlp_fwd_smem() { return static_cast<size_t>(kStageOff) + kStageBytes + 1024; }
 
 void launch_mlp_forward(MlpFwdArgs& a, cudaStream_t stream) {
     if (a.L < 1 || a.L > GFX_MAX_LAYERS) throw std::runtime_error("mlp forward: bad layer count");
+    uint64_t act = 0;
     for (int l = 0; l < a.L; ++l) {
         const MlpFwdLayer& ly = a.layer[l];
-        if (ly.K % kTileK || ly.K > kMlpMaxDim || ly.N > kMlpMaxDim || ly.tiles > 64 || ly.tiles * ly.splits > a.grid)
+        if (ly.K % kTileK || ly.K <= 0 || ly.N <= 0 || ly.K > kMlpMaxDim || ly.N > kMlpMaxDim ||
+            ly.tiles != (ly.N + kTileM - 1) / kTileM || ly.nkt != ly.K / kTileK || ly.act_off != act)
             throw std::runtime_error("mlp forward: unsupported layer shape");
-        if (a.cluster && (a.cluster % ly.splits || (ly.tiles + a.cluster / ly.splits - 1) / (a.cluster / ly.splits) >
-                                                        a.grid / a.cluster))
-            throw std::runtime_error("mlp forward: layer does not fit the cluster map");
         if (l > 0 && a.layer[l - 1].N != ly.K) throw std::runtime_error("mlp forward: layer widths do not chain");
+        act += static_cast<uint64_t>(ly.N) * kRows;
     }
-    if (a.layer[a.L - 1].N > 2048 || a.grid < kRows) throw std::runtime_error("mlp forward: at most 2048 classes, grid >= 32");
+    if (act > kMlpActWords) throw std::runtime_error("mlp forward: layer outputs exceed the workspace");
+    if (a.layer[a.L - 1].N > kMlpMaxClasses || a.grid < kRows)
+        throw std::runtime_error("mlp forward: at most 2048 classes, grid >= 32");
+    // Layer outputs: [N][32] u64 rows, boxes of 16 words x 32 features, SWIZZLE_128B (the drain's staging image).
+    for (int l = 0; l < a.L; ++l)
+        if (!encode_tensor_map_2d(&a.tmap_out[l], CU_TENSOR_MAP_DATA_TYPE_UINT64, 8, a.act + a.layer[l].act_off, kRows,
+                                  static_cast<uint64_t>(a.layer[l].N), kRows * 8, 16, 32, CU_TENSOR_MAP_SWIZZLE_128B))
+            throw CudaError("cuTensorMapEncodeTiled failed for a layer output");
     // Layer-0 input tiles: 32 x 32 fp32 boxes of the [32 x K0] request input, SWIZZLE_128B.
     if (!encode_tensor_map_2d(&a.tmap_in, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, a.in, static_cast<uint64_t>(a.layer[0].K),
                               kRows, static_cast<uint64_t>(a.layer[0].K) * 4, kTileK, kRows, CU_TENSOR_MAP_SWIZZLE_128B))
         throw CudaError("cuTensorMapEncodeTiled failed for the request input");
-    static bool attr_set = false;
     const size_t smem = mlp_fwd_smem();
-    if (!attr_set) {
-        GFX_CUDA(cudaFuncSetAttribute(mlp_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      static_cast<int>(smem)));
-        attr_set = true;
-    }
+    ensure_max_dynamic_smem(reinterpret_cast<const void*>(mlp_forward_kernel), static_cast<int>(smem));
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(static_cast<unsigned>(a.grid));
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
-    cudaLaunchAttribute attr[2];
-    attr[0].id = cudaLaunchAttributeCooperative;  // every CTA co-resident: the dataflow waits need it
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;  // every CTA co-resident: the counter waits need it
     attr[0].val.cooperative = 1;
-    attr[1].id = cudaLaunchAttributeClusterDimension;
-    attr[1].val.clusterDim.x = static_cast<unsigned>(a.cluster ? a.cluster : 1);
-    attr[1].val.clusterDim.y = 1;
-    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    static const bool no_coop = std::getenv("GFX_MLP_NOCOOP") != nullptr;  // debug A/B
-    cfg.numAttrs = a.cluster ? 2 : (no_coop ? 0 : 1);
+    cfg.numAttrs = 1;
     GFX_CUDA(cudaLaunchKernelEx(&cfg, mlp_forward_kernel, a));
 }
 

@@ -163,6 +163,14 @@ __device__ __forceinline__ void tma_tile2d_s2g(const CUtensorMap* map, int c0, i
                  "r"(c0), "r"(c1), "r"(smem_u32(src))
                  : "memory");
 }
+// 2-D tensor tile shared -> global ADD-reduction (u64 / f32 ... per the tensor
+// map's data type), performed in L2; bulk-group completion.
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, int c0, int c1, const void* src) {
+    asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1), "r"(smem_u32(src))
+                 : "memory");
+}
 __device__ __forceinline__ void bulk_commit_group() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 // Wait until at most N bulk groups of this thread are still reading their shared-memory source.
 template <int N>

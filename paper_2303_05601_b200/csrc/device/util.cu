@@ -5,7 +5,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
 #include <mutex>
+#include <utility>
 
 #include "common.cuh"
 #include "mlp.cuh"
@@ -34,6 +36,35 @@ EncodeTiledFn encode_fn() {
 }
 
 }  // namespace
+
+int current_device() {
+    int dev = 0;
+    GFX_CUDA(cudaGetDevice(&dev));
+    return dev;
+}
+
+int device_sm_count(int dev) {
+    static std::mutex mu;
+    static std::map<int, int> sms;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = sms.find(dev);
+    if (it != sms.end()) return it->second;
+    int n = 0;
+    GFX_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+    sms[dev] = n;
+    return n;
+}
+
+void ensure_max_dynamic_smem(const void* func, int bytes) {
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, int> done;  // (device, kernel) -> bytes set
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = done.find({dev, func});
+    if (it != done.end() && it->second >= bytes) return;
+    GFX_CUDA(cudaFuncSetAttribute(func, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    done[{dev, func}] = bytes;
+}
 
 bool encode_tensor_map_2d(CUtensorMap* map, CUtensorMapDataType dtype, uint32_t elem_bytes, const void* base,
                           uint64_t inner, uint64_t outer, uint64_t row_stride_bytes, uint32_t box_inner,

@@ -250,22 +250,6 @@ def test_mlp_edge_shapes(gfx, olib, dims):
         gfx._ffi.gfx_arena_destroy(a)
 
 
-def test_cluster_dsmem_variant():
-    """The opt-in K1 variant (GFX_MLP_CLUSTER=1, read once per process): split-K
-    partials exchanged through cluster DSMEM (clusters of 8, st.async into the
-    owner's smem) instead of global memory; same parity bar in a fresh process."""
-    import subprocess
-    import sys
-    env = dict(os.environ, GFX_MLP_CLUSTER="1")
-    here = os.path.dirname(os.path.abspath(__file__))
-    tests = [os.path.join(here, "test_gpu_parity.py") + "::" + t for t in
-             ("test_replay_outputs_match_oracle", "test_every_model_shape", "test_mlp_edge_shapes",
-              "test_peer_fetch_emulated_and_deterministic")]
-    r = subprocess.run([sys.executable, "-m", "pytest", "-x", "-q", "-p", "no:cacheprovider"] + tests,
-                       env=env, capture_output=True, text=True, timeout=900)
-    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
-
-
 def test_mlp_random_shapes(gfx, olib):
     """Twelve seeded random MLPs (1-6 layers, widths 32-4096 in steps of 32, any
     number of classes divisible by 4): every tile / split / boundary pattern the

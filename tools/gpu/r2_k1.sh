@@ -1,0 +1,3 @@
+# K1 release timings: back-to-back forwards per C2 model + interleaved.
+exec > gpurun_out/r2_k1.log 2>&1
+timeout 300 python tools/k1_bench.py 300 0,3,7,12,15,16,18,21 2>&1 | tail -12
