@@ -148,6 +148,13 @@ int gfx_evict(gfx_arena_t a, int model_idx);
  * BERT: in [batch*seq x d] bf16 embeddings, out [batch x d] fp32 pooled output. */
 int gfx_infer(gfx_arena_t a, int model_idx, const void* in, void* out, int batch, gfx_event_t* done);
 
+/* Bench: n back-to-back inferences of resident models models[i] on the compute
+ * stream (input i at in + i * in_stride, output at out + (i % 2) * out_stride,
+ * device pointers), bracketed by two CUDA events; *ms = their elapsed time.
+ * Synchronous. The dominant kernel's average launch duration = *ms / n. */
+int gfx_infer_sequence(gfx_arena_t a, const int32_t* models, int n, const void* in, uint64_t in_stride, void* out,
+                       uint64_t out_stride, double* ms);
+
 /* Test/debug: BERT inference that also copies every layer's hidden state into
  * hidden ([L+1][batch*seq][d] bf16, device) for teacher-forced parity checks. */
 int gfx_infer_debug(gfx_arena_t a, int model_idx, const void* in, void* out, int batch, void* hidden);

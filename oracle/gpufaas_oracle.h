@@ -108,6 +108,14 @@ void orc_fill_params(uint64_t model_seed, uint32_t tensor, uint64_t n, float sca
 int orc_mlp_forward(uint64_t model_seed, int n_layers, const int32_t* dims, int batch,
                     const float* x, float* logits, float* probs, int threads);
 
+/* The same forward on a model whose parameters were generated once
+ * (orc_mlp_create), so a CPU baseline times the forward alone. */
+#define ORC_MAX_LAYERS 16
+typedef struct orc_mlp orc_mlp;
+orc_mlp* orc_mlp_create(uint64_t model_seed, int n_layers, const int32_t* dims);
+int orc_mlp_run(const orc_mlp* m, int batch, const float* x, float* logits, float* probs, int threads);
+void orc_mlp_free(orc_mlp* m);
+
 /* BERT-base-style encoder (C5) forward, fp64 accumulation with the product's
  * bf16 rounding points. x_bits: [batch*seq x d] bf16 bit patterns;
  * pooled: [batch x d] fp32. */

@@ -55,19 +55,50 @@ static void* layer_worker(void* arg) {
     job* j = arg;
     for (int n = j->t; n < j->N; n += j->nt) {
         const float* wr = j->w + (size_t)n * (size_t)j->K;
-        for (int r = 0; r < j->B; ++r) {
-            const float* xr = j->in + (size_t)r * (size_t)j->K;
-            double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+        /* four batch rows per pass over the weight row (fp64 accumulation, two
+         * partial sums per row, combined in a fixed order) */
+        int r = 0;
+        for (; r + 3 < j->B; r += 4) {
+            const float* x0 = j->in + (size_t)r * (size_t)j->K;
+            const float* x1 = x0 + j->K;
+            const float* x2 = x1 + j->K;
+            const float* x3 = x2 + j->K;
+            double a0 = 0, b0 = 0, a1 = 0, b1 = 0, a2 = 0, b2 = 0, a3 = 0, b3 = 0;
             int k = 0;
-            for (; k + 3 < j->K; k += 4) {
+            for (; k + 1 < j->K; k += 2) {
+                const double w0 = wr[k], w1 = wr[k + 1];
+                a0 += (double)x0[k] * w0;
+                b0 += (double)x0[k + 1] * w1;
+                a1 += (double)x1[k] * w0;
+                b1 += (double)x1[k + 1] * w1;
+                a2 += (double)x2[k] * w0;
+                b2 += (double)x2[k + 1] * w1;
+                a3 += (double)x3[k] * w0;
+                b3 += (double)x3[k + 1] * w1;
+            }
+            for (; k < j->K; ++k) {
+                a0 += (double)x0[k] * wr[k];
+                a1 += (double)x1[k] * wr[k];
+                a2 += (double)x2[k] * wr[k];
+                a3 += (double)x3[k] * wr[k];
+            }
+            const double acc[4] = {a0 + b0, a1 + b1, a2 + b2, a3 + b3};
+            for (int i = 0; i < 4; ++i) {
+                float v = (float)((double)j->b[n] + acc[i]);
+                if (j->relu && v < 0.0f) v = 0.0f;
+                j->out[(size_t)(r + i) * (size_t)j->N + (size_t)n] = v;
+            }
+        }
+        for (; r < j->B; ++r) {
+            const float* xr = j->in + (size_t)r * (size_t)j->K;
+            double a0 = 0, b0 = 0;
+            int k = 0;
+            for (; k + 1 < j->K; k += 2) {
                 a0 += (double)xr[k] * (double)wr[k];
-                a1 += (double)xr[k + 1] * (double)wr[k + 1];
-                a2 += (double)xr[k + 2] * (double)wr[k + 2];
-                a3 += (double)xr[k + 3] * (double)wr[k + 3];
+                b0 += (double)xr[k + 1] * (double)wr[k + 1];
             }
             for (; k < j->K; ++k) a0 += (double)xr[k] * (double)wr[k];
-            double acc = (double)j->b[n] + ((a0 + a1) + (a2 + a3));
-            float v = (float)acc;
+            float v = (float)((double)j->b[n] + (a0 + b0));
             if (j->relu && v < 0.0f) v = 0.0f;
             j->out[(size_t)r * (size_t)j->N + (size_t)n] = v;
         }
@@ -91,8 +122,46 @@ static void run_layer(const float* in, const float* w, const float* b, float* ou
 
 /* Weight tensor of layer l is tensor id 2l (row-major N x K, PyTorch Linear
  * layout), its bias is tensor 2l+1; scale = 1/sqrt(K). */
-int orc_mlp_forward(uint64_t model_seed, int n_layers, const int32_t* dims, int batch, const float* x,
-                    float* logits, float* probs, int threads) {
+struct orc_mlp {
+    int n_layers;
+    int32_t dims[ORC_MAX_LAYERS + 1];
+    float* w[ORC_MAX_LAYERS];
+    float* b[ORC_MAX_LAYERS];
+};
+
+orc_mlp* orc_mlp_create(uint64_t model_seed, int n_layers, const int32_t* dims) {
+    if (n_layers < 1 || n_layers > ORC_MAX_LAYERS) return NULL;
+    orc_mlp* m = calloc(1, sizeof *m);
+    if (!m) return NULL;
+    m->n_layers = n_layers;
+    memcpy(m->dims, dims, (size_t)(n_layers + 1) * sizeof(int32_t));
+    for (int l = 0; l < n_layers; ++l) {
+        const int K = dims[l], N = dims[l + 1];
+        const float scale = (float)(1.0 / sqrt((double)K));
+        m->w[l] = malloc((size_t)N * (size_t)K * sizeof(float));
+        m->b[l] = malloc((size_t)N * sizeof(float));
+        if (!m->w[l] || !m->b[l]) {
+            orc_mlp_free(m);
+            return NULL;
+        }
+        orc_fill_params(model_seed, (uint32_t)(2 * l), (uint64_t)N * (uint64_t)K, scale, m->w[l]);
+        orc_fill_params(model_seed, (uint32_t)(2 * l + 1), (uint64_t)N, scale, m->b[l]);
+    }
+    return m;
+}
+
+void orc_mlp_free(orc_mlp* m) {
+    if (!m) return;
+    for (int l = 0; l < m->n_layers; ++l) {
+        free(m->w[l]);
+        free(m->b[l]);
+    }
+    free(m);
+}
+
+int orc_mlp_run(const orc_mlp* m, int batch, const float* x, float* logits, float* probs, int threads) {
+    const int n_layers = m->n_layers;
+    const int32_t* dims = m->dims;
     int maxd = 0;
     for (int l = 0; l <= n_layers; ++l) if (dims[l] > maxd) maxd = dims[l];
     float* cur = malloc((size_t)batch * (size_t)maxd * sizeof(float));
@@ -100,16 +169,7 @@ int orc_mlp_forward(uint64_t model_seed, int n_layers, const int32_t* dims, int 
     if (!cur || !nxt) { free(cur); free(nxt); return -1; }
     memcpy(cur, x, (size_t)batch * (size_t)dims[0] * sizeof(float));
     for (int l = 0; l < n_layers; ++l) {
-        int K = dims[l], N = dims[l + 1];
-        float scale = (float)(1.0 / sqrt((double)K));
-        float* w = malloc((size_t)N * (size_t)K * sizeof(float));
-        float* b = malloc((size_t)N * sizeof(float));
-        if (!w || !b) { free(w); free(b); free(cur); free(nxt); return -1; }
-        orc_fill_params(model_seed, (uint32_t)(2 * l), (uint64_t)N * (uint64_t)K, scale, w);
-        orc_fill_params(model_seed, (uint32_t)(2 * l + 1), (uint64_t)N, scale, b);
-        run_layer(cur, w, b, nxt, batch, K, N, l + 1 < n_layers, threads);
-        free(w);
-        free(b);
+        run_layer(cur, m->w[l], m->b[l], nxt, batch, dims[l], dims[l + 1], l + 1 < n_layers, threads);
         float* t = cur; cur = nxt; nxt = t;
     }
     int C = dims[n_layers];
@@ -117,16 +177,25 @@ int orc_mlp_forward(uint64_t model_seed, int n_layers, const int32_t* dims, int 
     if (probs) {
         for (int r = 0; r < batch; ++r) {
             const float* lr = cur + (size_t)r * (size_t)C;
-            double m = lr[0];
-            for (int c = 1; c < C; ++c) if (lr[c] > m) m = lr[c];
+            double mx = lr[0];
+            for (int c = 1; c < C; ++c) if (lr[c] > mx) mx = lr[c];
             double s = 0;
-            for (int c = 0; c < C; ++c) s += exp((double)lr[c] - m);
-            for (int c = 0; c < C; ++c) probs[(size_t)r * (size_t)C + (size_t)c] = (float)(exp((double)lr[c] - m) / s);
+            for (int c = 0; c < C; ++c) s += exp((double)lr[c] - mx);
+            for (int c = 0; c < C; ++c) probs[(size_t)r * (size_t)C + (size_t)c] = (float)(exp((double)lr[c] - mx) / s);
         }
     }
     free(cur);
     free(nxt);
     return 0;
+}
+
+int orc_mlp_forward(uint64_t model_seed, int n_layers, const int32_t* dims, int batch, const float* x,
+                    float* logits, float* probs, int threads) {
+    orc_mlp* m = orc_mlp_create(model_seed, n_layers, dims);
+    if (!m) return -1;
+    const int rc = orc_mlp_run(m, batch, x, logits, probs, threads);
+    orc_mlp_free(m);
+    return rc;
 }
 
 /* ------------------------------------------------------------------------ */

@@ -739,6 +739,27 @@ int gfx_infer(gfx_arena_t a, int model_idx, const void* in, void* out, int batch
     });
 }
 
+int gfx_infer_sequence(gfx_arena_t a, const int32_t* models, int n, const void* in, uint64_t in_stride, void* out,
+                       uint64_t out_stride, double* ms) {
+    return guarded([&] {
+        if (n <= 0) throw std::invalid_argument("empty inference sequence");
+        GpuManager& m = *a->mgr;
+        m.activate();
+        cudaEvent_t e0, e1;
+        GFX_CUDA(cudaEventCreate(&e0));
+        GFX_CUDA(cudaEventCreate(&e1));
+        GFX_CUDA(cudaEventRecord(e0, m.compute_stream()));
+        for (int i = 0; i < n; ++i)
+            m.infer(models[i], static_cast<const char*>(in) + static_cast<size_t>(i) * in_stride,
+                    static_cast<char*>(out) + static_cast<size_t>(i % 2) * out_stride);
+        GFX_CUDA(cudaEventRecord(e1, m.compute_stream()));
+        GFX_CUDA(cudaEventSynchronize(e1));
+        *ms = elapsed_ms(e0, e1);
+        cudaEventDestroy(e0);
+        cudaEventDestroy(e1);
+    });
+}
+
 int gfx_infer_debug(gfx_arena_t a, int model_idx, const void* in, void* out, int batch, void* hidden) {
     return guarded([&] {
         const gfx::ModelBlob& b = ModelStore::get().at(model_idx);
