@@ -105,8 +105,11 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
     size_t in_bytes = 0, out_bytes = 0;
     int family = 0;
     bool full_outputs = false;
-    // timing
-    KernelTimer layer_timer, load_timer, p2p_timer, req_timer;
+    // timing: events per GPU (an event belongs to the device current at its creation)
+    struct Timers {
+        KernelTimer layer, load, p2p, req;
+    };
+    std::vector<Timers> timers;  // per GPU id
     std::vector<cudaEvent_t> req_start, req_end;
     std::vector<int> req_gpu;
     // ---- cross-process peers (one process per GPU, only_gpu mode) ----
@@ -193,6 +196,16 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
         // Every catalog model must be registered and its charge must cover its pages.
         for (size_t i = 0; i < catalog.size(); ++i) {
             const gfx::ModelBlob& b = ModelStore::get().at(static_cast<int>(i));
+            // Catalog row i must be the model registered at index i (its parameter
+            // stream is seeded by the FNV-1a hash of the model id).
+            uint64_t h = 14695981039346656037ULL;
+            for (unsigned char c : catalog.profiles()[i].model_id) {
+                h ^= c;
+                h *= 1099511628211ULL;
+            }
+            if (b.desc.seed != h)
+                throw std::invalid_argument("model registered at index " + std::to_string(i) + " is not catalog row '" +
+                                            catalog.profiles()[i].model_id + "'");
             const double need = 2.0 * b.pages;
             if (catalog.profiles()[i].occupation_mb < need)
                 throw std::invalid_argument("catalog occupation_mb of '" + catalog.profiles()[i].model_id +
@@ -212,14 +225,15 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
         bufs.resize(static_cast<size_t>(G));
         dev_of.resize(static_cast<size_t>(G));
         pending_in.assign(static_cast<size_t>(G), nullptr);
+        timers.resize(static_cast<size_t>(G));
         const size_t n = requests.size();
         for (int g = 0; g < G; ++g) {
             dev_of[g] = args.first_device + (args.n_devices == 1 ? 0 : g);
             if (args.only_gpu >= 0 && g != args.only_gpu) continue;
             mgrs[g] = std::make_unique<GpuManager>(dev_of[g], cap_bytes, g);
-            mgrs[g]->layer_timer = args.record_kernels ? &layer_timer : nullptr;
-            mgrs[g]->load_timer = &load_timer;
-            mgrs[g]->p2p_timer = &p2p_timer;
+            mgrs[g]->layer_timer = args.record_kernels ? &timers[g].layer : nullptr;
+            mgrs[g]->load_timer = &timers[g].load;
+            mgrs[g]->p2p_timer = &timers[g].p2p;
             DevBufs& b = bufs[g];
             GFX_CUDA(cudaSetDevice(dev_of[g]));
             // Inputs: every request this GPU might serve (ids are global).
@@ -322,11 +336,12 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
         GpuManager& m = *mgrs[static_cast<size_t>(gpu)];
         DevBufs& b = bufs[static_cast<size_t>(gpu)];
         const int rid = req.request_id;
+        KernelTimer& rt = timers[static_cast<size_t>(gpu)].req;
         m.activate();
         cudaEvent_t e0 = nullptr;
         req_gpu[rid] = gpu;
         if (args.record_requests) {
-            e0 = req_timer.next();
+            e0 = rt.next();
             req_start[rid] = e0;
         }
         LiveTask live_t{};
@@ -334,7 +349,7 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
         if (!hit) {
             if (e0) GFX_CUDA(cudaEventRecord(e0, m.copy_stream()));
             if (lt) {
-                lt->ls = req_timer.next();
+                lt->ls = rt.next();
                 GFX_CUDA(cudaEventRecord(lt->ls, m.copy_stream()));
             }
             for (int v : evicted) {
@@ -372,7 +387,7 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
                     if (r != gpu) m.copy_write(remotes[static_cast<size_t>(r)].flags + fl_loaded(gpu, model),
                                                load_cnt[fl_loaded(gpu, model)]);
             if (lt) {
-                lt->le = req_timer.next();
+                lt->le = rt.next();
                 GFX_CUDA(cudaEventRecord(lt->le, m.copy_stream()));
             }
         } else if (e0) {
@@ -384,31 +399,31 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
             // e2e: this request's input crosses PCIe inside the timed region.
             GFX_CUDA(cudaMemcpyAsync(in, static_cast<const char*>(args.host_inputs) + static_cast<size_t>(rid) * in_bytes,
                                      in_bytes, cudaMemcpyHostToDevice, b.io_in));
-            cudaEvent_t ein = req_timer.next();
+            cudaEvent_t ein = rt.next();
             GFX_CUDA(cudaEventRecord(ein, b.io_in));
             GFX_CUDA(cudaStreamWaitEvent(m.compute_stream(), ein, 0));
             res.io_h2d_bytes += in_bytes;
         }
         if (lt) {
             if (lt->le) GFX_CUDA(cudaStreamWaitEvent(m.compute_stream(), lt->le, 0));
-            lt->is = req_timer.next();
+            lt->is = rt.next();
             GFX_CUDA(cudaEventRecord(lt->is, m.compute_stream()));
         }
         m.infer(model, in, out);
         if (lt) {
-            lt->ie = req_timer.next();
+            lt->ie = rt.next();
             GFX_CUDA(cudaEventRecord(lt->ie, m.compute_stream()));
         }
         const gfx::ModelBlob& blob = ModelStore::get().at(model);
         res.mlp_flops += blob.flops;
         res.mlp_weight_bytes += blob.alg_bytes;
         if (args.record_requests) {
-            cudaEvent_t e1 = req_timer.next();
+            cudaEvent_t e1 = rt.next();
             GFX_CUDA(cudaEventRecord(e1, m.compute_stream()));
             req_end[rid] = e1;
         }
         if (args.host_io) {
-            cudaEvent_t done = req_timer.next();
+            cudaEvent_t done = rt.next();
             GFX_CUDA(cudaEventRecord(done, m.compute_stream()));
             GFX_CUDA(cudaStreamWaitEvent(b.io_out, done, 0));
             GFX_CUDA(cudaMemcpyAsync(static_cast<char*>(args.host_outputs) + static_cast<size_t>(rid) * out_bytes, out,
@@ -417,7 +432,7 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
         }
         if (live_mode) {
             // Live mode: the engine polls this to learn the request finished (output included).
-            lt->done = req_timer.next();
+            lt->done = rt.next();
             GFX_CUDA(cudaEventRecord(lt->done, args.host_io ? b.io_out : m.compute_stream()));
             live_q[static_cast<size_t>(gpu)].push_back(live_t);
         }
@@ -479,7 +494,7 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
 
     void run(gfx_replay_result* out) {
         res = gfx_replay_result{};
-        layer_timer.used = load_timer.used = p2p_timer.used = req_timer.used = 0;
+        for (Timers& t : timers) t.layer.used = t.load.used = t.p2p.used = t.req.used = 0;
         std::fill(req_start.begin(), req_start.end(), nullptr);
         std::fill(req_end.begin(), req_end.end(), nullptr);
         const int G = gpu_count();
@@ -517,7 +532,7 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
             GpuManager& m = *mgrs[g];
             m.activate();
             for (cudaStream_t s : {m.copy_stream(), bufs[g].io_in, bufs[g].io_out}) {
-                cudaEvent_t e = req_timer.next();
+                cudaEvent_t e = timers[static_cast<size_t>(g)].req.next();
                 GFX_CUDA(cudaEventRecord(e, s));
                 GFX_CUDA(cudaStreamWaitEvent(m.compute_stream(), e, 0));
             }
@@ -564,16 +579,21 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
         res.sched_ms = std::chrono::duration<double, std::milli>(s1 - s0).count();
         for (int g = 0; g < G; ++g)
             if (mgrs[g]) res.kernel_launches += mgrs[g]->kernel_launches;
-        for (size_t i = 0; i + 1 < layer_timer.used; i += 2)
-            res.kernel_ms += elapsed_ms(layer_timer.ev[i], layer_timer.ev[i + 1]);
-        for (size_t i = 0; i + 1 < load_timer.used; i += 2)
-            res.h2d_ms += elapsed_ms(load_timer.ev[i], load_timer.ev[i + 1]);
-        for (size_t i = 0; i + 1 < p2p_timer.used; i += 2)
-            res.p2p_ms += elapsed_ms(p2p_timer.ev[i], p2p_timer.ev[i + 1]);
+        for (size_t g = 0; g < timers.size(); ++g) {
+            if (!mgrs[g]) continue;
+            GFX_CUDA(cudaSetDevice(dev_of[g]));
+            const Timers& t = timers[g];
+            for (size_t i = 0; i + 1 < t.layer.used; i += 2) res.kernel_ms += elapsed_ms(t.layer.ev[i], t.layer.ev[i + 1]);
+            for (size_t i = 0; i + 1 < t.load.used; i += 2) res.h2d_ms += elapsed_ms(t.load.ev[i], t.load.ev[i + 1]);
+            for (size_t i = 0; i + 1 < t.p2p.used; i += 2) res.p2p_ms += elapsed_ms(t.p2p.ev[i], t.p2p.ev[i + 1]);
+        }
         if (args.record_requests) {
             std::vector<double> svc;
             for (size_t r = 0; r < req_start.size(); ++r)
-                if (req_start[r] && req_end[r]) svc.push_back(elapsed_ms(req_start[r], req_end[r]));
+                if (req_start[r] && req_end[r]) {
+                    GFX_CUDA(cudaSetDevice(dev_of[static_cast<size_t>(req_gpu[r])]));
+                    svc.push_back(elapsed_ms(req_start[r], req_end[r]));
+                }
             res.service_p50_ms = percentile(svc, 50);
             res.service_p99_ms = percentile(svc, 99);
             service_ms = std::move(svc);
@@ -601,8 +621,9 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
             cudaEventDestroy(bufs[g].start);
             cudaEventDestroy(bufs[g].stop);
         }
-        for (KernelTimer* t : {&layer_timer, &load_timer, &p2p_timer, &req_timer})
-            for (cudaEvent_t e : t->ev) cudaEventDestroy(e);
+        for (Timers& tm : timers)
+            for (KernelTimer* t : {&tm.layer, &tm.load, &tm.p2p, &tm.req})
+                for (cudaEvent_t e : t->ev) cudaEventDestroy(e);
         for (RemoteArena& ra : remotes) {
             if (ra.arena) cudaIpcCloseMemHandle(ra.arena);
             if (ra.flags) cudaIpcCloseMemHandle(ra.flags);

@@ -48,6 +48,7 @@ SimConfig to_sim_config(const gfx_sim_config& c) {
     SimConfig cfg;
     cfg.gpu_count = c.gpu_count;
     cfg.capacity_mb = c.capacity_mb;
+    if (c.policy < 0 || c.policy > 2) throw std::invalid_argument("policy must be 0 (lb), 1 (lalb) or 2 (lalbo3)");
     cfg.scheduler.policy = c.policy == 0 ? Policy::LB : c.policy == 1 ? Policy::LALB : Policy::LALBO3;
     cfg.scheduler.o3_limit = c.o3_limit;
     cfg.workload.working_set_size = c.working_set;

@@ -97,3 +97,14 @@ def test_model_registration_limits_without_gpu():
     assert "multiples of 32" in reg([1000, 1024])[1]
     assert "multiples of 32" in reg([1024, 1001])[1]
     assert "family" in reg([1024, 1000], family=7)[1]
+
+
+def test_sim_rejects_unknown_policy_values():
+    """A policy id outside 0..2 is a caller error through the C-ABI, not a silent LALBO3."""
+    import pytest
+    import simabi
+    lib = simabi.load_product()
+    for bad in (3, -1, 17):
+        cfg = simabi.make_config(gpus=1, capacity_mb=204.0, policy=bad, minutes=1)
+        with pytest.raises(simabi.SimError, match="policy"):
+            lib.run(simabi.table1_catalog(), cfg)

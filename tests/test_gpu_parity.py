@@ -76,6 +76,19 @@ def test_replay_schedule_bit_exact(gfx, catalog, policy, gpus):
     assert res.loads_h2d + res.loads_p2p == res.misses
 
 
+def test_replay_rejects_models_registered_out_of_catalog_order(gfx):
+    """Catalog row i must be the model registered at index i: a store holding
+    another model there is refused at replay creation (domain error), instead
+    of silently serving the wrong weights under the catalog's id."""
+    specs = gfx.load_model_specs("mlp_c2")
+    try:
+        gfx.register_models(list(reversed(specs)))
+        with pytest.raises(gfx._ffi.GfxError, match="not catalog row"):
+            gfx.Replay(gfx.catalog_text("mlp_c2"), gfx.sim_config(gpus=1, capacity_mb=204.0, minutes=1))
+    finally:
+        gfx.register_models(specs)
+
+
 def test_replay_outputs_match_oracle(gfx, olib):
     cat = gfx.catalog_text("mlp_c2")
     specs = gfx.load_model_specs("mlp_c2")
