@@ -517,6 +517,10 @@ def main():
                           "note": "achieved = H2D bytes / summed H2D load-event time; peak = measured pinned H2D "
                                   "(1 GiB copies, tools/h2d_rate.cu); NVLink peer fetches (G > 1) are timed "
                                   "separately (p2p_*)",
+                          "h2d_aggregate_gbs": round(h2d_bytes / (dev_ms * 1e6), 2),
+                          "h2d_aggregate_note": "all ranks' model-load bytes / the step's device time (max over "
+                                                "ranks): the host links' combined load rate while GPUs load "
+                                                "concurrently",
                           "p2p_loads_per_step": p2p_loads // a.steps, "p2p_bytes_per_step": int(p2p_bytes // a.steps),
                           "p2p_achieved_gbs": round(p2p_bytes / (p2p_ms * 1e6), 2) if p2p_ms else None,
                           "p2p_peak_gbs": NVLINK_PEER_GBS},

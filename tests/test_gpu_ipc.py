@@ -41,7 +41,7 @@ def _digests(outs):
     return d
 
 
-def _worker(rank, port, q):
+def _worker(rank, port, q, distinct_devices=False):
     import torch.distributed as dist
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
@@ -50,7 +50,8 @@ def _worker(rank, port, q):
         import paper_2303_05601_b200 as gfx
         gfx.register_models(gfx.load_model_specs("mlp_c2"))
         cat = gfx.catalog_text("mlp_c2_paper")
-        rep = gfx.Replay(cat, _cfg(gfx), n_devices=1, only_gpu=rank, use_p2p=True, keep_outputs=True)
+        rep = gfx.Replay(cat, _cfg(gfx), n_devices=1, first_device=rank if distinct_devices else 0, only_gpu=rank,
+                         use_p2p=True, keep_outputs=True)
         rep.connect_peers()
         runs = []
         for _ in range(2):  # the second run exercises the cumulative cross-process counters
@@ -67,6 +68,10 @@ def _worker(rank, port, q):
 
 
 def test_cross_process_peer_fetch_matches_single_process():
+    run_cross_process(distinct_devices=False)
+
+
+def run_cross_process(distinct_devices):
     import torch.multiprocessing as mp
 
     import paper_2303_05601_b200 as gfx
@@ -82,7 +87,7 @@ def test_cross_process_peer_fetch_matches_single_process():
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, port, q)) for r in range(WORLD)]
+    procs = [ctx.Process(target=_worker, args=(r, port, q, distinct_devices)) for r in range(WORLD)]
     for p in procs:
         p.start()
     got = dict(q.get(timeout=600) for _ in range(WORLD))
