@@ -33,11 +33,12 @@ for r in rows:
     t0 = time.perf_counter()
     for _ in range(iters):
         F.check(F.gfx_infer(a, r, x.data_ptr(), y.data_ptr(), 32, None))
+    t_enq = time.perf_counter() - t0
     F.check(F.gfx_synchronize(a))
     per = (time.perf_counter() - t0) / iters
     alg = sum(4 * (k * n + n) for k, n in zip(s.dims[:-1], s.dims[1:])) + 4 * 32 * (s.dims[0] + 2 * s.dims[-1])
     print(f"row {r:2d} {s.model_id:18s} {'x'.join(map(str, s.dims)):28s} {per*1e6:7.1f} us  "
-          f"{alg/per/1e9:6.0f} GB/s = {alg/per/1e9/peak:.3f} of HBM", flush=True)
+          f"{alg/per/1e9:6.0f} GB/s = {alg/per/1e9/peak:.3f} of HBM  (host enqueue {t_enq / iters * 1e6:.1f} us)", flush=True)
 # all rows interleaved (a different model every launch, as in a replay of hits)
 t0 = time.perf_counter()
 for i in range(iters):
