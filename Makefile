@@ -30,7 +30,7 @@ HDRS      := $(wildcard include/*.h include/gpufaas/*.hpp $(PKG)/csrc/*/*.hpp $(
 
 .PHONY: all product oracle ref clean FORCE
 all: product
-product: $(OUT)/libgpufaas_b200.so
+product: $(OUT)/libgpufaas_b200.so $(OUT)/gfx_managerd
 
 # Rebuild everything when the compiler flags change (e.g. K1_DEBUG=1 <-> release).
 $(OBJ)/.flags: FORCE
@@ -48,6 +48,10 @@ $(OBJ)/%.cu.o: $(PKG)/csrc/%.cu $(HDRS) $(OBJ)/.flags
 $(OUT)/libgpufaas_b200.so: $(HOST_OBJS) $(CU_OBJS)
 	@mkdir -p $(OUT)
 	$(NVCC) -shared $(ARCH) -cudart static -o $@ $^ -lpthread -ldl -lrt
+
+# The per-GPU manager daemon (N1), linked against the library next to it.
+$(OUT)/gfx_managerd: $(PKG)/csrc/daemon/managerd.cpp $(OUT)/libgpufaas_b200.so include/gpufaas_b200.h
+	$(CXX) -std=c++20 -O2 -Wall -Iinclude $< -o $@ -L$(OUT) -lgpufaas_b200 -Wl,-rpath,'$$ORIGIN'
 
 oracle:
 	$(MAKE) -C oracle oracle

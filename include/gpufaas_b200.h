@@ -263,6 +263,48 @@ int gfx_replay_destroy(gfx_replay_t r);
 /* create + run + destroy */
 int gfx_replay(const gfx_replay_args* args, gfx_replay_result* out);
 
+/* ------------------------------------------------------------ cluster (N1) */
+/* One GPU Manager daemon process per GPU (gfx_managerd: the paper's GPU Manager,
+ * PAPER.md:288-303, owning that GPU's pre-allocated HBM arena, copy/compute
+ * streams and pinned model store), fed by the global cache manager — the
+ * reference control plane (scheduler + ClusterState,
+ * proj/include/gpufaas/cluster.hpp:88-140) in the calling process — over one
+ * POSIX shared-memory segment with a command ring and a completion ring per GPU.
+ * gfx_cluster_run replays the deterministic schedule (run_stream, bit-exact
+ * with the reference); gfx_cluster_run_live serves the trace in real time with
+ * device-observed completions (run_live) — with one process per GPU. False
+ * misses fetch from the holder daemon's arena over NVLink (CUDA IPC, device-side
+ * ordering by stream memory operations on IPC-mapped flag words). Each daemon
+ * builds request i's input on the device from its parameter stream
+ * (gfx_input_seed) and keeps every output for gfx_cluster_output. */
+typedef struct gfx_cluster_s* gfx_cluster_t;
+typedef struct {
+    const char* catalog_csv;
+    const char* trace_csv;         /* NULL -> synthetic trace of cfg */
+    gfx_sim_config cfg;            /* gpu_count <= 8 */
+    const gfx_model_desc* models;  /* catalog row i = models[i] (checked by seed), at most 64 */
+    int32_t n_models;
+    int32_t use_p2p;               /* false misses fetch from the holder daemon (NVLink / CUDA IPC) */
+    const int32_t* devices;        /* CUDA device of each GPU (NULL: device 0 for all = emulated peers) */
+    int32_t spawn;                 /* 1: start gfx_managerd processes (next to the library); 0: they attach themselves */
+    int32_t pad_;
+    const char* shm_name;          /* NULL: a unique name (spawn = 1); spawn = 0 needs the name the daemons use */
+} gfx_cluster_args;
+const char* gfx_cluster_last_error(void);
+int gfx_cluster_create(const gfx_cluster_args* args, gfx_cluster_t* out);
+int gfx_cluster_run(gfx_cluster_t c, gfx_replay_result* out);
+int gfx_cluster_run_live(gfx_cluster_t c, double time_scale, double ema_alpha, gfx_replay_result* out);
+/* Output of request_id in the last run (fetched from the daemon that served it). */
+int gfx_cluster_output(gfx_cluster_t c, int32_t request_id, void* host, uint64_t bytes);
+int gfx_cluster_request_gpu(gfx_cluster_t c, int32_t request_id, int32_t* gpu);
+int gfx_cluster_destroy(gfx_cluster_t c); /* stops the daemons */
+/* The daemon loop: attach to the segment as GPU gpu_index, serve until stopped.
+ * Returns 0 when stopped, nonzero on failure (the message is in the segment). */
+int gfx_managerd_serve(const char* shm_name, int32_t gpu_index);
+/* Test: a forked producer pushes n commands through a shared-memory command
+ * ring; the caller pops and checks them in order (no device needed). */
+int gfx_cluster_ring_selftest(int64_t n);
+
 #ifdef __cplusplus
 }
 #endif

@@ -11,7 +11,8 @@ from .models import (ModelSpec, load_model_specs, register_models, model_seed, c
                      DATA_DIR)
 from .replay import (Replay, ReplayResult, sim_config, c3_config, c3_rpm, C3_ARENA_MB,  # noqa: F401
                      azure_trace_to_csv)
+from .cluster import Cluster, ClusterError  # noqa: F401
 
 __all__ = ["lib", "GfxError", "ModelSpec", "load_model_specs", "register_models", "model_seed",
            "catalog_text", "Replay", "ReplayResult", "sim_config", "c3_config", "c3_rpm", "C3_ARENA_MB", "azure_trace_to_csv",
-           "DATA_DIR"]
+           "DATA_DIR", "Cluster", "ClusterError"]

@@ -57,6 +57,13 @@ class ReplayResultC(C.Structure):
                                    "sim_avg_latency_s", "mlp_flops", "mlp_weight_bytes", "p2p_ms")]
 
 
+class ClusterArgs(C.Structure):
+    _fields_ = [("catalog_csv", C.c_char_p), ("trace_csv", C.c_char_p), ("cfg", SimConfig),
+                ("models", C.POINTER(ModelDesc)), ("n_models", C.c_int32), ("use_p2p", C.c_int32),
+                ("devices", C.POINTER(C.c_int32)), ("spawn", C.c_int32), ("pad_", C.c_int32),
+                ("shm_name", C.c_char_p)]
+
+
 def _sig(name, res, args):
     f = getattr(lib, name)
     f.restype = res
@@ -113,6 +120,16 @@ gfx_replay_destroy = _sig("gfx_replay_destroy", C.c_int, [_vp])
 gfx_replay_ipc_blob_bytes = _sig("gfx_replay_ipc_blob_bytes", C.c_uint64, [])
 gfx_replay_ipc_export = _sig("gfx_replay_ipc_export", C.c_int, [_vp, _vp, C.c_uint64])
 gfx_replay_ipc_import = _sig("gfx_replay_ipc_import", C.c_int, [_vp, _vp, C.c_int32])
+
+gfx_cluster_last_error = _sig("gfx_cluster_last_error", C.c_char_p, [])
+gfx_cluster_create = _sig("gfx_cluster_create", C.c_int, [C.POINTER(ClusterArgs), C.POINTER(_vp)])
+gfx_cluster_run = _sig("gfx_cluster_run", C.c_int, [_vp, C.POINTER(ReplayResultC)])
+gfx_cluster_run_live = _sig("gfx_cluster_run_live", C.c_int, [_vp, C.c_double, C.c_double, C.POINTER(ReplayResultC)])
+gfx_cluster_output = _sig("gfx_cluster_output", C.c_int, [_vp, C.c_int32, _vp, C.c_uint64])
+gfx_cluster_request_gpu = _sig("gfx_cluster_request_gpu", C.c_int, [_vp, C.c_int32, C.POINTER(C.c_int32)])
+gfx_cluster_destroy = _sig("gfx_cluster_destroy", C.c_int, [_vp])
+gfx_cluster_ring_selftest = _sig("gfx_cluster_ring_selftest", C.c_int, [C.c_int64])
+gfx_managerd_serve = _sig("gfx_managerd_serve", C.c_int, [C.c_char_p, C.c_int32])
 
 
 def check(rc: int):

@@ -22,14 +22,10 @@
 #include <string>
 #include <vector>
 
+#include "capi_common.hpp"
 #include "gpufaas/engine.hpp"
 #include "gpufaas_b200.h"
 #include "manager.cuh"
-
-namespace gpufaas::capi {
-SimConfig to_sim_config(const gfx_sim_config& c);
-std::vector<Request> make_requests(const gfx_sim_config& c, const Catalog& cat, const char* trace_csv);
-}  // namespace gpufaas::capi
 
 using gfx::GpuManager;
 using gfx::KernelTimer;
@@ -41,24 +37,7 @@ thread_local std::string g_err;
 
 template <typename F>
 int guarded(F&& f) {
-    try {
-        f();
-        return GFX_OK;
-    } catch (const gfx::CudaError& e) {
-        g_err = e.what();
-        return GFX_ERR_CUDA;
-    } catch (const std::logic_error& e) {
-        // std::invalid_argument derives from logic_error but is a caller error.
-        if (dynamic_cast<const std::invalid_argument*>(&e)) {
-            g_err = e.what();
-            return GFX_ERR_DOMAIN;
-        }
-        g_err = e.what();
-        return GFX_ERR_INTERNAL;
-    } catch (const std::exception& e) {
-        g_err = e.what();
-        return GFX_ERR_DOMAIN;
-    }
+    return gpufaas::capi::guarded_call(g_err, std::forward<F>(f));
 }
 
 double elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
@@ -67,13 +46,7 @@ double elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
     return ms;
 }
 
-double percentile(std::vector<double> v, double q) {
-    if (v.empty()) return 0.0;
-    std::sort(v.begin(), v.end());
-    size_t rank = static_cast<size_t>(std::ceil(q / 100.0 * static_cast<double>(v.size())));
-    rank = std::clamp<size_t>(rank, 1, v.size());
-    return v[rank - 1];
-}
+using gpufaas::capi::percentile;
 
 }  // namespace
 
@@ -554,26 +527,7 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
         res.false_misses = sim.report.false_misses;
         res.local_enqueues = sim.report.local_enqueues;
         res.evictions = sim.report.evictions;
-        uint64_t h = 14695981039346656037ULL;
-        auto fnv = [&](const void* p, size_t len) {
-            const unsigned char* c = static_cast<const unsigned char*>(p);
-            for (size_t i = 0; i < len; ++i) {
-                h ^= c[i];
-                h *= 1099511628211ULL;
-            }
-        };
-        for (const gpufaas::Decision& d : sim.decisions) {
-            const int32_t a[6] = {static_cast<int32_t>(d.kind), d.request_id, d.gpu_id, d.from_local_queue,
-                                  d.false_miss, d.skip_count};
-            fnv(a, sizeof a);
-            fnv(&d.completion_us, 8);
-            fnv(&d.load_us, 8);
-            fnv(&d.infer_us, 8);
-            const int32_t ne = static_cast<int32_t>(d.evicted.size());
-            fnv(&ne, 4);
-            for (const std::string& s : d.evicted) fnv(s.c_str(), s.size() + 1);
-        }
-        res.decision_digest = h;
+        res.decision_digest = gpufaas::capi::decision_digest(sim.decisions);
         res.device_ms = dev_ms;
         res.host_ms = std::chrono::duration<double, std::milli>(h1 - h0).count();
         res.sched_ms = std::chrono::duration<double, std::milli>(s1 - s0).count();

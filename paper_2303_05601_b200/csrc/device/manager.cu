@@ -44,6 +44,20 @@ void mlp_layout(const gfx_model_desc& d, std::vector<uint64_t>& w_off, std::vect
     bytes = align(off, 256);
 }
 
+uint32_t model_pages(const gfx_model_desc& desc) {
+    uint64_t bytes = 0;
+    if (desc.family == GFX_MODEL_BERT) {
+        bytes = bert_layout(desc.n_layers, desc.dims[0], desc.dims[1], desc.dims[2], desc.dims[3]).bytes;
+    } else if (desc.family == GFX_MODEL_MLP) {
+        if (desc.n_layers < 1 || desc.n_layers > GFX_MAX_LAYERS) throw std::invalid_argument("bad layer count");
+        std::vector<uint64_t> w, b;
+        mlp_layout(desc, w, b, bytes);
+    } else {
+        throw std::invalid_argument("unsupported model family");
+    }
+    return static_cast<uint32_t>((bytes + kPageBytes - 1) / kPageBytes);
+}
+
 ModelStore& ModelStore::get() {
     static ModelStore store;
     return store;

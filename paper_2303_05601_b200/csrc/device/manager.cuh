@@ -53,6 +53,9 @@ private:
     std::vector<std::unique_ptr<ModelBlob>> blobs_;
 };
 
+// Arena pages a model occupies (its blob layout, without building the blob).
+uint32_t model_pages(const gfx_model_desc& desc);
+
 // Blob layout of an MLP: per layer the weight tiles (16 KB,
 // 16 KB-aligned, N padded to 128 rows) then b [N] fp32 (256 B-aligned).
 void mlp_layout(const gfx_model_desc& d, std::vector<uint64_t>& w_off, std::vector<uint64_t>& b_off,

@@ -108,3 +108,30 @@ def test_sim_rejects_unknown_policy_values():
         cfg = simabi.make_config(gpus=1, capacity_mb=204.0, policy=bad, minutes=1)
         with pytest.raises(simabi.SimError, match="policy"):
             lib.run(simabi.table1_catalog(), cfg)
+
+
+def test_cluster_command_ring_across_processes():
+    """N1's shared-memory SPSC command ring: 200k commands from a forked producer
+    arrive in order and untorn (the daemon/coordinator transport, no device)."""
+    import paper_2303_05601_b200 as gfx
+    rc = gfx._ffi.gfx_cluster_ring_selftest(200_000)
+    assert rc == 0, gfx._ffi.gfx_cluster_last_error()
+
+
+def test_cluster_without_device_fails_loudly():
+    """The manager daemons start, fail on the missing device, and the coordinator
+    raises the daemon's CUDA error (no hang, no CPU fallback, segment removed)."""
+    import ctypes as C
+    import os
+
+    import pytest
+
+    import paper_2303_05601_b200 as gfx
+    n = C.c_int(0)
+    if gfx._ffi.gfx_device_count(C.byref(n)) == 0 and n.value > 0:
+        pytest.skip("a GPU is present (covered by tests/test_gpu_cluster.py)")
+    with pytest.raises(gfx.ClusterError) as ei:
+        gfx.Cluster(gfx.catalog_text("mlp_c2_paper"), gfx.sim_config(gpus=2, capacity_mb=204.0, minutes=1),
+                    gfx.load_model_specs("mlp_c2"))
+    assert ei.value.code == 3 and "gfx_managerd" in str(ei.value)
+    assert not [f for f in os.listdir("/dev/shm") if f.startswith(f"gfx_cluster_{os.getpid()}_")]
