@@ -163,6 +163,11 @@ Shm* map_shm(const char* name, bool create, int* fd_out) {
         close(fd);
         throw std::runtime_error(std::string("ftruncate shm: ") + std::strerror(errno));
     }
+    struct stat st{};
+    if (!create && (fstat(fd, &st) != 0 || static_cast<size_t>(st.st_size) < sizeof(Shm))) {
+        close(fd);  // created but not sized yet: the caller retries
+        throw std::runtime_error("shm segment not ready");
+    }
     void* p = mmap(nullptr, sizeof(Shm), PROT_READ | PROT_WRITE, MAP_SHARED, fd, 0);
     if (p == MAP_FAILED) {
         close(fd);
@@ -215,7 +220,9 @@ struct Daemon {
         G = shm->gpu_count;
         M = shm->n_models;
         GFX_CUDA(cudaSetDevice(b.device));
-        for (int i = 0; i < M; ++i) ModelStore::get().add(i, shm->models[i]);
+        for (int i = 0; i < M; ++i)  // a rank may have registered the models already (same process)
+            if (!ModelStore::get().has(i) || ModelStore::get().at(i).desc.seed != shm->models[i].seed)
+                ModelStore::get().add(i, shm->models[i]);
         const gfx::ModelBlob& b0 = ModelStore::get().at(0);
         in_bytes = b0.in_bytes;
         out_bytes = b0.out_bytes;
@@ -509,7 +516,6 @@ struct gfx_cluster_s : gpufaas::ExecutionListener, gpufaas::LiveExecutor {
                           : "/gfx_cluster_" + std::to_string(getpid()) + "_" + std::to_string(seq.fetch_add(1));
         shm = map_shm(name.c_str(), true, &fd);
         std::memset(static_cast<void*>(shm), 0, sizeof(Shm));
-        shm->magic = kMagic;
         shm->gpu_count = G;
         shm->n_models = M;
         shm->n_requests = static_cast<int32_t>(requests.size());
@@ -517,6 +523,7 @@ struct gfx_cluster_s : gpufaas::ExecutionListener, gpufaas::LiveExecutor {
         shm->arena_bytes = pages * gfx::kPageBytes;
         for (int i = 0; i < M; ++i) shm->models[i] = a.models[i];
         for (int g = 0; g < G; ++g) shm->gpu[g].device = a.devices ? a.devices[g] : 0;
+        __atomic_store_n(&shm->magic, kMagic, __ATOMIC_RELEASE);  // header complete: daemons may attach
         shadow.assign(static_cast<size_t>(G), {});
         for (Shadow& s : shadow) {
             for (uint32_t p = 0; p < pages; ++p) s.free.insert(p);
@@ -792,8 +799,20 @@ int gfx_cluster_ring_selftest(int64_t n) {
 int gfx_managerd_serve(const char* shm_name, int32_t gpu_index) {
     Daemon d;
     try {
-        d.shm = map_shm(shm_name, false, &d.fd);
-        if (d.shm->magic != kMagic) throw std::invalid_argument("not a gfx cluster segment");
+        // The coordinator may create the segment after a rank started its daemon (spawn = 0).
+        for (int i = 0;; ++i) {
+            try {
+                d.shm = map_shm(shm_name, false, &d.fd);
+                break;
+            } catch (const std::runtime_error&) {
+                if (i >= 12000) throw;  // 60 s
+                std::this_thread::sleep_for(std::chrono::milliseconds(5));
+            }
+        }
+        for (int i = 0; __atomic_load_n(&d.shm->magic, __ATOMIC_ACQUIRE) != kMagic; ++i) {
+            if (i >= 60000) throw std::runtime_error("segment never initialised");
+            std::this_thread::sleep_for(std::chrono::milliseconds(1));
+        }
         if (gpu_index < 0 || gpu_index >= d.shm->gpu_count) throw std::invalid_argument("gpu index out of range");
         d.gpu = gpu_index;
         d.setup();
