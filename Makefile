@@ -18,6 +18,9 @@ CXXFLAGS := -std=c++20 -O2 -fPIC -ffp-contract=off -Wall -Wextra $(INC) -I$(CUDA
 NVFLAGS  := -std=c++20 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -ffp-contract=off \
             --expt-relaxed-constexpr -Xptxas -v $(INC)
 
+ifeq ($(K2_DEBUG),1)
+NVFLAGS += -DGFX_K2_DEBUG   # BERT GEMM per-CTA phase tables (debug only, never shipped)
+endif
 ifeq ($(K1_DEBUG),1)
 NVFLAGS += -DGFX_K1_DEBUG $(K1_EXTRA)   # K1 wait watchdogs + phase marks (debug only, never shipped)
 endif

@@ -1,7 +1,7 @@
 """Device time of one BERT-base (C5) forward through the C-ABI: model 0 of the
 bert_c5 catalog resident, `iters` back-to-back gfx_infer calls, wall time of the
 synchronised loop (host launch cost ~0.2 ms/forward < device time).
-usage: python tools/bert_bench.py [iters]"""
+usage: python tools/bert_bench.py [iters] [pair 0|1]"""
 import ctypes as C
 import os
 import sys
@@ -17,6 +17,8 @@ gfx.register_models(specs[:1])
 s = specs[0]
 a = C.c_void_p()
 F.check(F.gfx_arena_create(0, C.c_uint64(s.pages << 21), C.byref(a)))
+pair = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+F.check(F.gfx_arena_set_option(a, F.GFX_OPT_GEMM_PAIR, pair))
 F.check(F.gfx_load_h2d(a, 0, None))
 inb, outb = C.c_uint64(), C.c_uint64()
 F.check(F.gfx_model_io_bytes(0, C.byref(inb), C.byref(outb)))
@@ -35,4 +37,4 @@ dt = (time.perf_counter() - t0) / iters
 L, D, FF, S = s.dims[0], 768, s.dims[2], 128
 T = batch * S
 flops = L * (2.0 * T * (4 * D * D + 2 * D * FF) + 4.0 * T * S * D) + 2.0 * batch * D * D
-print(f"bert {s.model_id}: {dt * 1e3:.3f} ms/forward  {flops / dt / 1e12:.1f} TFLOP/s")
+print(f"bert {s.model_id} (pair={pair}): {dt * 1e3:.3f} ms/forward  {flops / dt / 1e12:.1f} TFLOP/s")
