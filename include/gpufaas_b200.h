@@ -41,7 +41,7 @@ extern "C" {
 #define GFX_ERR_CUDA 3
 
 #define GFX_PAGE_BYTES (2u << 20) /* HBM arena page: 2 MiB */
-#define GFX_MAX_PAGES 192         /* largest model: 384 MiB */
+#define GFX_MAX_PAGES 1024        /* largest model: 2 GiB (the page table travels by value in kernel parameters) */
 #define GFX_MAX_LAYERS 16
 
 /* ---------------------------------------------------------------- sim ABI */

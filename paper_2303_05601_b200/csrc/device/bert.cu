@@ -134,7 +134,6 @@ __global__ void __launch_bounds__(kGThreads, 1)
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
     __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], tfull_bar[2], tempty_bar[2], res_bar[4];
     __shared__ uint32_t tmem_s;
-    __shared__ uint32_t pt[GFX_MAX_PAGES];
     __shared__ float bias_s[kBN];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -150,7 +149,9 @@ __global__ void __launch_bounds__(kGThreads, 1)
     auto tile_m0 = [&](int t) { return kPair ? ((t / n_tiles) * 2 + static_cast<int>(rank)) * kGM : (t / n_tiles) * kGM; };
     const int ktiles_row = a.K / kGK;  // blob weight tiles per 128 rows
 
-    for (int i = tid; i < static_cast<int>(a.pt.n); i += kGThreads) pt[i] = a.pt.page[i];
+    // The page table is read straight from the __grid_constant__ parameter (up to
+    // GFX_MAX_PAGES entries, 4 KB: no room for a shared-memory copy).
+    const uint32_t* const pt = a.pt.page;
     if (tid == 0) {
         for (int s = 0; s < kStages; ++s) {
             // One arrive.expect_tx per producer warp: A (warp 0) and each B tile

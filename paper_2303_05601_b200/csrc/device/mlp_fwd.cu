@@ -252,7 +252,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     __shared__ __align__(8) uint64_t w_full[kSlots], raw_full[kSlots], ready[kSlots], step_done[kSlots];
     __shared__ __align__(8) uint64_t tfull[kAccBufs], tempty[kAccBufs];
     __shared__ uint32_t tmem_base_s;
-    __shared__ uint32_t pt[GFX_MAX_PAGES];
     __shared__ float red_s[2][4];
 #ifdef GFX_K1_DEBUG
     __shared__ unsigned long long k1_marks[32];
@@ -268,7 +267,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int grid = a.grid;
     const int L = a.L;
 
-    for (int i = tid; i < static_cast<int>(a.pt.n); i += kThreads) pt[i] = a.pt.page[i];
+    // The page table is read straight from the __grid_constant__ parameter (up to
+    // GFX_MAX_PAGES entries, 4 KB: no room for a shared-memory copy).
+    const uint32_t* const pt = a.pt.page;
     if (tid == 0) {
         for (int s = 0; s < kSlots; ++s) {
             mbar_init(&w_full[s], 1);

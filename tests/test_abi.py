@@ -97,6 +97,8 @@ def test_model_registration_limits_without_gpu():
     assert "multiples of 32" in reg([1000, 1024])[1]
     assert "multiples of 32" in reg([1024, 1001])[1]
     assert "family" in reg([1024, 1000], family=7)[1]
+    # 16 layers of 8192 x 8192 fp32 = 4.3 GB: beyond the 1024-page (2 GiB) page table
+    assert "page-table limit" in reg([8192] * 16 + [1000], n_layers=16)[1]
 
 
 def test_sim_rejects_unknown_policy_values():

@@ -231,7 +231,8 @@ def test_pipelined_replay(gfx, policy, gpus):
     [96, 160, 352, 100],               # widths that are not multiples of 64 / 128
     [256] * 16 + [1000],               # the maximum of 16 layers
     [8192, 8192, 1000],                # the maximum width (282 MiB of weights)
-], ids=["L1", "min", "h64", "odd", "L16", "w8192"])
+    [1024, 8192, 8192, 8192, 1000],    # 604 MB, 289 arena pages (beyond round 1's 192-page table)
+], ids=["L1", "min", "h64", "odd", "L16", "w8192", "p289"])
 def test_mlp_edge_shapes(gfx, olib, dims):
     """Edge shapes of the one-launch forward against the oracle's fp64 forward."""
     import ctypes as C
