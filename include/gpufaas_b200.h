@@ -162,7 +162,8 @@ int gfx_infer_debug(gfx_arena_t a, int model_idx, const void* in, void* out, int
 /* Test/debug: one encoder GEMM of a resident BERT model with its fused epilogue,
  * on `tokens` rows (bf16, device pointers). op 0: QKV (+bias) [tokens x 3d];
  * 1: attention output (+bias, +resid) [tokens x d]; 2: FFN1 (+bias, GELU)
- * [tokens x ffn]; 3: FFN2 (+bias, +resid) [tokens x d]. Synchronous. */
+ * [tokens x ffn]; 3: FFN2 (+bias, +resid) [tokens x d]; 4 / 5: op 1 / 3 followed
+ * by LayerNorm 1 / 2 (the forward's fused residual + LayerNorm step). Synchronous. */
 int gfx_bert_gemm(gfx_arena_t a, int model_idx, int layer, int op, const void* x, const void* resid, void* y,
                   int tokens);
 

@@ -22,6 +22,8 @@
 #include <algorithm>
 #include <cstdio>
 #include <vector>
+#include <map>
+#include <mutex>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -55,9 +57,34 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
             a.dbg[blockIdx.x * 24 + (i)] = t_;                                       \
         }                                                                            \
     } while (0)
+// Per-launch span (debug build): [0] earliest CTA start, [1] latest CTA end
+// (%globaltimer ns) of one kernel launch; bert_forward prints the forward's
+// kernel timeline from these (gaps between launches included).
+#define K2_SPAN_BEGIN(tr)                                                            \
+    do {                                                                             \
+        if ((tr) && threadIdx.x == 0) {                                              \
+            unsigned long long t_;                                                   \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                   \
+            atomicMin((tr), t_);                                                     \
+        }                                                                            \
+    } while (0)
+#define K2_SPAN_END(tr)                                                              \
+    do {                                                                             \
+        if ((tr) && threadIdx.x == 0) {                                              \
+            unsigned long long t_;                                                   \
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));                   \
+            atomicMax((tr) + 1, t_);                                                 \
+        }                                                                            \
+    } while (0)
 #else
 #define K2_MARK(i) \
     do {           \
+    } while (0)
+#define K2_SPAN_BEGIN(tr) \
+    do {                  \
+    } while (0)
+#define K2_SPAN_END(tr) \
+    do {                \
     } while (0)
 #endif
 
@@ -78,6 +105,24 @@ __device__ __forceinline__ float gelu(float x) {
     return 0.5f * x * (1.0f + copysignf(erf_abs, x));
 }
 
+// Debug build: kernel spans of one traced forward (bert_forward's 10th call).
+#ifdef GFX_K2_DEBUG
+struct SpanTrace {
+    unsigned long long* buf = nullptr;  // [kMax][2]
+    std::vector<const char*> names;
+    bool on = false;
+    static constexpr int kMax = 256;
+};
+SpanTrace g_span;
+unsigned long long* next_span(const char* name) {
+    if (!g_span.on || static_cast<int>(g_span.names.size()) >= SpanTrace::kMax) return nullptr;
+    g_span.names.push_back(name);
+    return g_span.buf + 2 * (g_span.names.size() - 1);
+}
+#else
+inline unsigned long long* next_span(const char*) { return nullptr; }
+#endif
+
 // ------------------------------------------------------------------ K2 GEMM
 // Persistent: one CTA per SM loops over 128 x kBN output tiles; the TMEM holds
 // two accumulators so the epilogue of tile i overlaps the MMAs of tile i+1.
@@ -93,17 +138,35 @@ constexpr int kGEpiWarps = 16, kGAWarp = 16, kGMmaWarp = 17, kGBWarp0 = 18;
 constexpr uint32_t kGATile = 128 * 128;  // A: 128 rows x 64 bf16 (16 KB)
 constexpr uint32_t kGSmem = 192 * 1024;  // stage ring budget
 
-enum Epi : int { kEpiBias = 0, kEpiGelu = 1, kEpiResid = 2 };
+// kEpiResidLN: bias + residual + the post-LN LayerNorm of the whole d = 768 row,
+// fused (K4 disappears from the forward). The row's three 256-column tiles are
+// computed by the three CTAs of a cluster; each CTA reduces its tile's per-row
+// (mean, M2) and sends it to all three CTAs by st.async into their shared
+// memory (DSMEM, completing a tx-counted mbarrier), so the statistics never
+// touch global memory and no CTA waits on a flag in L2. One tile per CTA (the
+// host falls back to kEpiResid + layernorm_kernel when the row blocks exceed
+// the resident clusters).
+enum Epi : int { kEpiBias = 0, kEpiGelu = 1, kEpiResid = 2, kEpiResidLN = 3 };
 
 struct GemmArgs {
     unsigned long long* dbg;      // GFX_K2_DEBUG builds: [grid][24] %globaltimer marks, else nullptr
+    unsigned long long* span;     // GFX_K2_DEBUG builds: this launch's [start, end] span, else nullptr
     const char* arena;
     uint64_t w_off, b_off;        // weight tiles, fp32 bias
+    uint64_t g_off, be_off;       // kEpiResidLN: LayerNorm gamma / beta (fp32)
     __nv_bfloat16* y;             // [T x N]
-    const __nv_bfloat16* resid;   // [T x N] (kEpiResid)
+    const __nv_bfloat16* resid;   // [T x N] (kEpiResid, kEpiResidLN)
     int T, K, N;
     PageTable pt;
 };
+
+// Chan et al. pairwise combination of (count, mean, M2) partial statistics.
+__device__ __forceinline__ void chan_combine(float& n_a, float& mean_a, float& m2_a, float n_b, float mean_b, float m2_b) {
+    const float n = n_a + n_b, dlt = mean_b - mean_a;
+    mean_a = fmaf(dlt, n_b / n, mean_a);
+    m2_a = m2_a + m2_b + dlt * dlt * (n_a * n_b / n);
+    n_a = n;
+}
 
 // kPair: 2-SM tcgen05 (cta_group::2). A CTA pair (cluster of 2) computes a
 // 256 x kBN tile: each CTA stages its own 128 rows of A and its half of the
@@ -130,14 +193,19 @@ __global__ void __launch_bounds__(kGThreads, 1)
     constexpr uint32_t kStage = kGATile + kBBytes;
     constexpr int kStages = static_cast<int>(kGSmem / kStage);
     constexpr uint32_t kTmemCols = 2 * kBN <= 256 ? 256 : 512;
+    constexpr bool kLN = kEpi == kEpiResidLN;
+    constexpr bool kCluster = kPair || kLN;
+    static_assert(!kLN || (kBN == 256 && !kPair), "the fused LayerNorm runs 128 x 256 single-CTA tiles");
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // stays in the shared window
     __shared__ __align__(8) uint64_t full_bar[kStages], empty_bar[kStages], tfull_bar[2], tempty_bar[2], res_bar[4];
+    __shared__ __align__(8) uint64_t stat_bar;  // kLN: the three CTAs' row statistics landed
     __shared__ uint32_t tmem_s;
     __shared__ float bias_s[kBN];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     if (tid == 0) K2_MARK(0);
+    K2_SPAN_BEGIN(a.span);
     const int n_tiles = a.N / kBN, m_tiles = a.T / kGM;
     // Tile sequence of this CTA: single -> tiles t = blockIdx.x (step grid);
     // pair -> pair tiles t = cluster id (step clusters), rows 2*(t / n) + rank.
@@ -166,12 +234,22 @@ __global__ void __launch_bounds__(kGThreads, 1)
             mbar_init(&tempty_bar[b], kPair ? 2 * kGEpiWarps : kGEpiWarps);  // epilogue warps (of both CTAs in pair mode)
         }
         for (int g = 0; g < 4; ++g) mbar_init(&res_bar[g], 1);
+        if (kLN) mbar_init(&stat_bar, 1);
         mbar_fence_init();
+        // 3 senders x 128 rows x (mean, M2); remote bytes may land before this
+        // CTA's epilogue runs, never before the cluster_sync below.
+        if (kLN) mbar_arrive_expect_tx(&stat_bar, 3 * 128 * 8);
         tma_prefetch_desc(&tmap_x);
         tma_prefetch_desc(&tmap_y);
-        if (kEpi == kEpiResid) tma_prefetch_desc(&tmap_r);
+        if (kEpi == kEpiResid || kLN) tma_prefetch_desc(&tmap_r);
         if (kPair) tma_prefetch_desc(&tmap_w);
     }
+    // kLN: the residual tile (8 boxes of 128 rows x 32 columns, SWIZZLE_64B) goes
+    // into the two ring stages after the tile's last K stage, loaded as soon as
+    // the MMAs free them; the normalised output is written over it in place.
+    auto ln_box = [&](int c) {
+        return smem + static_cast<size_t>((nk + c / 6) % kStages) * kStage + static_cast<size_t>(c % 6) * 8192;
+    };
     if (warp == kGMmaWarp) {
         if (kPair)
             tmem_alloc_pair<kTmemCols>(&tmem_s);
@@ -180,7 +258,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if (kPair) cluster_sync();  // the peer's barriers exist before any remote arrive reaches them
+    if (kCluster) cluster_sync();  // the peers' barriers exist before any remote arrive / st.async reaches them
     tc_fence_after();
     const uint32_t tmem = tmem_s;
     if (tid == 0) K2_MARK(1);
@@ -226,6 +304,20 @@ __global__ void __launch_bounds__(kGThreads, 1)
                     }
                 }
             }
+            if (kLN && warp == kGAWarp) {
+                // One tile per CTA: stages nk and nk + 1 are free once the MMAs of
+                // K stages nk - kStages and nk + 1 - kStages completed.
+                // Chunks 0-5 go to the first stage, 6-7 to the second; the epilogue's
+                // first pass (chunks 0-3) waits on res_bar[0] only.
+                const int m0 = tile_m0(t_first), n0 = (t_first % n_tiles) * kBN;
+                if (g >= kStages) mbar_wait(&empty_bar[g % kStages], ((g / kStages) & 1) ^ 1);
+                mbar_arrive_expect_tx(&res_bar[0], 4 * 8192);
+                for (int c = 0; c < 4; ++c) tma_tile2d_g2s(ln_box(c), &tmap_r, n0 + c * 32, m0, &res_bar[0]);
+                mbar_arrive_expect_tx(&res_bar[1], 4 * 8192);
+                for (int c = 4; c < 6; ++c) tma_tile2d_g2s(ln_box(c), &tmap_r, n0 + c * 32, m0, &res_bar[1]);
+                if (g + 1 >= kStages) mbar_wait(&empty_bar[(g + 1) % kStages], (((g + 1) / kStages) & 1) ^ 1);
+                for (int c = 6; c < 8; ++c) tma_tile2d_g2s(ln_box(c), &tmap_r, n0 + c * 32, m0, &res_bar[1]);
+            }
         }
     } else if (warp == kGMmaWarp) {
         if (kPair && rank == 1) {
@@ -264,6 +356,134 @@ __global__ void __launch_bounds__(kGThreads, 1)
                 if (i < 4) K2_MARK(4 + 4 * i);
             }
         }
+    } else if constexpr (kLN) {
+        // Fused residual + LayerNorm epilogue (one 128 x 256 tile per CTA, the
+        // cluster's three CTAs hold the row's three column tiles). Thread = row
+        // r (TMEM lane), group gp = column chunks gp and gp + 4 (32 each).
+        // t1 = bf16(acc + bias + resid) stays in registers as bf16 pairs; the
+        // row's (mean, M2) is reduced over chunks (registers), groups (shared
+        // memory) and CTAs (st.async into every CTA of the cluster), then the
+        // normalised row overwrites the thread's own residual bytes in the ring
+        // and goes out by TMA stores. Bias / gamma / beta and the statistics
+        // scratch live in the (otherwise unused) staging-box region.
+        const int q = warp & 3, gp = warp >> 2, r = q * 32 + lane, ht = tid & 127;
+        const uint32_t gbar = 4u + static_cast<uint32_t>(gp);
+        auto group_sync = [&] { asm volatile("bar.sync %0, 128;\n" ::"r"(gbar) : "memory"); };
+        auto epi_sync = [&] { asm volatile("bar.sync 3, %0;\n" ::"r"(kGEpiWarps * 32) : "memory"); };
+        float* gam_s = reinterpret_cast<float*>(smem + kGSmem);
+        float* bet_s = gam_s + kBN;
+        float2* part = reinterpret_cast<float2*>(smem + kGSmem + 4096);   // [4 groups][128 rows]
+        float2* xbuf = reinterpret_cast<float2*>(smem + kGSmem + 8192);   // [3 CTAs][128 rows]
+        const int t = t_first;
+        const int m0 = tile_m0(t), n0 = (t % n_tiles) * kBN;
+        for (int c = tid; c < kBN; c += kGEpiWarps * 32) {
+            bias_s[c] = *reinterpret_cast<const float*>(translate(a.arena, pt, a.b_off + 4ull * (n0 + c)));
+            gam_s[c] = *reinterpret_cast<const float*>(translate(a.arena, pt, a.g_off + 4ull * (n0 + c)));
+            bet_s[c] = *reinterpret_cast<const float*>(translate(a.arena, pt, a.be_off + 4ull * (n0 + c)));
+        }
+        epi_sync();
+        mbar_wait(&tfull_bar[0], 0);
+        tc_fence_after();
+        if (tid == 0) K2_MARK(5);
+        pdl_trigger();
+        uint32_t hold[2][16];
+        float cnt = 32.f, mean = 0.f, m2 = 0.f;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int c = gp + 4 * j;
+            float v[32];
+            tmem_ld_32x32b_x32(tmem + static_cast<uint32_t>(c * 32) + (static_cast<uint32_t>(q * 32) << 16), v);
+            mbar_wait(&res_bar[j], 0);
+            const uint8_t* box = ln_box(c);
+            float s = 0.f;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint4 w = *reinterpret_cast<const uint4*>(box + r * 64 + ((u ^ ((r >> 1) & 3)) << 4));
+                const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&w);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int e = u * 8 + 2 * k;
+                    const float2 f2 = __bfloat1622float2(h2[k]);
+                    const __nv_bfloat162 x2 = __floats2bfloat162_rn(v[e] + bias_s[c * 32 + e] + f2.x,
+                                                                    v[e + 1] + bias_s[c * 32 + e + 1] + f2.y);
+                    hold[j][u * 4 + k] = *reinterpret_cast<const uint32_t*>(&x2);
+                    const float2 xf = __bfloat1622float2(x2);
+                    v[e] = xf.x;
+                    v[e + 1] = xf.y;
+                    s += xf.x + xf.y;
+                }
+            }
+            const float mc = s * (1.f / 32.f);
+            float mc2 = 0.f;
+#pragma unroll
+            for (int e = 0; e < 32; ++e) mc2 = fmaf(v[e] - mc, v[e] - mc, mc2);
+            if (j == 0) {
+                mean = mc;
+                m2 = mc2;
+            } else {
+                chan_combine(cnt, mean, m2, 32.f, mc, mc2);
+            }
+        }
+        part[gp * 128 + r] = make_float2(mean, m2);
+        if (tid == 0) K2_MARK(7);
+        epi_sync();
+        if (gp == 0) {
+#pragma unroll
+            for (int g = 1; g < 4; ++g) {
+                const float2 p = part[g * 128 + r];
+                chan_combine(cnt, mean, m2, 64.f, p.x, p.y);
+            }
+            const uint32_t my = static_cast<uint32_t>(t % n_tiles);
+#pragma unroll
+            for (uint32_t dst = 0; dst < 3; ++dst)
+                st_async_v2f32(mapa_u32(&xbuf[my * 128 + r], dst), mean, m2, mapa_u32(&stat_bar, dst));
+        }
+        if (tid == 0) K2_MARK(8);
+        mbar_wait(&stat_bar, 0);
+        cluster_arrive();  // every statistic this CTA expects has landed: peers may exit once all arrived
+        if (tid == 0) K2_MARK(9);
+        {
+            float2 p = xbuf[r];
+            float n_r = 256.f;
+            mean = p.x;
+            m2 = p.y;
+#pragma unroll
+            for (int k = 1; k < 3; ++k) {
+                p = xbuf[k * 128 + r];
+                chan_combine(n_r, mean, m2, 256.f, p.x, p.y);
+            }
+        }
+        const float rstd = rsqrtf(m2 * (1.f / 768.f) + 1e-12f);
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+            const int c = gp + 4 * j;
+            uint8_t* box = ln_box(c);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                uint4 o;
+                uint32_t* o32 = reinterpret_cast<uint32_t*>(&o);
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int e = c * 32 + u * 8 + 2 * k;
+                    const uint32_t pr = hold[j][u * 4 + k];
+                    const float2 xf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pr));
+                    const __nv_bfloat162 y2 = __floats2bfloat162_rn((xf.x - mean) * rstd * gam_s[e] + bet_s[e],
+                                                                    (xf.y - mean) * rstd * gam_s[e + 1] + bet_s[e + 1]);
+                    o32[k] = *reinterpret_cast<const uint32_t*>(&y2);
+                }
+                *reinterpret_cast<uint4*>(box + r * 64 + ((u ^ ((r >> 1) & 3)) << 4)) = o;  // this thread's own residual bytes
+            }
+        }
+        fence_proxy_async_smem();
+        group_sync();
+        if (ht == 0) {
+            tma_tile2d_s2g(&tmap_y, n0 + gp * 32, m0, ln_box(gp));
+            tma_tile2d_s2g(&tmap_y, n0 + (gp + 4) * 32, m0, ln_box(gp + 4));
+            bulk_commit_group();
+        }
+        if (tid == 0) K2_MARK(10);
+        if (ht == 0) bulk_wait_group_read<0>();
+        if (tid == 0) K2_MARK(6);
     } else {
         // Epilogue (16 warps): TMEM lane = token row, column = output feature.
         // Four warps per TMEM lane quarter; group gp takes the 32-column chunks
@@ -350,13 +570,19 @@ __global__ void __launch_bounds__(kGThreads, 1)
             }
             if (ct == 0 && i < 4) K2_MARK(6 + 4 * i);
         }
-        if (ht == 0) bulk_wait_group<0>();  // every output box written before the CTA exits
+        // The boxes must stay valid until the stores have read them; the grid's
+        // completion (the next kernel's griddepcontrol.wait) covers the writes.
+        if (ht == 0) bulk_wait_group_read<0>();
     }
     tc_fence_before();
     __syncthreads();
-    if (kPair) cluster_sync();  // no MMA / remote arrive may target an exited CTA
+    if (kCluster) {  // no MMA / remote arrive / st.async may target an exited CTA
+        if (!(kLN && warp < kGEpiWarps)) cluster_arrive();  // (kLN epilogue threads arrived after their statistics)
+        cluster_wait();
+    }
     tc_fence_after();
     if (tid == 0) K2_MARK(19);
+    K2_SPAN_END(a.span);
     if (warp == kGMmaWarp) {
         if (kPair)
             tmem_dealloc_pair<kTmemCols>(tmem);
@@ -386,7 +612,9 @@ __device__ __forceinline__ float ex2_approx(float x) {
 }
 
 __global__ void __launch_bounds__(128, 4) attention_tc_kernel(const __grid_constant__ CUtensorMap tmap_qkv,
-                                                           __nv_bfloat16* __restrict__ ctx, int heads) {
+                                                           __nv_bfloat16* __restrict__ ctx, int heads,
+                                                           unsigned long long* span) {
+    K2_SPAN_BEGIN(span);
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* qs = sm;
@@ -504,6 +732,7 @@ __global__ void __launch_bounds__(128, 4) attention_tc_kernel(const __grid_const
     __syncthreads();
     tc_fence_after();
     if (warp == 0) tmem_dealloc<128>(tmem);
+    K2_SPAN_END(span);
 }
 
 // ------------------------------------------------------------------ K4 LayerNorm
@@ -511,7 +740,9 @@ __global__ void __launch_bounds__(128, 4) attention_tc_kernel(const __grid_const
 template <int kD>
 __global__ void __launch_bounds__(256) layernorm_kernel(const __nv_bfloat16* __restrict__ x, __nv_bfloat16* __restrict__ y,
                                                         const char* arena, const __grid_constant__ PageTable ptab,
-                                                        uint64_t g_off, uint64_t b_off, int rows) {
+                                                        uint64_t g_off, uint64_t b_off, int rows,
+                                                        unsigned long long* span) {
+    K2_SPAN_BEGIN(span);
     // One warp per row, kRowsPerWarp rows per warp with every load of a row
     // issued before any math (HBM latency, not arithmetic, bounds this
     // kernel). gamma / beta come straight into registers from the arena (lane
@@ -588,6 +819,7 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const __nv_bfloat16* __r
             *reinterpret_cast<uint4*>(yr + (i * 32 + lane) * 8) = u;
         }
     }
+    K2_SPAN_END(span);
 }
 
 // ------------------------------------------------------------------ pooler
@@ -599,7 +831,9 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const __nv_bfloat16* __r
 // tile layout, one page translation per chunk).
 __global__ void __launch_bounds__(256) pooler_kernel(const __nv_bfloat16* __restrict__ x, float* __restrict__ out,
                                                      const char* arena, const __grid_constant__ PageTable ptab,
-                                                     uint64_t w_off, uint64_t b_off, int d, int seq, int batch) {
+                                                     uint64_t w_off, uint64_t b_off, int d, int seq, int batch,
+                                                     unsigned long long* span) {
+    K2_SPAN_BEGIN(span);
     constexpr int kD = 768, kChunks = kD / 8 / 32;  // 16-byte chunks per lane
     extern __shared__ __align__(16) uint8_t cls_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -624,6 +858,7 @@ __global__ void __launch_bounds__(256) pooler_kernel(const __nv_bfloat16* __rest
             *reinterpret_cast<const uint4*>(x + static_cast<size_t>(b) * seq * kD + c * 8);
     }
     __syncthreads();
+    K2_SPAN_END(span);  // (pooler: start of the per-row loop)
     if (n >= d) return;
     for (int b = 0; b < batch; ++b) {
         float acc = 0.f;
@@ -673,7 +908,9 @@ void launch_pdl(Kern k, dim3 grid, dim3 block, size_t smem, cudaStream_t s, bool
 
 template <int kEpi, int kBN, bool kPair>
 void gemm_bn(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_off, const __nv_bfloat16* x,
-             __nv_bfloat16* y, const __nv_bfloat16* resid, int T, int K, int N, cudaStream_t s, bool pdl) {
+             __nv_bfloat16* y, const __nv_bfloat16* resid, int T, int K, int N, cudaStream_t s, bool pdl,
+             uint64_t g_off = 0, uint64_t be_off = 0) {
+    constexpr bool kLN = kEpi == kEpiResidLN;
     CUtensorMap tm;
     if (!encode_tensor_map_2d(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, x, static_cast<uint64_t>(K),
                               static_cast<uint64_t>(T), static_cast<uint64_t>(K) * 2, kGK, kGM,
@@ -701,7 +938,8 @@ void gemm_bn(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_
                                   CU_TENSOR_MAP_SWIZZLE_NONE))
             throw CudaError("cuTensorMapEncodeTiled failed (bert gemm arena weights)");
     }
-    GemmArgs a{nullptr, arena, w_off, b_off, y, resid, T, K, N, pt};
+    unsigned long long* span = next_span(kLN ? "gemm+LN" : kEpi == kEpiGelu ? "gemm GELU" : kEpi == kEpiResid ? "gemm resid" : "gemm bias");
+    GemmArgs a{nullptr, span, arena, w_off, b_off, g_off, be_off, y, resid, T, K, N, pt};
 #ifdef GFX_K2_DEBUG
     static unsigned long long* dbg = nullptr;
     static int calls = 0;
@@ -718,7 +956,8 @@ void gemm_bn(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_
     const int tiles = (T / kGM) * (N / kBN);
     int grid = tiles < sms ? tiles : sms;
     if (kPair) grid &= ~1;
-    if (kPair) {
+    if (kLN) grid = tiles;  // one 128 x 256 tile per CTA, clusters of N / 256 = 3 (host-checked: ln_fusable)
+    if (kPair || kLN) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(grid);
         cfg.blockDim = dim3(kGThreads);
@@ -728,7 +967,7 @@ void gemm_bn(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
         attr[1].id = cudaLaunchAttributeClusterDimension;
-        attr[1].val.clusterDim.x = 2;
+        attr[1].val.clusterDim.x = kPair ? 2 : 3;
         attr[1].val.clusterDim.y = 1;
         attr[1].val.clusterDim.z = 1;
         cfg.attrs = attr;
@@ -782,6 +1021,57 @@ void gemm(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_off
         gemm_bn<kEpi, 256, false>(arena, pt, w_off, b_off, x, y, resid, T, K, N, s, pdl);
     else
         gemm_bn<kEpi, 128, false>(arena, pt, w_off, b_off, x, y, resid, T, K, N, s, pdl);
+}
+
+// Residual GEMM (N = d = 768) with the post-LN LayerNorm fused into its
+// epilogue when every 128-row block gets its own resident 3-CTA cluster
+// (T <= 128 x max active clusters; 4096 tokens = 32 clusters); otherwise the
+// residual GEMM and layernorm_kernel (via `t`).
+int ln_max_clusters() {
+    static std::mutex mu;
+    static std::map<int, int> cache;
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(dev);
+    if (it != cache.end()) return it->second;
+    auto k = gemm_bf16_kernel<kEpiResidLN, 256, false>;
+    const size_t smem = kGSmem + 4 * 8192 + 1024;
+    ensure_max_dynamic_smem(reinterpret_cast<const void*>(k), static_cast<int>(smem));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(3 * 64);
+    cfg.blockDim = dim3(kGThreads);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 3;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    GFX_CUDA(cudaOccupancyMaxActiveClusters(&n, k, &cfg));
+    cache[dev] = n;
+    return n;
+}
+
+bool ln_fusable(int T, int N) {
+#ifdef GFX_K2_DEBUG
+    if (std::getenv("GFX_K2_NOLN")) return false;  // debug A/B only
+#endif
+    return N == 768 && T % kGM == 0 && T / kGM <= ln_max_clusters();
+}
+
+void gemm_resid_ln(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_off, uint64_t g_off,
+                   uint64_t be_off, const __nv_bfloat16* x, __nv_bfloat16* y, const __nv_bfloat16* resid,
+                   __nv_bfloat16* t, int T, int K, int N, cudaStream_t s, bool pdl, bool pair) {
+    if (ln_fusable(T, N)) {
+        if (K % kGK) throw std::runtime_error("bert gemm: K multiple of 64");
+        gemm_bn<kEpiResidLN, 256, false>(arena, pt, w_off, b_off, x, y, resid, T, K, N, s, pdl, g_off, be_off);
+        return;
+    }
+    gemm<kEpiResid>(arena, pt, w_off, b_off, x, t, resid, T, K, N, s, pdl, pair);
+    launch_pdl(layernorm_kernel<768>, dim3((T + 15) / 16), dim3(256), 0, s, true, static_cast<const __nv_bfloat16*>(t),
+               y, arena, pt, g_off, be_off, T, next_span("layernorm"));
 }
 
 }  // namespace
@@ -860,6 +1150,18 @@ int bert_forward(const char* arena, const PageTable& pt, const BertLayout& lay, 
         throw std::runtime_error("bert: this build serves seq 128, d_head 64, d 768");
     ws.ensure(T, d, lay.ffn);
     int launches = 0;
+#ifdef GFX_K2_DEBUG
+    static int forwards = 0;
+    if (++forwards == 10 && !hidden) {
+        if (!g_span.buf) GFX_CUDA(cudaMalloc(&g_span.buf, 16 * SpanTrace::kMax));
+        std::vector<unsigned long long> init(2 * SpanTrace::kMax);
+        for (int i = 0; i < SpanTrace::kMax; ++i) init[2 * i] = ~0ull, init[2 * i + 1] = 0;
+        GFX_CUDA(cudaMemcpyAsync(g_span.buf, init.data(), init.size() * 8, cudaMemcpyHostToDevice, s));
+        GFX_CUDA(cudaStreamSynchronize(s));
+        g_span.names.clear();
+        g_span.on = true;
+    }
+#endif
     const __nv_bfloat16* x = in;
     const size_t hbytes = static_cast<size_t>(T) * d * 2;
     if (hidden) GFX_CUDA(cudaMemcpyAsync(hidden, in, hbytes, cudaMemcpyDeviceToDevice, s));
@@ -873,16 +1175,14 @@ int bert_forward(const char* arena, const PageTable& pt, const BertLayout& lay, 
                                       CU_TENSOR_MAP_SWIZZLE_128B))
                 throw CudaError("cuTensorMapEncodeTiled failed (attention)");
             ensure_max_dynamic_smem(reinterpret_cast<const void*>(attention_tc_kernel), static_cast<int>(kAttnSmem));
-            launch_pdl(attention_tc_kernel, dim3(batch * lay.heads), dim3(128), kAttnSmem, s, true, tq, ws.ctx, lay.heads);
+            launch_pdl(attention_tc_kernel, dim3(batch * lay.heads), dim3(128), kAttnSmem, s, true, tq, ws.ctx, lay.heads,
+                       next_span("attention"));
         }
-        gemm<kEpiResid>(arena, pt, o.wo, o.bo, ws.ctx, ws.t, x, T, d, d, s, true, ws.gemm_pair);
-        launch_pdl(layernorm_kernel<768>, dim3((T + 15) / 16), dim3(256), 0, s, true,
-                   static_cast<const __nv_bfloat16*>(ws.t), ws.h, arena, pt, o.ln1_g, o.ln1_b, T);
+        gemm_resid_ln(arena, pt, o.wo, o.bo, o.ln1_g, o.ln1_b, ws.ctx, ws.h, x, ws.t, T, d, d, s, true, ws.gemm_pair);
         gemm<kEpiGelu>(arena, pt, o.w1, o.b1, ws.h, ws.f, nullptr, T, d, lay.ffn, s, true, ws.gemm_pair);
-        gemm<kEpiResid>(arena, pt, o.w2, o.b2, ws.f, ws.t, ws.h, T, lay.ffn, d, s, true, ws.gemm_pair);
-        launch_pdl(layernorm_kernel<768>, dim3((T + 15) / 16), dim3(256), 0, s, true,
-                   static_cast<const __nv_bfloat16*>(ws.t), ws.x, arena, pt, o.ln2_g, o.ln2_b, T);
-        launches += 7;
+        gemm_resid_ln(arena, pt, o.w2, o.b2, o.ln2_g, o.ln2_b, ws.f, ws.x, ws.h, ws.t, T, lay.ffn, d, s, true,
+                      ws.gemm_pair);
+        launches += ln_fusable(T, d) ? 5 : 7;
         x = ws.x;
         if (hidden)
             GFX_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(hidden) + (l + 1) * hbytes, ws.x, hbytes,
@@ -893,7 +1193,27 @@ int bert_forward(const char* arena, const PageTable& pt, const BertLayout& lay, 
     ensure_max_dynamic_smem(reinterpret_cast<const void*>(pooler_kernel), 160 * 1024);
     launch_pdl(pooler_kernel, dim3((d + 7) / 8), dim3(256), static_cast<size_t>(batch) * d * 2, s, !hidden,
                static_cast<const __nv_bfloat16*>(x), out,
-               arena, pt, lay.wp, lay.bp, d, lay.seq, batch);
+               arena, pt, lay.wp, lay.bp, d, lay.seq, batch, next_span("pooler"));
+#ifdef GFX_K2_DEBUG
+    if (g_span.on) {
+        std::vector<unsigned long long> v(2 * g_span.names.size());
+        GFX_CUDA(cudaStreamSynchronize(s));
+        GFX_CUDA(cudaMemcpy(v.data(), g_span.buf, v.size() * 8, cudaMemcpyDeviceToHost));
+        const unsigned long long t0 = v[0];
+        double busy = 0;
+        std::fprintf(stderr, "[K2 span] T %d: kernel, start, end, duration, gap after previous end (us)\n", T);
+        for (size_t i = 0; i < g_span.names.size(); ++i) {
+            const double st = (v[2 * i] - t0) * 1e-3, en = (v[2 * i + 1] - t0) * 1e-3;
+            const double gap = i ? st - (v[2 * i - 1] - t0) * 1e-3 : 0.0;
+            busy += en - st;
+            if (i < 16 || i + 2 >= g_span.names.size())
+                std::fprintf(stderr, "  %3zu %-12s %9.2f %9.2f %7.2f %7.2f\n", i, g_span.names[i], st, en, en - st, gap);
+        }
+        std::fprintf(stderr, "  forward %.2f us, sum of kernel spans %.2f us\n",
+                     (v[2 * g_span.names.size() - 1] - t0) * 1e-3, busy);
+        g_span.on = false;
+    }
+#endif
     return launches + 1;
 }
 
@@ -908,7 +1228,19 @@ void bert_gemm_op(const char* arena, const PageTable& pt, const BertLayout& lay,
         case 1: gemm<kEpiResid>(arena, pt, o.wo, o.bo, x, y, resid, T, d, d, s, false, pair); break;
         case 2: gemm<kEpiGelu>(arena, pt, o.w1, o.b1, x, y, nullptr, T, d, lay.ffn, s, false, pair); break;
         case 3: gemm<kEpiResid>(arena, pt, o.w2, o.b2, x, y, resid, T, lay.ffn, d, s, false, pair); break;
-        default: throw std::invalid_argument("bert gemm: op must be 0..3");
+        case 4:
+        case 5: {
+            // The forward's residual + LayerNorm step (fused when ln_fusable, else GEMM + K4 through a scratch).
+            __nv_bfloat16* t = nullptr;
+            if (!ln_fusable(T, d)) GFX_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&t), static_cast<size_t>(T) * d * 2, s));
+            if (op == 4)
+                gemm_resid_ln(arena, pt, o.wo, o.bo, o.ln1_g, o.ln1_b, x, y, resid, t, T, d, d, s, false, pair);
+            else
+                gemm_resid_ln(arena, pt, o.w2, o.b2, o.ln2_g, o.ln2_b, x, y, resid, t, T, lay.ffn, d, s, false, pair);
+            if (t) GFX_CUDA(cudaFreeAsync(t, s));
+            break;
+        }
+        default: throw std::invalid_argument("bert gemm: op must be 0..5");
     }
 }
 

@@ -68,7 +68,8 @@ int bert_forward(const char* arena, const PageTable& pt, const BertLayout& lay, 
                  __nv_bfloat16* hidden = nullptr);  // debug: [L+1][T][d] hidden states
 
 // Test hook: one K2 GEMM of layer l with its fused epilogue. op 0: QKV (+bias),
-// 1: attention output (+bias +resid), 2: FFN1 (+bias, GELU), 3: FFN2 (+bias +resid).
+// 1: attention output (+bias +resid), 2: FFN1 (+bias, GELU), 3: FFN2 (+bias +resid);
+// 4 / 5: ops 1 / 3 followed by LayerNorm 1 / 2 (the forward's fused residual + LN step).
 void bert_gemm_op(const char* arena, const PageTable& pt, const BertLayout& lay, int l, int op,
                   const __nv_bfloat16* x, const __nv_bfloat16* resid, __nv_bfloat16* y, int T, bool pair,
                   cudaStream_t s);

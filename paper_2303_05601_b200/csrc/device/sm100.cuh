@@ -142,6 +142,12 @@ __device__ __forceinline__ void st_async_f32(uint32_t remote_addr, float v, uint
                  "r"(__float_as_uint(v)), "r"(remote_mbar)
                  : "memory");
 }
+// 8-byte (two f32) variant of st_async_f32.
+__device__ __forceinline__ void st_async_v2f32(uint32_t remote_addr, float x, float y, uint32_t remote_mbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f32 [%0], {%1, %2}, [%3];\n" ::"r"(remote_addr),
+                 "f"(x), "f"(y), "r"(remote_mbar)
+                 : "memory");
+}
 __device__ __forceinline__ int ld_acquire_cluster_s32(uint32_t remote_addr) {
     int v;
     asm volatile("ld.acquire.cluster.shared::cluster.b32 %0, [%1];\n" : "=r"(v) : "r"(remote_addr) : "memory");
@@ -150,6 +156,9 @@ __device__ __forceinline__ int ld_acquire_cluster_s32(uint32_t remote_addr) {
 __device__ __forceinline__ void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
+// Split cluster barrier (per thread, not .aligned): arrive once per phase, wait later.
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release;\n" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire;\n" ::: "memory"); }
 __device__ __forceinline__ uint32_t cluster_ctarank() {
     uint32_t r;
     asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));

@@ -182,11 +182,16 @@ def bf16_bits(x):
 
 
 @pytest.mark.parametrize("pair", [False, True])
-@pytest.mark.parametrize("op,tokens", [(0, 4096), (1, 4096), (1, 8192), (2, 4096), (3, 4096), (3, 8192)])
+@pytest.mark.parametrize("op,tokens", [(0, 4096), (1, 4096), (1, 8192), (2, 4096), (3, 4096), (3, 8192),
+                                       (4, 256), (4, 4096), (4, 8192), (5, 4096), (5, 8192)])
 def test_bert_gemm_epilogue_parity(gfx, olib, op, tokens, pair):
     """One K2 GEMM with its fused epilogue at T = 4096 / 8192 (the persistent
     CTAs run 1-6 tiles each, cycling both TMEM accumulators) against numpy:
-    y = bf16(x . W^T + b [GELU] [+ resid]) with W, b from the parameter stream."""
+    y = bf16(x . W^T + b [GELU] [+ resid]) with W, b from the parameter stream.
+    Ops 4 / 5 add the post-LN LayerNorm (fp64 statistics of the bf16-rounded
+    residual sum, as the oracle's layernorm_rows): fused into the GEMM's
+    epilogue through the 3-CTA cluster at 256 / 4096 tokens, the residual GEMM
+    + layernorm_kernel fallback at 8192 (more row blocks than resident clusters)."""
     from scipy.special import erf
     layer, seqs = 3, tokens // SEQ
     idx = 73
@@ -195,8 +200,8 @@ def test_bert_gemm_epilogue_parity(gfx, olib, op, tokens, pair):
     gfx.check(gfx._ffi.gfx_model_register(idx, C.byref(desc)))
     pages = C.c_int32()
     gfx.check(gfx._ffi.gfx_model_pages(idx, C.byref(pages)))
-    K, N = {0: (D, 3 * D), 1: (D, D), 2: (D, 3072), 3: (3072, D)}[op]
-    wt, bt = {0: (0, 1), 1: (2, 3), 2: (6, 7), 3: (8, 9)}[op]
+    K, N = {0: (D, 3 * D), 1: (D, D), 2: (D, 3072), 3: (3072, D), 4: (D, D), 5: (3072, D)}[op]
+    wt, bt = {0: (0, 1), 1: (2, 3), 2: (6, 7), 3: (8, 9), 4: (2, 3), 5: (8, 9)}[op]
     rng = np.random.default_rng(100 + op)
     x = bf16_round(rng.standard_normal((tokens, K)).astype(np.float32))
     r = bf16_round(rng.standard_normal((tokens, N)).astype(np.float32))
@@ -208,9 +213,20 @@ def test_bert_gemm_epilogue_parity(gfx, olib, op, tokens, pair):
     v = x.astype(np.float64) @ w.T.astype(np.float64) + b
     if op == 2:
         v = 0.5 * v * (1.0 + erf(v / np.sqrt(2.0)))
-    if op in (1, 3):
+    if op in (1, 3, 4, 5):
         v = v + r
     want = bf16_round(v.astype(np.float32))
+    if op in (4, 5):
+        gt, bet = (4, 5) if op == 4 else (10, 11)
+        g = np.zeros(N, np.float32)
+        be = np.zeros(N, np.float32)
+        olib.orc_fill_params(seed, 16 * layer + gt, N, np.float32(0.1), g.ctypes.data)
+        olib.orc_fill_params(seed, 16 * layer + bet, N, np.float32(0.1), be.ctypes.data)
+        g = g + np.float32(1.0)
+        t1 = want.astype(np.float64)
+        mean = t1.mean(axis=1, keepdims=True)
+        var = ((t1 - mean) ** 2).mean(axis=1, keepdims=True)
+        want = bf16_round(((t1 - mean) / np.sqrt(var + 1e-12) * g + be).astype(np.float32))
     a = C.c_void_p()
     gfx.check(gfx._ffi.gfx_arena_create(0, (pages.value + 2) << 21, C.byref(a)))
     try:

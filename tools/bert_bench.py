@@ -34,7 +34,7 @@ for _ in range(iters):
     F.check(F.gfx_infer(a, 0, x, y, batch, None))
 F.check(F.gfx_synchronize(a))
 dt = (time.perf_counter() - t0) / iters
-L, D, FF, S = s.dims[0], 768, s.dims[2], 128
+L, D, FF, S = s.dims[0], s.dims[1], s.dims[3], s.dims[4]
 T = batch * S
 flops = L * (2.0 * T * (4 * D * D + 2 * D * FF) + 4.0 * T * S * D) + 2.0 * batch * D * D
 print(f"bert {s.model_id} (pair={pair}): {dt * 1e3:.3f} ms/forward  {flops / dt / 1e12:.1f} TFLOP/s")
