@@ -228,6 +228,8 @@ struct Daemon {
         out_bytes = b0.out_bytes;
         family = b0.desc.family;
         if (out_bytes > kMailboxBytes) throw std::invalid_argument("request output larger than the mailbox");
+        for (int g = 0; g < G; ++g)  // another daemon serves a GPU on this device
+            if (g != gpu && shm->gpu[g].device == b.device) gfx::mark_device_shared(b.device);
         mgr = std::make_unique<GpuManager>(b.device, shm->arena_bytes, gpu);
         GFX_CUDA(cudaMalloc(&flags, flag_words(G, M) * 4));
         GFX_CUDA(cudaMemset(flags, 0, flag_words(G, M) * 4));

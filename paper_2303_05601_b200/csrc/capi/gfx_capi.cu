@@ -262,6 +262,7 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
         uint64_t arena_pages;
         int32_t gpu;
         int32_t models;
+        char uuid[16];  // the exporting process's device (ranks sharing one B200 -> cooperative K1)
     };
 
     void ipc_export(void* out, uint64_t bytes) {
@@ -275,6 +276,9 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
         b.arena_pages = m.total_pages();
         b.gpu = args.only_gpu;
         b.models = static_cast<int32_t>(M);
+        cudaDeviceProp prop{};
+        GFX_CUDA(cudaGetDeviceProperties(&prop, dev_of[static_cast<size_t>(args.only_gpu)]));
+        std::memcpy(b.uuid, &prop.uuid, sizeof b.uuid);
         std::memcpy(out, &b, sizeof b);
     }
 
@@ -284,6 +288,10 @@ struct gfx_replay_s : gpufaas::ExecutionListener {
         GFX_CUDA(cudaSetDevice(dev_of[static_cast<size_t>(args.only_gpu)]));
         remotes.assign(static_cast<size_t>(n), RemoteArena{});
         const IpcBlob* b = static_cast<const IpcBlob*>(blobs);
+        const int my = args.only_gpu;
+        for (int g = 0; g < n; ++g)
+            if (g != my && std::memcmp(b[g].uuid, b[my].uuid, sizeof b[g].uuid) == 0)
+                gfx::mark_device_shared(dev_of[static_cast<size_t>(my)]);
         for (int g = 0; g < n; ++g) {
             if (b[g].gpu != g || static_cast<size_t>(b[g].models) != M)
                 throw std::invalid_argument("ipc blob " + std::to_string(g) + " is not GPU " + std::to_string(g) +

@@ -4,6 +4,8 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <map>
+#include <mutex>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -252,7 +254,27 @@ cudaEvent_t KernelTimer::next() {
 
 // ------------------------------------------------------------- manager
 
+// Managers per device in this process. K1 chains its launches by PDL only on a
+// device one manager owns: two managers' persistent forwards on one device
+// (the emulated fleets, or another process's manager: mark_device_shared)
+// could each hold part of the SMs while waiting for their own missing CTAs,
+// so a shared device keeps the cooperative launch.
+namespace {
+std::mutex g_dev_mu;
+std::map<int, int> g_dev_managers;
+std::map<int, bool> g_dev_shared;  // other processes run managers on the device
+}  // namespace
+
+void mark_device_shared(int dev) {
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    g_dev_shared[dev] = true;
+}
+
 GpuManager::GpuManager(int device, uint64_t capacity_bytes, int manager_id) : device_(device), id_(manager_id) {
+    {
+        std::lock_guard<std::mutex> lk(g_dev_mu);
+        ++g_dev_managers[device];
+    }
     if (capacity_bytes == 0 || capacity_bytes % kPageBytes != 0)
         throw std::invalid_argument("arena capacity must be a positive multiple of 2 MiB");
     activate();
@@ -268,6 +290,10 @@ GpuManager::GpuManager(int device, uint64_t capacity_bytes, int manager_id) : de
 }
 
 GpuManager::~GpuManager() {
+    {
+        std::lock_guard<std::mutex> lk(g_dev_mu);
+        --g_dev_managers[device_];
+    }
     cudaSetDevice(device_);
     cudaStreamSynchronize(compute_);
     cudaStreamSynchronize(copy_);
@@ -494,6 +520,10 @@ void GpuManager::infer(int model, const void* in_v, void* out_v, void* debug_hid
     f.logits = static_cast<float*>(out_v);
     f.probs = f.logits + static_cast<size_t>(kBatch) * blob.desc.dims[f.L];
     f.grid = sm_count_;
+    {
+        std::lock_guard<std::mutex> lk(g_dev_mu);
+        f.pdl = g_dev_managers[device_] == 1 && !g_dev_shared[device_] ? 1 : 0;
+    }
     uint32_t act = 0;
     for (int l = 0; l < f.L; ++l) {
         MlpFwdLayer& ly = f.layer[l];

@@ -67,6 +67,11 @@ struct KernelTimer {  // optional per-launch CUDA-event timing
     cudaEvent_t next();
 };
 
+// Declares that another process also runs GPU managers on device `dev` (two
+// daemons / replay ranks on one GPU in tests and emulation): K1 then keeps the
+// cooperative launch instead of the PDL chain (see GpuManager::infer).
+void mark_device_shared(int dev);
+
 class GpuManager {
 public:
     GpuManager(int device, uint64_t capacity_bytes, int manager_id);

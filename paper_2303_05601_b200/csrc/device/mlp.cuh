@@ -44,6 +44,7 @@ struct MlpFwdArgs {
     unsigned long long* dbg;  // GFX_K1_DEBUG builds: [grid][32] phase marks (%globaltimer), else unused
     int L;
     int grid;
+    int pdl;                  // 1: chained to the previous launch by PDL (device owned by one manager), 0: cooperative
     MlpFwdLayer layer[GFX_MAX_LAYERS];
     PageTable pt;
 };

@@ -260,6 +260,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 0) K1_MARK(0);
 #endif
 
+    // PDL chain (a.pdl): the next forward may place its CTAs on SMs this one
+    // frees (the softmax CTAs finish last), so its weight stream and layer 0 —
+    // which share nothing with this launch — overlap this launch's tail. Only
+    // what touches the layer-output buffers waits for this grid's predecessor
+    // (griddepcontrol.wait: the drain before clearing / reducing, the X
+    // producer before polling layer outputs). No-ops without the attribute.
+    asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory");
     const int tid = threadIdx.x;
     const int warp = tid >> 5;
     const int lane = tid & 31;
@@ -339,6 +346,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     complete_words(v, pp, static_cast<unsigned>(a.layer[l - 1].nkt), 10, g_);
                     seen = src;
                 };
+                if (l == 1) asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the buffers' clear by the predecessor
                 for (int s = r.s0; s < r.s1;) {
                     const int slot = g % kSlots, kt = s % ly.nkt;
                     const bool pair = l > 0 && (g & 1) == 0 && s + 1 < r.s1;
@@ -450,6 +458,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 tc_fence_after();
                 tmem_st_32x32b_x32(tmem + (static_cast<uint32_t>(q * 32) << 16) + kLoBase + static_cast<uint32_t>(kTileK * slot), wlo);
+                if (q == 0 && lane == 0) K1_STEP(g, 6);
                 // X: warp q converts K columns 8q .. 8q+7 (16-byte chunks 2q, 2q+1) of all 32 rows; lane = batch row.
                 K1_WAIT(&raw_full[second && l > 0 ? slot - 1 : slot], (g / kSlots) & 1, 7, g);
                 if (q == 0 && lane == 0) K1_STEP(g, 3);
@@ -486,6 +495,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     xv[0] = make_float4(x[0], x[1], x[2], x[3]);
                     xv[1] = make_float4(x[4], x[5], x[6], x[7]);
                     conv_sync(group);  // every warp of the group has read its raw rows before the operand overwrites them
+                    if (q == 0 && lane == 0) K1_STEP(g, 7);
                     if (l == 1 && lane == 0) K1_MARK(27);
                 }
 #pragma unroll
@@ -517,7 +527,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int q = warp & 3;            // TMEM lane quarter (warps 10..13 -> 2,3,0,1)
         const int fl = q * 32 + lane;      // feature row within the tile
 
-        // The other parity's buffer, for the next launch (stream-ordered after this one).
+        // The other parity's buffer, for the next launch, once the previous launch
+        // (its owner) has completed; also orders this launch's reductions after it.
+        asm volatile("griddepcontrol.wait;\n" ::: "memory");
         for (uint32_t i = static_cast<uint32_t>(cta * 128 + ct); i < a.clear_vec; i += static_cast<uint32_t>(grid * 128))
             a.act_clear[i] = make_uint4(0u, 0u, 0u, 0u);
         // Staging (after the ring): half h holds rows 16h..16h+15 as [128 features][128 B], 16-byte chunk j of
@@ -674,13 +686,13 @@ void mlp_debug_report(const unsigned long long* dbg, int grid, int L, int model,
         std::fprintf(stderr, "  %-18s %7.2f %7.2f %7.2f %7.2f %7.2f\n", name, v[0], v[n / 10], v[n / 2], v[n * 9 / 10],
                      v[n - 1]);
     }
-    std::fprintf(stderr, "  CTA 0 steps (us): W issued, X issued, W landed, raw landed, operand ready, MMA issued\n");
+    std::fprintf(stderr, "  CTA 0 steps (us): W issued, X issued, W landed, raw landed, operand ready, MMA issued, W_lo stored, X read\n");
     for (int g = 0; g < 96; ++g) {
         const unsigned long long* p = m.data() + static_cast<size_t>(grid) * 32 + g * 8;
-        if (!p[0]) break;
+        if (!p[0] && !p[2]) break;  // (odd steps of a producer pair have no issue mark of their own)
         auto us = [&](unsigned long long t) { return t ? (t - t0) * 1e-3 : -1.0; };
-        std::fprintf(stderr, "   %2d %7.2f %7.2f %7.2f %7.2f %7.2f %7.2f\n", g, us(p[0]), us(p[1]), us(p[2]), us(p[3]),
-                     us(p[4]), us(p[5]));
+        std::fprintf(stderr, "   %2d %7.2f %7.2f %7.2f %7.2f %7.2f %7.2f %7.2f %7.2f\n", g, us(p[0]), us(p[1]), us(p[2]), us(p[3]),
+                     us(p[4]), us(p[5]), us(p[6]), us(p[7]));
     }
     GFX_CUDA(cudaMemset(const_cast<unsigned long long*>(dbg), 0, m.size() * 8));
 }
@@ -717,9 +729,17 @@ void launch_mlp_forward(MlpFwdArgs& a, cudaStream_t stream) {
     cfg.blockDim = dim3(kThreads);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = stream;
+    // Every CTA must become resident (CTAs wait on each other's partials):
+    // cooperative launch, or — on a device this process's one manager owns —
+    // a PDL-chained launch whose CTAs take SMs as the previous forward frees them.
     cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;  // every CTA co-resident: the counter waits need it
-    attr[0].val.cooperative = 1;
+    if (a.pdl) {
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+    } else {
+        attr[0].id = cudaLaunchAttributeCooperative;
+        attr[0].val.cooperative = 1;
+    }
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     GFX_CUDA(cudaLaunchKernelEx(&cfg, mlp_forward_kernel, a));
