@@ -543,18 +543,44 @@ void GpuManager::infer(int model, const void* in_v, void* out_v, void* debug_hid
     f.act_clear = reinterpret_cast<uint4*>(fwd_act_ + (p ^ 1u) * kMlpActWords);
     f.clear_vec = act_dirty_[p ^ 1u] / 2;
 #ifdef GFX_K1_DEBUG
+    // Four consecutive launches (8..11 of every 64) mark into their own tables,
+    // then one report: the chain's per-launch CTA start / end spread (does the
+    // next forward's CTAs start before this one's last CTA ends?) and launch 10's
+    // phase table.
+    constexpr size_t kDbgWords = 32 * 1024 + 96 * 8;
     static unsigned long long* dbg = nullptr;
     static unsigned launches = 0;
     if (!dbg) {
-        GFX_CUDA(cudaMalloc(&dbg, sizeof(unsigned long long) * (32 * 1024 + 96 * 8)));
-        GFX_CUDA(cudaMemset(dbg, 0, sizeof(unsigned long long) * (32 * 1024 + 96 * 8)));
+        GFX_CUDA(cudaMalloc(&dbg, sizeof(unsigned long long) * kDbgWords * 4));
+        GFX_CUDA(cudaMemset(dbg, 0, sizeof(unsigned long long) * kDbgWords * 4));
     }
-    f.dbg = dbg;
+    const unsigned ph = ++launches % 64;
+    f.dbg = ph >= 8 && ph <= 11 ? dbg + kDbgWords * (ph - 8) : nullptr;
 #endif
     if (layer_timer) GFX_CUDA(cudaEventRecord(layer_timer->next(), compute_));
     launch_mlp_forward(f, compute_);
 #ifdef GFX_K1_DEBUG
-    if (++launches % 64 == 8) mlp_debug_report(dbg, f.grid, f.L, model, compute_);
+    if (ph == 11) {
+        std::vector<unsigned long long> m(kDbgWords * 4);
+        GFX_CUDA(cudaStreamSynchronize(compute_));
+        GFX_CUDA(cudaMemcpy(m.data(), dbg, m.size() * 8, cudaMemcpyDeviceToHost));
+        unsigned long long t0 = ~0ull;
+        for (int c = 0; c < f.grid; ++c) t0 = std::min(t0, m[static_cast<size_t>(c) * 32]);
+        std::fprintf(stderr, "[K1 chain, pdl %d] us from launch 8's first CTA: start min/max, end min/median/max\n", f.pdl);
+        for (int k = 0; k < 4; ++k) {
+            std::vector<double> st, en;
+            for (int c = 0; c < f.grid; ++c) {
+                st.push_back((m[kDbgWords * k + static_cast<size_t>(c) * 32] - t0) * 1e-3);
+                en.push_back((m[kDbgWords * k + static_cast<size_t>(c) * 32 + 26] - t0) * 1e-3);
+            }
+            std::sort(st.begin(), st.end());
+            std::sort(en.begin(), en.end());
+            std::fprintf(stderr, "  launch %d: start %7.2f %7.2f  end %7.2f %7.2f %7.2f\n", 8 + k, st.front(), st.back(),
+                         en.front(), en[en.size() / 2], en.back());
+        }
+        mlp_debug_report(dbg + kDbgWords * 2, f.grid, f.L, model, compute_);
+        GFX_CUDA(cudaMemset(dbg, 0, sizeof(unsigned long long) * kDbgWords * 4));
+    }
 #endif
     act_dirty_[p ^ 1u] = 0;
     act_dirty_[p] = act;

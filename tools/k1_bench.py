@@ -7,7 +7,7 @@ import os
 import sys
 import time
 
-ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+ROOT = os.environ.get("GFX_PKG_ROOT") or os.path.dirname(os.path.dirname(os.path.abspath(__file__)))  # GFX_PKG_ROOT: A/B a copy of the package
 sys.path.insert(0, ROOT)
 import paper_2303_05601_b200 as gfx
 from paper_2303_05601_b200 import _ffi as F
