@@ -290,7 +290,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
                         } else {
                             const int bt = nb * (kBN / 128) + static_cast<int>(rank) * kBTiles + h;
                             const uint64_t v = a.w_off + (static_cast<uint64_t>(bt) * ktiles_row + k) * kGATile;
-                            const uint64_t row = static_cast<uint64_t>(translate(a.arena, pt, v) - a.arena) / 128;
+                            const uint64_t row = static_cast<uint64_t>(translate(a.arena, pt, v) - a.arena) / 512;
                             tma_tile2d_g2s_pair(st + kGATile + h * kGATile, &tmap_w, 0, static_cast<int>(row), &full_bar[s]);
                         }
                     } else if (warp == kGAWarp) {
@@ -933,8 +933,9 @@ void gemm_bn(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_
     if (kPair) {
         uint32_t maxp = 0;
         for (uint32_t i = 0; i < pt.n; ++i) maxp = std::max(maxp, pt.page[i]);
-        const uint64_t rows = (static_cast<uint64_t>(maxp) + 1) * (kPageBytes / 128);
-        if (!encode_tensor_map_2d(&tmw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, arena, 64, rows, 128, 64, 128,
+        // 512-byte rows, 32-row boxes: a 16 KB tile as 32 row requests instead of 128.
+        const uint64_t rows = (static_cast<uint64_t>(maxp) + 1) * (kPageBytes / 512);
+        if (!encode_tensor_map_2d(&tmw, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, arena, 256, rows, 512, 256, 32,
                                   CU_TENSOR_MAP_SWIZZLE_NONE))
             throw CudaError("cuTensorMapEncodeTiled failed (bert gemm arena weights)");
     }
