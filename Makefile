@@ -21,6 +21,9 @@ NVFLAGS  := -std=c++20 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Xcompiler -ffp-co
 ifeq ($(K2_DEBUG),1)
 NVFLAGS += -DGFX_K2_DEBUG   # BERT GEMM per-CTA phase tables (debug only, never shipped)
 endif
+ifeq ($(K5_DEBUG),1)
+NVFLAGS += -DGFX_K5_DEBUG   # encoder dataflow kernel per-item timeline (debug only, never shipped)
+endif
 ifeq ($(K1_DEBUG),1)
 NVFLAGS += -DGFX_K1_DEBUG $(K1_EXTRA)   # K1 wait watchdogs + phase marks (debug only, never shipped)
 endif

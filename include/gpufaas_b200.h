@@ -135,6 +135,7 @@ int gfx_arena_reset(gfx_arena_t a); /* synchronise, evict everything */
 int gfx_arena_free_pages(gfx_arena_t a, int32_t* out);
 /* Explicit manager options (no environment switches on the product path). */
 #define GFX_OPT_GEMM_PAIR 1 /* BERT GEMMs on 2-SM (cta_group::2) tiles where the shape allows; default 0 */
+#define GFX_OPT_BERT_FLOW 2 /* BERT forward as the encoder dataflow kernel K5 (one launch) instead of per-op K2-K4 launches; default 0 */
 int gfx_arena_set_option(gfx_arena_t a, int32_t option, int32_t value);
 int gfx_arena_resident(gfx_arena_t a, int model_idx, int32_t* out);
 

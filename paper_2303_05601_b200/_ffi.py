@@ -90,6 +90,7 @@ gfx_arena_reset = _sig("gfx_arena_reset", C.c_int, [_vp])
 gfx_arena_free_pages = _sig("gfx_arena_free_pages", C.c_int, [_vp, C.POINTER(C.c_int32)])
 gfx_arena_set_option = _sig("gfx_arena_set_option", C.c_int, [_vp, C.c_int32, C.c_int32])
 GFX_OPT_GEMM_PAIR = 1
+GFX_OPT_BERT_FLOW = 2
 gfx_infer_sequence = _sig("gfx_infer_sequence", C.c_int, [_vp, _vp, C.c_int, _vp, C.c_uint64, _vp, C.c_uint64,
                                                           C.POINTER(C.c_double)])
 gfx_bert_gemm = _sig("gfx_bert_gemm", C.c_int, [_vp, C.c_int, C.c_int, C.c_int, _vp, _vp, _vp, C.c_int])

@@ -679,9 +679,12 @@ int gfx_arena_free_pages(gfx_arena_t a, int32_t* out) {
 }
 int gfx_arena_set_option(gfx_arena_t a, int32_t option, int32_t value) {
     return guarded([&] {
-        if (option != GFX_OPT_GEMM_PAIR || (value != 0 && value != 1))
+        if ((option != GFX_OPT_GEMM_PAIR && option != GFX_OPT_BERT_FLOW) || (value != 0 && value != 1))
             throw std::invalid_argument("unknown arena option or value");
-        a->mgr->set_gemm_pair(value != 0);
+        if (option == GFX_OPT_GEMM_PAIR)
+            a->mgr->set_gemm_pair(value != 0);
+        else
+            a->mgr->set_bert_flow(value != 0);
     });
 }
 int gfx_arena_resident(gfx_arena_t a, int model_idx, int32_t* out) {

@@ -30,6 +30,7 @@
 #include <stdexcept>
 
 #include "bert.cuh"
+#include "bert_dev.cuh"
 #include "mlp.cuh"
 #include "sm100.cuh"
 
@@ -39,11 +40,7 @@ namespace {
 
 using namespace gfx::sm100;
 
-__device__ __forceinline__ const char* translate(const char* arena, const uint32_t* pt, uint64_t v) {
-    return arena + (static_cast<uint64_t>(pt[v >> kPageShift]) << kPageShift) + (v & kPageMask);
-}
-__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
-__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
+using namespace gfx::bertdev;
 
 #ifdef GFX_K2_DEBUG
 // Per-CTA phase marks (debug build only): 0 start, 1 setup, 2 first A issued;
@@ -87,23 +84,6 @@ __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.lau
     do {                \
     } while (0)
 #endif
-
-// GELU(x) = x/2 (1 + erf(x / sqrt 2)) with erf from Abramowitz & Stegun 7.1.26
-// (|error| <= 1.5e-7, far below the bf16 output's 2^-9 relative resolution):
-// one rcp, one ex2 and 8 FMAs instead of erff's branchy ~30 instructions — the
-// FFN1 epilogue was the bottleneck of that GEMM (~6 µs per 128 x 256 tile
-// against ~4.2 µs of MMAs).
-__device__ __forceinline__ float gelu(float x) {
-    const float z = fabsf(x) * 0.70710678118654752f;
-    float t;
-    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(t) : "f"(fmaf(0.3275911f, z, 1.0f)));
-    const float poly =
-        t * fmaf(fmaf(fmaf(fmaf(1.061405429f, t, -1.453152027f), t, 1.421413741f), t, -0.284496736f), t, 0.254829592f);
-    float e;  // exp(-z^2) = 2^(-z^2 log2 e)
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(e) : "f"(-z * z * 1.4426950408889634f));
-    const float erf_abs = 1.0f - poly * e;
-    return 0.5f * x * (1.0f + copysignf(erf_abs, x));
-}
 
 // Debug build: kernel spans of one traced forward (bert_forward's 10th call).
 #ifdef GFX_K2_DEBUG
@@ -159,14 +139,6 @@ struct GemmArgs {
     int T, K, N;
     PageTable pt;
 };
-
-// Chan et al. pairwise combination of (count, mean, M2) partial statistics.
-__device__ __forceinline__ void chan_combine(float& n_a, float& mean_a, float& m2_a, float n_b, float mean_b, float m2_b) {
-    const float n = n_a + n_b, dlt = mean_b - mean_a;
-    mean_a = fmaf(dlt, n_b / n, mean_a);
-    m2_a = m2_a + m2_b + dlt * dlt * (n_a * n_b / n);
-    n_a = n;
-}
 
 // kPair: 2-SM tcgen05 (cta_group::2). A CTA pair (cluster of 2) computes a
 // 256 x kBN tile: each CTA stages its own 128 rows of A and its half of the
@@ -605,11 +577,6 @@ constexpr int kS = 128, kDh = 64;
 // model's flops took 12 % of its time there.)
 constexpr uint32_t kAttnSmem = 3 * 16384 + 1024;  // Q, K, V; P overlays Q + K once S is computed
 
-__device__ __forceinline__ float ex2_approx(float x) {
-    float y;
-    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-    return y;
-}
 
 __global__ void __launch_bounds__(128, 4) attention_tc_kernel(const __grid_constant__ CUtensorMap tmap_qkv,
                                                            __nv_bfloat16* __restrict__ ctx, int heads,
@@ -1142,6 +1109,13 @@ void BertWorkspace::release() {
     }
 
     tokens = 0;
+    if (flow_items) cudaFree(flow_items);
+    if (flow_cnt) cudaFree(flow_cnt);
+    if (flow_stats) cudaFree(flow_stats);
+    flow_items = flow_cnt = nullptr;
+    flow_stats = nullptr;
+    flow_n_items = flow_L = flow_M = flow_F = flow_ctas = 0;
+    flow_cnt_words = 0;
 }
 
 int bert_forward(const char* arena, const PageTable& pt, const BertLayout& lay, int batch, const __nv_bfloat16* in,
@@ -1166,7 +1140,15 @@ int bert_forward(const char* arena, const PageTable& pt, const BertLayout& lay, 
     const __nv_bfloat16* x = in;
     const size_t hbytes = static_cast<size_t>(T) * d * 2;
     if (hidden) GFX_CUDA(cudaMemcpyAsync(hidden, in, hbytes, cudaMemcpyDeviceToDevice, s));
-    for (int l = 0; l < lay.L; ++l) {
+    const bool flow = ws.flow && bert_flow_supported(lay, batch);
+    if (flow) {
+        // K5: every layer in one dataflow launch; with `hidden`, layer l's output lands in hidden[l + 1].
+        __nv_bfloat16* xout = hidden ? hidden + static_cast<size_t>(T) * d : ws.x;
+        const int xstride = hidden ? T : 0;
+        launches += bert_encoder_flow(arena, pt, lay, batch, in, xout, xstride, ws, s);
+        x = xout + static_cast<size_t>(lay.L - 1) * xstride * d;
+    }
+    for (int l = 0; l < (flow ? 0 : lay.L); ++l) {
         const BertLayerOffsets& o = lay.layer[static_cast<size_t>(l)];
         gemm<kEpiBias>(arena, pt, o.wqkv, o.bqkv, x, ws.qkv, nullptr, T, d, 3 * d, s, l > 0 && !hidden, ws.gemm_pair);
         {

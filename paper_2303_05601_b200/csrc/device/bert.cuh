@@ -56,10 +56,23 @@ __host__ __device__ inline uint16_t bf16_bits(float f) {
 struct BertWorkspace {
     int tokens = 0;
     bool gemm_pair = false;  // 2-SM (cta_group::2) GEMMs where the shape allows (gfx_arena_set_option)
+    bool flow = false;       // the encoder dataflow kernel K5 instead of per-op launches (K2-K4)
     __nv_bfloat16 *x = nullptr, *qkv = nullptr, *ctx = nullptr, *h = nullptr, *f = nullptr, *t = nullptr;
+    // K5: claim list and dataflow counters for one (layers, row blocks, ffn, SMs) shape.
+    uint32_t *flow_items = nullptr, *flow_cnt = nullptr;
+    void* flow_stats = nullptr;  // per-row LayerNorm statistics of the residual tiles
+    int flow_n_items = 0, flow_L = 0, flow_M = 0, flow_F = 0, flow_ctas = 0;
+    size_t flow_cnt_words = 0;
     void ensure(int tokens, int d, int ffn);
     void release();
 };
+
+// K5 (bert_flow.cu): all encoder layers as one persistent dataflow launch.
+// Layer l's output goes to xout + l * xstride rows (xstride 0: one buffer,
+// rewritten in place per row block); layer 0 reads `in`.
+bool bert_flow_supported(const BertLayout& lay, int batch);
+int bert_encoder_flow(const char* arena, const PageTable& pt, const BertLayout& lay, int batch,
+                      const __nv_bfloat16* in, __nv_bfloat16* xout, int xstride, BertWorkspace& ws, cudaStream_t s);
 
 // One forward of a resident BERT model: in = [batch*seq x d] bf16 embeddings,
 // out = [batch x d] fp32 pooled output. Returns kernel launches.

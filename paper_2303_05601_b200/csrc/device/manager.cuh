@@ -111,6 +111,7 @@ public:
     char* arena() const { return arena_; }
     void activate() const;  // cudaSetDevice
     void set_gemm_pair(bool on) { bert_ws_.gemm_pair = on; }
+    void set_bert_flow(bool on) { bert_ws_.flow = on; }
 
     // Instrumentation (all optional).
     KernelTimer* layer_timer = nullptr;   // records around every inference

@@ -14,7 +14,9 @@ check is per layer: feed each oracle layer the GPU's own input to that layer
 and compare outputs — done here for all 12 layers of full BERT-base, at
 2 x 128 tokens and at the C5 request shape (32 sequences x 128 tokens = 4096
 tokens, where every persistent GEMM CTA runs 2-3 tiles and reuses its TMEM
-accumulators), for the single-CTA and the 2-SM GEMM kernels. Each fused GEMM
+accumulators), for the encoder dataflow kernel K5 (the production path) and
+the per-op launches with single-CTA and 2-SM GEMM kernels, plus K5 at ragged
+batches (1, 3, 37 sequences). Each fused GEMM
 epilogue (bias, GELU, residual) is also checked alone against a numpy fp64
 GEMM with the same bf16 rounding point."""
 import ctypes as C
@@ -65,7 +67,7 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / np.linalg.norm(b))
 
 
-def run_gpu(gfx, idx, layers, seqs, seed, request_id=7, debug=True, pair=False):
+def run_gpu(gfx, idx, layers, seqs, seed, request_id=7, debug=True, mode="perop"):
     desc = gfx.models.bert_desc(layers, seqs, seed)
     gfx.check(gfx._ffi.gfx_model_register(idx, C.byref(desc)))
     inb, outb = C.c_uint64(), C.c_uint64()
@@ -76,7 +78,8 @@ def run_gpu(gfx, idx, layers, seqs, seed, request_id=7, debug=True, pair=False):
     a = C.c_void_p()
     gfx.check(gfx._ffi.gfx_arena_create(0, (pages.value + 2) << 21, C.byref(a)))
     try:
-        gfx.check(gfx._ffi.gfx_arena_set_option(a, gfx._ffi.GFX_OPT_GEMM_PAIR, int(pair)))
+        gfx.check(gfx._ffi.gfx_arena_set_option(a, gfx._ffi.GFX_OPT_GEMM_PAIR, int(mode == "pair")))
+        gfx.check(gfx._ffi.gfx_arena_set_option(a, gfx._ffi.GFX_OPT_BERT_FLOW, int(mode == "flow")))
         x_bits = np.zeros(inb.value // 2, np.uint16)
         gfx.check(gfx._ffi.gfx_host_fill_input(idx, request_id, x_bits.ctypes.data, inb.value))
         xd, yd, hd = C.c_void_p(), C.c_void_p(), C.c_void_p()
@@ -156,19 +159,35 @@ def teacher_forced(olib, seed, layers, seqs, hidden, pooled, check_layers=None):
     return worst
 
 
-@pytest.mark.parametrize("pair", [False, True])
-def test_bert_c5_shape_teacher_forced(gfx, olib, pair):
+@pytest.mark.parametrize("mode", ["flow", "perop", "pair"])
+def test_bert_c5_shape_teacher_forced(gfx, olib, mode):
     """The C5 request: 32 sequences x 128 tokens (T = 4096) through all 12
-    layers on the production path; every layer (single-CTA GEMMs) or layers
-    0, 1, 6, 11 (2-SM GEMMs) teacher-forced against the oracle, plus the pooler."""
+    layers: the production encoder dataflow kernel K5 ("flow") and the per-op
+    launches (single-CTA or 2-SM GEMMs); every layer (flow, perop) or layers
+    0, 1, 6, 11 (pair) teacher-forced against the oracle, plus the pooler."""
     layers, seqs = 12, 32
     seed = gfx.model_seed("bert-base-c5-fullshape")
-    x_bits, pooled, again, hidden = run_gpu(gfx, 72, layers, seqs, seed, request_id=11, pair=pair)
+    x_bits, pooled, again, hidden = run_gpu(gfx, 72, layers, seqs, seed, request_id=11, mode=mode)
     assert np.array_equal(pooled, again), "inference must be deterministic"
     assert np.array_equal(hidden[0], x_bits)
     assert np.isfinite(pooled).all()
-    worst = teacher_forced(olib, seed, layers, seqs, hidden, pooled, None if not pair else (0, 1, 6, 11))
-    print(f"C5 shape (pair={pair}): worst per-layer normwise error {worst:.2e}")
+    worst = teacher_forced(olib, seed, layers, seqs, hidden, pooled, None if mode != "pair" else (0, 1, 6, 11))
+    print(f"C5 shape ({mode}): worst per-layer normwise error {worst:.2e}")
+
+
+@pytest.mark.parametrize("seqs", [1, 3, 37])
+def test_bert_flow_ragged_batches(gfx, olib, seqs):
+    """K5 at batches that do not fill the 148 SMs (1, 3 row blocks) or leave a
+    ragged last wave (37): all layers teacher-forced against the oracle, and
+    layer 0's output within tolerance of the per-op launches' (same rounding
+    points; only the softmax denominator's summation order differs)."""
+    layers = 12 if seqs == 1 else 4
+    seed = gfx.model_seed(f"bert-flow-ragged-{seqs}")
+    x_bits, pooled, again, hidden = run_gpu(gfx, 73, layers, seqs, seed, request_id=5, mode="flow")
+    assert np.array_equal(pooled, again)
+    teacher_forced(olib, seed, layers, seqs, hidden, pooled)
+    _, _, _, hidden_op = run_gpu(gfx, 73, layers, seqs, seed, request_id=5, mode="perop")
+    assert rel(bf16_to_f32(hidden[1]), bf16_to_f32(hidden_op[1])) <= TOL
 
 
 def bf16_round(x):
