@@ -79,6 +79,7 @@ constexpr uint32_t kFRing = kFStages * kFStage;  // 192 KB
 constexpr uint32_t kFBoxes = 4 * 8192;          // epilogue staging (4 groups x 128 x 32 bf16)
 constexpr size_t kFSmem = kFRing + kFBoxes + 1024;
 constexpr int kFQueue = 4;
+constexpr uint32_t kFCluster = 3;  // CTAs per cluster = a row block's three d-column tiles
 constexpr int kFD = 768, kFHeads = 12, kFSeq = 128;
 
 enum FlowOp : uint32_t { kOpQkv = 0, kOpAtt = 1, kOpO = 2, kOpF1 = 3, kOpF2 = 4, kOpEnd = 7 };
@@ -119,7 +120,7 @@ __device__ __forceinline__ unsigned long long gtimer() {
 struct FlowMaps {
     CUtensorMap a_in, a_x, a_ctx, a_h, a_f;  // A operands: 64 x 128 boxes, SWIZZLE_128B
     CUtensorMap qkv;                         // attention Q / K / V: 64 x 128 boxes, SWIZZLE_128B
-    CUtensorMap y_qkv, y_f, y_t;             // outputs: 32 x 128 boxes, SWIZZLE_64B
+    CUtensorMap y_qkv, y_f, y_h, y_x;        // outputs: 32 x 128 boxes, SWIZZLE_64B
     CUtensorMap r_in, r_x, r_h;              // residuals: 32 x 128 boxes, SWIZZLE_64B
 };
 
@@ -127,16 +128,24 @@ struct FlowArgs {
     const char* arena;
     BertLayerOffsets l0;    // layer 0's parameter offsets; layer l = l0 + l * stride
     uint64_t stride;
-    uint32_t* slots;        // ready queue: item + 1 per pushed entry (zeroed per launch)
-    int n_items, n_first;   // all items; layer 0's QKV tiles = the queue's implicit first n_first entries
+    uint32_t* slots;        // ready queue of cluster items: item + 1 per pushed entry (zeroed per launch)
+    int n_items, n_first;   // all cluster items; layer 0's QKV triples = the queue's implicit first n_first
     uint32_t* cnt;          // [L][M][kCSlots] completion counters, then head, tail (zeroed per launch)
-    __nv_bfloat16 *ctx, *h, *t, *xout;
-    float2* stats;          // [L][M][2 LayerNorms][3 column tiles][128 rows] (mean, M2) of t
+    float2* stats;          // [L][M][2 LayerNorms][3 column tiles][128 rows] (mean, M2) of the pre-LN rows
+    __nv_bfloat16 *ctx, *h, *xout;
     int M, L, ffn;
     int xstride;            // rows between consecutive layers' outputs in xout (0: one buffer)
     unsigned long long* trace;  // GFX_K5_DEBUG builds: [grid][kFTraceItems][8], else nullptr
     PageTable pt;
 };
+
+// This CTA's unit of a cluster item (op, l, m, t): the O / FFN2 triple is the row
+// block's three column tiles, the others are the t-th triple of tiles / heads.
+__device__ __forceinline__ uint32_t cta_item(uint32_t cit, uint32_t rank) {
+    const uint32_t op = cit >> 29, t = cit & 4095u;
+    const uint32_t n = (op == kOpO || op == kOpF2) ? rank : 3u * t + rank;
+    return (cit & ~4095u) | n;
+}
 
 __global__ void __launch_bounds__(kFThreads, 1)
     encoder_flow_kernel(const __grid_constant__ FlowMaps mp, const __grid_constant__ FlowArgs a) {
@@ -144,12 +153,13 @@ __global__ void __launch_bounds__(kFThreads, 1)
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* boxes = smem + kFRing;
     __shared__ __align__(8) uint64_t full_bar[kFStages], empty_bar[kFStages], tfull_bar[2], tempty_bar[2], res_bar[4];
-    __shared__ __align__(8) uint64_t o_bar, q_full[kFQueue], q_empty[kFQueue];
+    __shared__ __align__(8) uint64_t o_bar, q_full[kFQueue], q_empty[kFQueue], sib_bar[2];
     __shared__ uint32_t q_item[kFQueue];
-    __shared__ uint32_t tmem_s, ln_flag;
+    __shared__ uint32_t tmem_s;
     __shared__ float bias_s[256];
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const uint32_t rank = cluster_ctarank();
     const uint32_t* const pt = a.pt.page;
     if (tid == 0) {
         for (int s = 0; s < kFStages; ++s) {
@@ -159,28 +169,33 @@ __global__ void __launch_bounds__(kFThreads, 1)
         for (int b = 0; b < 2; ++b) {
             mbar_init(&tfull_bar[b], 1);
             mbar_init(&tempty_bar[b], kFEpiWarps);
+            mbar_init(&sib_bar[b], kFCluster);  // the cluster's three CTAs' LayerNorm statistics written
         }
         for (int g = 0; g < 4; ++g) mbar_init(&res_bar[g], 1);
         mbar_init(&o_bar, 1);
         for (int q = 0; q < kFQueue; ++q) {
             mbar_init(&q_full[q], 1);
-            mbar_init(&q_empty[q], 2 + 1 + kFEpiWarps);  // weight producers, MMA, epilogue warps
+            // Leader's copy: every consumer of the cluster (weight producers, MMA, epilogue
+            // warps of each CTA, and the other CTAs' A producers) releases the slot here.
+            mbar_init(&q_empty[q], kFCluster * (2 + 1 + kFEpiWarps) + (kFCluster - 1));
         }
         mbar_fence_init();
         tma_prefetch_desc(&mp.a_in), tma_prefetch_desc(&mp.a_x), tma_prefetch_desc(&mp.a_ctx);
         tma_prefetch_desc(&mp.a_h), tma_prefetch_desc(&mp.a_f), tma_prefetch_desc(&mp.qkv);
-        tma_prefetch_desc(&mp.y_qkv), tma_prefetch_desc(&mp.y_f), tma_prefetch_desc(&mp.y_t);
-        tma_prefetch_desc(&mp.r_in), tma_prefetch_desc(&mp.r_x), tma_prefetch_desc(&mp.r_h);
+        tma_prefetch_desc(&mp.y_qkv), tma_prefetch_desc(&mp.y_f), tma_prefetch_desc(&mp.y_h);
+        tma_prefetch_desc(&mp.y_x), tma_prefetch_desc(&mp.r_in), tma_prefetch_desc(&mp.r_x);
+        tma_prefetch_desc(&mp.r_h);
     }
     if (warp == kFMmaWarp) tmem_alloc<512>(&tmem_s);
     tc_fence_before();
     __syncthreads();
+    cluster_sync();  // every CTA's barriers exist before any remote arrive reaches them
     tc_fence_after();
     const uint32_t tmem = tmem_s;
     uint32_t* const qhead = a.cnt + static_cast<size_t>(a.L) * a.M * kCSlots;
     uint32_t* const qtail = qhead + 1;
     auto counter = [&](int l, int m, uint32_t op) { return a.cnt + (static_cast<size_t>(l) * a.M + m) * kCSlots + op; };
-    // Make items first .. first + count - 1 (consecutive tiles / heads) ready: after the
+    // Make cluster items first .. first + count - 1 (consecutive triples) ready: after the
     // caller's fence, one tail bump and a release store per queue slot.
     auto push = [&](uint32_t first, int count) {
         const uint32_t base = atomicAdd(qtail, static_cast<uint32_t>(count));
@@ -188,40 +203,53 @@ __global__ void __launch_bounds__(kFThreads, 1)
     };
     const int nk_ffn = a.ffn / 64, nf1 = a.ffn / 256;
     auto nk_of = [&](uint32_t op) { return op == kOpAtt ? 1 : op == kOpF2 ? nk_ffn : kFD / 64; };
-    // Consumers of the item queue: wait for slot j, read, release.
+    // Consumers of the cluster's item queue: wait for slot j (filled by the leader CTA),
+    // read this CTA's unit, release the slot in the leader.
     auto take = [&](int j) {
         const int slot = j % kFQueue;
-        mbar_wait(&q_full[slot], (j / kFQueue) & 1);
-        return q_item[slot];
+        mbar_wait_cluster(&q_full[slot], (j / kFQueue) & 1);
+        const uint32_t cit = q_item[slot];
+        return (cit >> 29) == kOpEnd ? cit : cta_item(cit, rank);
     };
+    auto release = [&](int j) { mbar_arrive_remote(&q_empty[j % kFQueue], 0); };
 
     if (warp == kFAWarp) {
-        // ---------------- A producer: pops ready items, loads A (or Q, K, V).
+        // ---------------- A producer (leader: pops ready cluster items and hands them to the
+        // cluster's three CTAs); loads A (or Q, K, V) of this CTA's unit.
         if (lane == 0) {
             int g = 0;
             for (int j = 0;; ++j) {
                 const int slot = j % kFQueue;
-                if (j >= kFQueue) mbar_wait(&q_empty[slot], ((j / kFQueue) & 1) ^ 1);
-                // Pop the next READY item (its inputs are complete and visible).
-                const uint32_t idx = atomicAdd(qhead, 1u);
                 uint32_t it;
-                if (idx >= static_cast<uint32_t>(a.n_items)) {
-                    it = flow_item(kOpEnd, 0, 0, 0);
-                } else if (idx < static_cast<uint32_t>(a.n_first)) {
-                    it = flow_item(kOpQkv, 0, idx / 9, idx % 9);
+                if (rank == 0) {
+                    if (j >= kFQueue) mbar_wait(&q_empty[slot], ((j / kFQueue) & 1) ^ 1);
+                    const uint32_t idx = atomicAdd(qhead, 1u);
+                    uint32_t cit;
+                    if (idx >= static_cast<uint32_t>(a.n_items)) {
+                        cit = flow_item(kOpEnd, 0, 0, 0);
+                    } else if (idx < static_cast<uint32_t>(a.n_first)) {
+                        cit = flow_item(kOpQkv, 0, idx / 3, idx % 3);
+                    } else {
+                        const uint32_t* sl = a.slots + (idx - a.n_first);
+                        uint32_t v;
+                        while ((v = ld_acquire_gpu_u32(sl)) == 0) __nanosleep(32);
+                        cit = v - 1;
+                    }
+                    for (uint32_t r = 0; r < kFCluster; ++r) {
+                        st_cluster_u32(mapa_u32(&q_item[slot], r), cit);
+                        mbar_arrive_remote(&q_full[slot], r);
+                    }
+                    it = (cit >> 29) == kOpEnd ? cit : cta_item(cit, 0);
+                    mbar_wait_cluster(&q_full[slot], (j / kFQueue) & 1);  // keep this CTA's own slot phase in step
                 } else {
-                    const uint32_t* sl = a.slots + (idx - a.n_first);
-                    uint32_t v;
-                    while ((v = ld_acquire_gpu_u32(sl)) == 0) __nanosleep(32);
-                    it = v - 1;
-                    fence_proxy_async_global();  // generic-proxy acquire -> the TMA reads below
+                    it = take(j);
+                    release(j);
                 }
-                q_item[slot] = it;
                 K5_MARK(j, 0, it);
                 K5_MARK(j, 1, gtimer());
-                mbar_arrive(&q_full[slot]);
                 const uint32_t op = it_op(it);
                 if (op == kOpEnd) break;
+                fence_proxy_async_global();  // the pusher's release (acquired above) -> the TMA reads below
                 const int l = it_l(it), m = it_m(it);
                 K5_MARK(j, 2, gtimer());
                 const int m0 = m * kFSeq;
@@ -256,7 +284,7 @@ __global__ void __launch_bounds__(kFThreads, 1)
             int g = 0;
             for (int j = 0;; ++j) {
                 const uint32_t it = take(j);
-                mbar_arrive(&q_empty[j % kFQueue]);
+                release(j);
                 const uint32_t op = it_op(it);
                 if (op == kOpEnd) break;
                 if (op == kOpAtt) {  // attention: nothing to load, keep the stage's arrival count
@@ -285,15 +313,14 @@ __global__ void __launch_bounds__(kFThreads, 1)
         if (lane == 0) {
             constexpr uint32_t idesc = umma_idesc<128, 256, 1>();    // bf16 x bf16 -> f32
             constexpr uint32_t idesc_s = umma_idesc<128, 128, 1>();  // S = Q K^T
-            int g = 0, jt = 0;  // jt: items using the accumulators (GEMM tiles, attention)
+            int g = 0;
             for (int j = 0;; ++j) {
                 const uint32_t it = take(j);
-                mbar_arrive(&q_empty[j % kFQueue]);
+                release(j);
                 const uint32_t op = it_op(it);
                 if (op == kOpEnd) break;
-                const int b = jt & 1;
-                if (jt >= 2) mbar_wait(&tempty_bar[b], ((jt >> 1) & 1) ^ 1);  // epilogue drained item jt-2
-                ++jt;
+                const int b = j & 1;
+                if (j >= 2) mbar_wait(&tempty_bar[b], ((j >> 1) & 1) ^ 1);  // epilogue drained item j - 2
                 tc_fence_after();
                 const uint32_t acc = tmem + static_cast<uint32_t>(b * 256);
                 if (op == kOpAtt) {
@@ -336,17 +363,17 @@ __global__ void __launch_bounds__(kFThreads, 1)
         auto epi_sync = [&] { asm volatile("bar.sync 3, %0;\n" ::"r"(kFEpiWarps * 32) : "memory"); };
         uint8_t* box = boxes + gp * 8192;
         const uint32_t lane_off = static_cast<uint32_t>(q * 32) << 16;
-        int g = 0, na = 0, e = 0, jt = 0;
+        auto box_chunk = [&](int u) { return box + r * 64 + ((u ^ ((r >> 1) & 3)) << 4); };  // SWIZZLE_64B row r
+        int g = 0, na = 0, e = 0, nln = 0;
         for (int j = 0;; ++j) {
             const uint32_t it = take(j);
             __syncwarp();
-            if (lane == 0) mbar_arrive(&q_empty[j % kFQueue]);
+            if (lane == 0) release(j);
             const uint32_t op = it_op(it);
             if (op == kOpEnd) break;
             const int l = it_l(it), m = it_m(it), n = it_n(it), m0 = m * kFSeq;
             const uint64_t lo = a.stride * static_cast<uint64_t>(l);
-            const int b = jt & 1, tpar = (jt >> 1) & 1;
-            ++jt;
+            const int b = j & 1, tpar = (j >> 1) & 1;
             const uint32_t acc = tmem + static_cast<uint32_t>(b * 256);
             if (op == kOpAtt) {
                 // ---- attention of (row block m, head n): softmax over S in TMEM, P V, ctx.
@@ -413,88 +440,106 @@ __global__ void __launch_bounds__(kFThreads, 1)
                 dst[0] = o[0];
                 dst[1] = o[1];
                 epi_sync();
-                if (tid == 0) {  // the row block's last head makes its three O tiles ready
+                if (tid == 0) {  // the row block's last head makes its O triple ready
                     __threadfence();
-                    if (atom_acq_rel_gpu_add(counter(l, m, kOpAtt), 1) == kFHeads - 1) push(flow_item(kOpO, l, m, 0), 3);
+                    if (atom_acq_rel_gpu_add(counter(l, m, kOpAtt), 1) == kFHeads - 1) push(flow_item(kOpO, l, m, 0), 1);
                     K5_MARK(j, 6, gtimer());
                 }
                 ++g;
                 ++na;
                 continue;
             }
-            // ---- GEMM tile epilogue: bias (+ GELU | + residual), bf16, TMA stores.
+            // ---- GEMM tile epilogue: bias (+ GELU | + residual [+ LayerNorm]), bf16, TMA stores.
             const bool resid = op == kOpO || op == kOpF2;
             const uint64_t boff = lo + (op == kOpQkv ? a.l0.bqkv : op == kOpO ? a.l0.bo : op == kOpF1 ? a.l0.b1 : a.l0.b2);
             const int n0 = n * 256;
             epi_sync();  // the previous item's reads of bias_s / the boxes' scratch are done
             if (tid < 256) bias_s[tid] = *reinterpret_cast<const float*>(translate(a.arena, pt, boff + 4ull * (n0 + tid)));
             epi_sync();
-            const CUtensorMap* ym = op == kOpQkv ? &mp.y_qkv : op == kOpF1 ? &mp.y_f : &mp.y_t;
+            const CUtensorMap* ym = op == kOpQkv ? &mp.y_qkv : &mp.y_f;
             const CUtensorMap* rm = op == kOpF2 ? &mp.r_h : l == 0 ? &mp.r_in : &mp.r_x;
             const int rrow = (op == kOpO && l > 0) ? (l - 1) * a.xstride + m0 : m0;
-            if (resid && ht == 0) fence_proxy_async_global();  // residual rows written by other CTAs
+            if (resid) {
+                // The first chunk's residual box is loaded before the accumulator is ready, and the
+                // LayerNorm's gamma / beta lines are pulled into L1 while the MMAs run.
+                if (ht == 0) {
+                    fence_proxy_async_global();  // residual rows written by other CTAs
+                    bulk_wait_group_read<0>();   // this group's previous store has read the box
+                    mbar_arrive_expect_tx(&res_bar[gp], 8192);
+                    tma_tile2d_g2s(box, rm, n0 + gp * 32, rrow, &res_bar[gp]);
+                }
+                if (tid < 16) {
+                    const uint64_t lnp = lo + (op == kOpO ? (tid < 8 ? a.l0.ln1_g : a.l0.ln1_b) : (tid < 8 ? a.l0.ln2_g : a.l0.ln2_b));
+                    const char* pf = translate(a.arena, pt, lnp + 4ull * n0 + 128ull * (tid & 7));
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(pf));
+                }
+            }
             mbar_wait(&tfull_bar[b], tpar);
             tc_fence_after();
             if (tid == 0) K5_MARK(j, 5, gtimer());
-            float st_n = 0.f, st_mean = 0.f, st_m2 = 0.f;  // resid: this row's (count, mean, M2) over this thread's chunks
-#pragma unroll 1
-            for (int c = gp; c < 8; c += 4) {
-                if (ht == 0) bulk_wait_group_read<0>();  // this group's previous store has read the box
-                group_sync();
-                if (resid && ht == 0) {
+            float st_n = 0.f, st_mean = 0.f, st_m2 = 0.f;  // resid: this row's (count, mean, M2) over its chunks
+            uint32_t hold[2][16];                            // resid: the pre-LN bf16 pairs of both chunks
+#pragma unroll
+            for (int ci = 0; ci < 2; ++ci) {
+                const int c = gp + 4 * ci;
+                if (!resid || ci == 1) {
+                    if (ht == 0) bulk_wait_group_read<0>();  // this group's previous store has read the box
+                    group_sync();                            // (resid: every row read the first residual chunk)
+                }
+                if (resid && ci == 1 && ht == 0) {
                     mbar_arrive_expect_tx(&res_bar[gp], 8192);
                     tma_tile2d_g2s(box, rm, n0 + c * 32, rrow, &res_bar[gp]);
                 }
                 float v[32];
                 tmem_ld_32x32b_x32(acc + static_cast<uint32_t>(c * 32) + lane_off, v);
-                if (c + 4 >= 8) {  // last chunk of this thread: the accumulator is free for item j + 2
+                if (ci == 1) {  // the accumulator is free for item j + 2
                     tc_fence_before();
                     __syncwarp();
                     if (lane == 0) mbar_arrive(&tempty_bar[b]);
                 }
-                uint4 out[4];
-                __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(out);
                 const float* bc = bias_s + c * 32;
-                if (op == kOpF1) {
-#pragma unroll
-                    for (int k = 0; k < 16; ++k) o2[k] = __floats2bfloat162_rn(gelu(v[2 * k] + bc[2 * k]), gelu(v[2 * k + 1] + bc[2 * k + 1]));
-                } else if (resid) {
+                if (resid) {
+                    // t = bf16(acc + bias + resid) stays in registers; its row statistics feed the
+                    // LayerNorm (the values as the LayerNorm reads them).
                     mbar_wait(&res_bar[gp], e & 1);
                     ++e;
+                    float sm = 0.f;
 #pragma unroll
                     for (int u = 0; u < 4; ++u) {
-                        const uint4 w = *reinterpret_cast<const uint4*>(box + r * 64 + ((u ^ ((r >> 1) & 3)) << 4));
+                        const uint4 w = *reinterpret_cast<const uint4*>(box_chunk(u));
                         const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&w);
 #pragma unroll
                         for (int k = 0; k < 4; ++k) {
                             const int i = u * 8 + 2 * k;
                             const float2 f2 = __bfloat1622float2(h2[k]);
-                            o2[u * 4 + k] = __floats2bfloat162_rn(v[i] + bc[i] + f2.x, v[i + 1] + bc[i + 1] + f2.y);
+                            const __nv_bfloat162 x2 = __floats2bfloat162_rn(v[i] + bc[i] + f2.x, v[i + 1] + bc[i + 1] + f2.y);
+                            hold[ci][u * 4 + k] = *reinterpret_cast<const uint32_t*>(&x2);
+                            const float2 xf = __bfloat1622float2(x2);
+                            v[i] = xf.x, v[i + 1] = xf.y;
+                            sm += xf.x + xf.y;
                         }
-                    }
-                    // LayerNorm statistics of the bf16-rounded t values (as the LayerNorm reads them).
-                    float xs[32], sm = 0.f;
-#pragma unroll
-                    for (int k = 0; k < 16; ++k) {
-                        const float2 x = __bfloat1622float2(o2[k]);
-                        xs[2 * k] = x.x, xs[2 * k + 1] = x.y;
-                        sm += x.x + x.y;
                     }
                     const float mc = sm * (1.f / 32.f);
                     float mc2 = 0.f;
 #pragma unroll
-                    for (int k = 0; k < 32; ++k) mc2 = fmaf(xs[k] - mc, xs[k] - mc, mc2);
-                    if (st_n == 0.f)
+                    for (int k = 0; k < 32; ++k) mc2 = fmaf(v[k] - mc, v[k] - mc, mc2);
+                    if (ci == 0)
                         st_n = 32.f, st_mean = mc, st_m2 = mc2;
                     else
                         chan_combine(st_n, st_mean, st_m2, 32.f, mc, mc2);
+                    continue;
+                }
+                uint4 out[4];
+                __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(out);
+                if (op == kOpF1) {
+#pragma unroll
+                    for (int k = 0; k < 16; ++k) o2[k] = __floats2bfloat162_rn(gelu(v[2 * k] + bc[2 * k]), gelu(v[2 * k + 1] + bc[2 * k + 1]));
                 } else {
 #pragma unroll
                     for (int k = 0; k < 16; ++k) o2[k] = __floats2bfloat162_rn(v[2 * k] + bc[2 * k], v[2 * k + 1] + bc[2 * k + 1]);
                 }
-                if (resid) group_sync();  // every row's residual read before the box is overwritten
 #pragma unroll
-                for (int u = 0; u < 4; ++u) *reinterpret_cast<uint4*>(box + r * 64 + ((u ^ ((r >> 1) & 3)) << 4)) = out[u];
+                for (int u = 0; u < 4; ++u) *reinterpret_cast<uint4*>(box_chunk(u)) = out[u];
                 fence_proxy_async_smem();  // generic-proxy writes -> the TMA store reads
                 group_sync();
                 if (ht == 0) {
@@ -503,28 +548,31 @@ __global__ void __launch_bounds__(kFThreads, 1)
                 }
             }
             g += nk_of(op);
-            // ---- publish: this group's stores are complete (written, not just read).
-            if (ht == 0) {
-                bulk_wait_group<0>();
-                fence_proxy_async_global();
-            }
             if (!resid) {
+                // ---- publish: this group's stores complete, then the row block's counter.
+                if (ht == 0) {
+                    bulk_wait_group<0>();
+                    fence_proxy_async_global();
+                }
                 epi_sync();
-                if (tid == 0) {  // the row block's last QKV (FFN1) tile makes its heads (FFN2 tiles) ready
+                if (tid == 0) {  // the row block's last QKV (FFN1) tile makes its heads (FFN2 triple) ready
                     __threadfence();
                     const bool qkv = op == kOpQkv;
                     if (atom_acq_rel_gpu_add(counter(l, m, op), 1) == (qkv ? 9u : static_cast<uint32_t>(nf1)) - 1u)
-                        push(qkv ? flow_item(kOpAtt, l, m, 0) : flow_item(kOpF2, l, m, 0), qkv ? kFHeads : 3);
+                        push(qkv ? flow_item(kOpAtt, l, m, 0) : flow_item(kOpF2, l, m, 0), qkv ? 4 : 1);
                     K5_MARK(j, 6, gtimer());
                 }
                 continue;
             }
-            // Residual tile: this tile's per-row (mean, M2) over its 256 columns (four groups
-            // combined through the now idle staging boxes) for the row block's LayerNorm.
+            // ---- residual tile + LayerNorm. The row block's three column tiles are this cluster's
+            // three CTAs: each publishes its per-row (mean, M2) in global memory and signals its
+            // siblings (cluster-scope release on their mbarrier; two barriers alternate so a fast
+            // sibling's next statistics never land in a phase still being waited on).
             const bool ln1 = op == kOpO;
             float2* const stats = a.stats + ((static_cast<size_t>(l) * a.M + m) * 2 + (ln1 ? 0 : 1)) * 3 * 128;
             float2* part = reinterpret_cast<float2*>(boxes);  // [4 groups][128 rows]
-            epi_sync();
+            if (ht == 0) bulk_wait_group_read<0>();
+            epi_sync();  // residual boxes read, previous stores read: the boxes are scratch
             part[gp * 128 + r] = make_float2(st_mean, st_m2);
             epi_sync();
             if (gp == 0) {
@@ -533,79 +581,88 @@ __global__ void __launch_bounds__(kFThreads, 1)
                     const float2 p = part[k * 128 + r];
                     chan_combine(st_n, st_mean, st_m2, 64.f, p.x, p.y);
                 }
-                stats[n * 128 + r] = make_float2(st_mean, st_m2);
+                stats[rank * 128 + r] = make_float2(st_mean, st_m2);
             }
             epi_sync();
+            const int sb = nln & 1;
             if (tid == 0) {
-                __threadfence();
-                ln_flag = atom_acq_rel_gpu_add(counter(l, m, op), 1) == 2 ? 1u : 0u;
-                if (!ln_flag) K5_MARK(j, 6, gtimer());
+                fence_acq_rel_cluster();
+                for (uint32_t rr = 0; rr < kFCluster; ++rr) mbar_arrive_remote(&sib_bar[sb], rr);
             }
-            epi_sync();
-            if (!ln_flag) continue;
-            // ---- the row block's LayerNorm (this CTA completed its last residual tile): t -> h
-            // (LN1) or -> the layer output (LN2), three passes of 256 columns. Warp w: rows
-            // 8 w .. 8 w + 7; lane: 8 columns (512 contiguous bytes per warp and row). Each pass
-            // issues all its loads before using any: the L2 is loaded by the GEMMs' operand
-            // streams, so a pass costs one round trip.
+            mbar_wait_cluster(&sib_bar[sb], (nln >> 1) & 1);
+            ++nln;
+            float mean, rstd;
             {
-                if (tid == 0) K5_MARK(j, 7, gtimer());
-                // Lane 3 i + k (i < 8, k < 3): row 8 w + i's statistics of column tile k; lane i < 8
-                // then holds row 8 w + i's (mean, rstd).
-                const float2 pt3 = lane < 24 ? __ldcg(stats + (lane % 3) * 128 + warp * 8 + lane / 3) : make_float2(0.f, 0.f);
-                const int sl = 3 * (lane & 7);
-                float cnt = 256.f, mean = __shfl_sync(0xffffffffu, pt3.x, sl), m2 = __shfl_sync(0xffffffffu, pt3.y, sl);
+                float2 p = __ldcg(stats + r);
+                float cnt = 256.f;
+                mean = p.x;
+                float m2 = p.y;
 #pragma unroll
-                for (int k = 1; k < 3; ++k) {
-                    const float pm = __shfl_sync(0xffffffffu, pt3.x, sl + k), pq = __shfl_sync(0xffffffffu, pt3.y, sl + k);
-                    chan_combine(cnt, mean, m2, 256.f, pm, pq);
+                for (int k = 1; k < kFCluster; ++k) {
+                    p = __ldcg(stats + k * 128 + r);
+                    chan_combine(cnt, mean, m2, 256.f, p.x, p.y);
                 }
-                const float rstd_l = rsqrtf(m2 * (1.f / kFD) + 1e-12f);
-                const uint64_t go = lo + (ln1 ? a.l0.ln1_g : a.l0.ln2_g), bo = lo + (ln1 ? a.l0.ln1_b : a.l0.ln2_b);
-                const __nv_bfloat16* src = a.t + static_cast<size_t>(m0 + warp * 8) * kFD;
-                __nv_bfloat16* dst = (ln1 ? a.h : a.xout + static_cast<size_t>(l) * a.xstride * kFD) +
-                                     static_cast<size_t>(m0 + warp * 8) * kFD;
-#pragma unroll 1
-                for (int p3 = 0; p3 < 3; ++p3) {
-                    const int col = p3 * 256 + lane * 8;
-                    uint4 raw[8];
+                rstd = rsqrtf(m2 * (1.f / kFD) + 1e-12f);
+            }
+            if (tid == 0) K5_MARK(j, 7, gtimer());
+            const uint64_t go = lo + (ln1 ? a.l0.ln1_g : a.l0.ln2_g), bo = lo + (ln1 ? a.l0.ln1_b : a.l0.ln2_b);
+            const CUtensorMap* lm = ln1 ? &mp.y_h : &mp.y_x;
+            const int lrow = (ln1 ? 0 : l * a.xstride) + m0;
 #pragma unroll
-                    for (int rr = 0; rr < 8; ++rr) raw[rr] = __ldcg(reinterpret_cast<const uint4*>(src + rr * kFD + col));
-                    const float4* gam = reinterpret_cast<const float4*>(translate(a.arena, pt, go + 4ull * col));
-                    const float4* bet = reinterpret_cast<const float4*>(translate(a.arena, pt, bo + 4ull * col));
-                    const float4 g0 = __ldg(gam), g1 = __ldg(gam + 1), b0 = __ldg(bet), b1 = __ldg(bet + 1);
+            for (int ci = 0; ci < 2; ++ci) {
+                const int c = gp + 4 * ci;
+                if (ci == 1) {
+                    if (ht == 0) bulk_wait_group_read<0>();
+                    group_sync();
+                }
+                const float4* gam = reinterpret_cast<const float4*>(translate(a.arena, pt, go + 4ull * (n0 + c * 32)));
+                const float4* bet = reinterpret_cast<const float4*>(translate(a.arena, pt, bo + 4ull * (n0 + c * 32)));
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const float4 g0 = __ldg(gam + 2 * u), g1 = __ldg(gam + 2 * u + 1);
+                    const float4 b0 = __ldg(bet + 2 * u), b1 = __ldg(bet + 2 * u + 1);
                     const float gg[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
                     const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+                    uint4 o;
+                    uint32_t* o32 = reinterpret_cast<uint32_t*>(&o);
 #pragma unroll
-                    for (int rr = 0; rr < 8; ++rr) {
-                        const float mu = __shfl_sync(0xffffffffu, mean, rr), rs = __shfl_sync(0xffffffffu, rstd_l, rr);
-                        const __nv_bfloat162* h2 = reinterpret_cast<const __nv_bfloat162*>(&raw[rr]);
-                        uint4 u;
-                        __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(&u);
-#pragma unroll
-                        for (int k = 0; k < 4; ++k) {
-                            const float2 x = __bfloat1622float2(h2[k]);
-                            o2[k] = __floats2bfloat162_rn((x.x - mu) * rs * gg[2 * k] + bb[2 * k],
-                                                          (x.y - mu) * rs * gg[2 * k + 1] + bb[2 * k + 1]);
-                        }
-                        *reinterpret_cast<uint4*>(dst + rr * kFD + col) = u;
+                    for (int k = 0; k < 4; ++k) {
+                        const uint32_t pr = hold[ci][u * 4 + k];
+                        const float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&pr));
+                        const __nv_bfloat162 y2 = __floats2bfloat162_rn((x.x - mean) * rstd * gg[2 * k] + bb[2 * k],
+                                                                        (x.y - mean) * rstd * gg[2 * k + 1] + bb[2 * k + 1]);
+                        o32[k] = *reinterpret_cast<const uint32_t*>(&y2);
                     }
+                    *reinterpret_cast<uint4*>(box_chunk(u)) = o;
                 }
-                epi_sync();
-                if (tid == 0) {  // LN1 makes the row block's FFN1 tiles ready, LN2 the next layer's QKV tiles
-                    __threadfence();
+                fence_proxy_async_smem();
+                group_sync();
+                if (ht == 0) {
+                    tma_tile2d_s2g(lm, n0 + c * 32, lrow, box);
+                    bulk_commit_group();
+                }
+            }
+            if (ht == 0) {
+                bulk_wait_group<0>();
+                fence_proxy_async_global();
+            }
+            epi_sync();
+            if (tid == 0) {  // LN1 makes the row block's FFN1 triples ready, LN2 the next layer's QKV triples
+                __threadfence();
+                if (atom_acq_rel_gpu_add(counter(l, m, op), 1) == kFCluster - 1) {
                     if (ln1)
-                        push(flow_item(kOpF1, l, m, 0), nf1);
+                        push(flow_item(kOpF1, l, m, 0), nf1 / 3);
                     else if (l + 1 < a.L)
-                        push(flow_item(kOpQkv, l + 1, m, 0), 9);
-                    K5_MARK(j, 6, gtimer());
+                        push(flow_item(kOpQkv, l + 1, m, 0), 3);
                 }
+                K5_MARK(j, 6, gtimer());
             }
         }
         if (ht == 0) bulk_wait_group<0>();
     }
     tc_fence_before();
     __syncthreads();
+    cluster_sync();  // no remote arrive may target an exited CTA
     tc_fence_after();
     if (warp == kFMmaWarp) tmem_dealloc<512>(tmem);
 }
@@ -620,10 +677,39 @@ bool encode_or_throw(CUtensorMap* map, const void* base, uint64_t inner, uint64_
     return true;
 }
 
+// Co-resident 3-CTA clusters of the kernel on this device (every CTA must be resident:
+// CTAs of one cluster wait for each other). Cached per device.
+int flow_clusters() {
+    static std::mutex mu;
+    static std::map<int, int> cache;
+    const int dev = current_device();
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cache.find(dev);
+    if (it != cache.end()) return it->second;
+    ensure_max_dynamic_smem(reinterpret_cast<const void*>(encoder_flow_kernel), static_cast<int>(kFSmem));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(kFCluster * 64);
+    cfg.blockDim = dim3(kFThreads);
+    cfg.dynamicSmemBytes = kFSmem;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kFCluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    int n = 0;
+    GFX_CUDA(cudaOccupancyMaxActiveClusters(&n, encoder_flow_kernel, &cfg));
+    n = std::min(n, device_sm_count(dev) / static_cast<int>(kFCluster));
+    if (n < 1) throw std::runtime_error("encoder flow: no 3-CTA cluster fits on this device");
+    cache[dev] = n;
+    return n;
+}
+
 }  // namespace
 
 bool bert_flow_supported(const BertLayout& lay, int batch) {
-    if (lay.d != kFD || lay.heads != kFHeads || lay.seq != kFSeq || lay.ffn % 256 || lay.L < 1 || lay.L > 31) return false;
+    if (lay.d != kFD || lay.heads != kFHeads || lay.seq != kFSeq || lay.ffn % 768 || lay.L < 1 || lay.L > 31) return false;
     if (batch < 1 || batch > 4095) return false;
     // Layer l's parameters must sit at layer 0's offsets + l * stride (bert_layout's periodic blob).
     const uint64_t stride = lay.L > 1 ? lay.layer[1].wqkv - lay.layer[0].wqkv : 0;
@@ -643,10 +729,11 @@ int bert_encoder_flow(const char* arena, const PageTable& pt, const BertLayout& 
                       const __nv_bfloat16* in, __nv_bfloat16* xout, int xstride, BertWorkspace& ws, cudaStream_t s) {
     if (!bert_flow_supported(lay, batch)) throw std::runtime_error("encoder flow: unsupported BERT shape");
     const int T = batch * kFSeq, M = batch, L = lay.L, F = lay.ffn;
-    const int dev = current_device();
-    const int ctas = device_sm_count(dev);
+    const int clusters = flow_clusters();
+    const int ctas = clusters * static_cast<int>(kFCluster);
     // Queue slots, counters and LayerNorm statistics (sized per shape in the workspace).
-    const int n_items = L * M * (9 + kFHeads + 3 + F / 256 + 3);
+    // Cluster items per (layer, row block): 3 QKV, 4 attention, 1 O, ffn / 768 FFN1, 1 FFN2.
+    const int n_items = L * M * (3 + 4 + 1 + F / 768 + 1);
     if (ws.flow_L != L || ws.flow_M != M || ws.flow_F != F) {
         if (ws.flow_items) GFX_CUDA(cudaFree(ws.flow_items));
         if (ws.flow_cnt) GFX_CUDA(cudaFree(ws.flow_cnt));
@@ -671,7 +758,8 @@ int bert_encoder_flow(const char* arena, const PageTable& pt, const BertLayout& 
     encode_or_throw(&mp.qkv, ws.qkv, 3 * kFD, T, 64, k128, "qkv");
     encode_or_throw(&mp.y_qkv, ws.qkv, 3 * kFD, T, 32, k64, "qkv out");
     encode_or_throw(&mp.y_f, ws.f, F, T, 32, k64, "f out");
-    encode_or_throw(&mp.y_t, ws.t, kFD, T, 32, k64, "t out");
+    encode_or_throw(&mp.y_h, ws.h, kFD, T, 32, k64, "h out");
+    encode_or_throw(&mp.y_x, xout, kFD, xrows, 32, k64, "layer out");
     encode_or_throw(&mp.r_in, in, kFD, T, 32, k64, "input resid");
     encode_or_throw(&mp.r_x, xout, kFD, xrows, 32, k64, "layer input resid");
     encode_or_throw(&mp.r_h, ws.h, kFD, T, 32, k64, "h resid");
@@ -682,10 +770,9 @@ int bert_encoder_flow(const char* arena, const PageTable& pt, const BertLayout& 
     fa.cnt = ws.flow_cnt;
     fa.slots = ws.flow_cnt + static_cast<size_t>(L) * M * kCSlots + 2;
     fa.n_items = n_items;
-    fa.n_first = 9 * M;
+    fa.n_first = 3 * M;
     fa.ctx = ws.ctx;
     fa.h = ws.h;
-    fa.t = ws.t;
     fa.xout = xout;
     fa.stats = static_cast<float2*>(ws.flow_stats);
     fa.M = M;
@@ -706,8 +793,19 @@ int bert_encoder_flow(const char* arena, const PageTable& pt, const BertLayout& 
 #endif
     GFX_CUDA(cudaMemsetAsync(ws.flow_cnt, 0, ws.flow_cnt_words * 4, s));
     ensure_max_dynamic_smem(reinterpret_cast<const void*>(encoder_flow_kernel), static_cast<int>(kFSmem));
-    encoder_flow_kernel<<<ctas, kFThreads, kFSmem, s>>>(mp, fa);
-    GFX_CUDA(cudaGetLastError());
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(ctas));
+    cfg.blockDim = dim3(kFThreads);
+    cfg.dynamicSmemBytes = kFSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kFCluster;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    GFX_CUDA(cudaLaunchKernelEx(&cfg, encoder_flow_kernel, mp, fa));
 #ifdef GFX_K5_DEBUG
     if (tracing) {
         std::vector<unsigned long long> v(trace_words);
