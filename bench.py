@@ -44,7 +44,7 @@ DATA = os.path.join(ROOT, "paper_2303_05601_b200", "data")
 sys.path.insert(0, ROOT)
 
 METRIC = "trace-replay requests/sec + p50/p99 latency at 1/2/4/8 B200; cache hit rate"
-H2D_PEAK_GBS = 55.4       # measured pinned H2D, 1 GiB copies on this pool (profiles/r1_k1_v6.md, tools/h2d_rate.cu)
+H2D_PEAK_GBS = 55.4       # measured pinned H2D, 1 GiB in 64 MB copies on this pool (tools/h2d_rate.cu, profiles/r2_h2d_rate.txt)
 HOST_LINK_NOMINAL = 64.0  # PCIe Gen5 x16 per direction, nominal
 NVLINK_PEER_GBS = 770.0   # measured peer copy per direction on this pool (B200_PROFILING.md)
 REF_SAMPLE_EVERY = 50     # reference arm: every 50th request of the step is inferred on the CPU (39 of 1950)

@@ -578,9 +578,14 @@ constexpr int kS = 128, kDh = 64;
 constexpr uint32_t kAttnSmem = 3 * 16384 + 1024;  // Q, K, V; P overlays Q + K once S is computed
 
 
-__global__ void __launch_bounds__(128, 4) attention_tc_kernel(const __grid_constant__ CUtensorMap tmap_qkv,
-                                                           __nv_bfloat16* __restrict__ ctx, int heads,
-                                                           unsigned long long* span) {
+// 8 warps: warp w owns TMEM lane quarter w & 3 (query rows 32 (w & 3) ..) and key
+// half w >> 2 (keys 64 (w >> 2) .. + 63, i.e. P block w >> 2): each thread takes
+// half a row, the two halves exchange their row max and sum through shared
+// memory (a 4-warp version, one thread per row, ran ~9.7 µs per layer).
+constexpr int kAttnThreads = 256;
+__global__ void __launch_bounds__(kAttnThreads, 4) attention_tc_kernel(const __grid_constant__ CUtensorMap tmap_qkv,
+                                                                    __nv_bfloat16* __restrict__ ctx, int heads,
+                                                                    unsigned long long* span) {
     K2_SPAN_BEGIN(span);
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -590,9 +595,11 @@ __global__ void __launch_bounds__(128, 4) attention_tc_kernel(const __grid_const
     uint8_t* ps = sm;  // P (keys 0-63 block, keys 64-127 block) over Q and K: dead after the S MMAs
     __shared__ __align__(8) uint64_t ld_bar, s_bar, o_bar;
     __shared__ uint32_t tmem_s;
+    __shared__ float red_max[2][kS], red_sum[2][kS];
     const int seq = blockIdx.x / heads, h = blockIdx.x % heads;
     const int d = heads * kDh;
-    const int tid = threadIdx.x, warp = tid >> 5;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int q = warp & 3, hf = warp >> 2, r = q * 32 + lane;
     if (tid == 0) {
         mbar_init(&ld_bar, 1);
         mbar_init(&s_bar, 1);
@@ -620,45 +627,43 @@ __global__ void __launch_bounds__(128, 4) attention_tc_kernel(const __grid_const
         umma_commit(&s_bar);
     }
     pdl_trigger();
-    // Softmax: thread = query row = TMEM lane (warp w owns lanes 32w..32w+31).
     mbar_wait(&s_bar, 0);
     tc_fence_after();
-    const uint32_t lane_base = tmem + (static_cast<uint32_t>(warp * 32) << 16);
-    // Two passes over the row's 128 TMEM columns in 32-column chunks (row max,
-    // then exp / sum / bf16 P), so a thread holds 32 scores, not 128: registers
-    // for four CTAs per SM.
+    const uint32_t row_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(hf * 64);
     float mx = -INFINITY;
 #pragma unroll
-    for (int c = 0; c < kS / 32; ++c) {
+    for (int c = 0; c < 2; ++c) {
         float part[32];
-        tmem_ld_32x32b_x32(lane_base + static_cast<uint32_t>(c * 32), part);
+        tmem_ld_32x32b_x32(row_base + static_cast<uint32_t>(c * 32), part);
 #pragma unroll
         for (int j = 0; j < 32; ++j) mx = fmaxf(mx, part[j]);
     }
-    constexpr float kScaleLog2 = 0.125f * 1.4426950408889634f;  // 1/sqrt(64) * log2(e)
-    const float off = mx * kScaleLog2;
+    red_max[hf][r] = mx;
+    __syncthreads();
+    mx = fmaxf(red_max[0][r], red_max[1][r]);
+    const float off = mx * kAttnScaleLog2;
     float sum = 0.f;
-    const int r = tid;
+    uint8_t* pb = ps + hf * 16384;  // this half's 64 keys = P block hf
 #pragma unroll
-    for (int c32 = 0; c32 < kS / 32; ++c32) {
+    for (int c32 = 0; c32 < 2; ++c32) {
         float part[32];
-        tmem_ld_32x32b_x32(lane_base + static_cast<uint32_t>(c32 * 32), part);
+        tmem_ld_32x32b_x32(row_base + static_cast<uint32_t>(c32 * 32), part);
 #pragma unroll
         for (int q8 = 0; q8 < 4; ++q8) {  // 16-byte chunks of 8 keys
-            const int c = c32 * 4 + q8;
+            const int cc = c32 * 4 + q8;
             uint4 u;
             __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const float p0 = ex2_approx(fmaf(part[q8 * 8 + 2 * j], kScaleLog2, -off));
-                const float p1 = ex2_approx(fmaf(part[q8 * 8 + 2 * j + 1], kScaleLog2, -off));
+                const float p0 = ex2_approx(fmaf(part[q8 * 8 + 2 * j], kAttnScaleLog2, -off));
+                const float p1 = ex2_approx(fmaf(part[q8 * 8 + 2 * j + 1], kAttnScaleLog2, -off));
                 sum += p0 + p1;
                 h2[j] = __floats2bfloat162_rn(p0, p1);
             }
-            const int blk = c >> 3, cc = c & 7;
-            *reinterpret_cast<uint4*>(ps + blk * 16384 + r * 128 + ((cc ^ (r & 7)) << 4)) = u;
+            *reinterpret_cast<uint4*>(pb + r * 128 + ((cc ^ (r & 7)) << 4)) = u;
         }
     }
+    red_sum[hf][r] = sum;
     fence_proxy_async_smem();  // P (generic-proxy writes) -> the PV MMA reads
     tc_fence_before();
     __syncthreads();
@@ -675,20 +680,12 @@ __global__ void __launch_bounds__(128, 4) attention_tc_kernel(const __grid_const
     }
     mbar_wait(&o_bar, 0);
     tc_fence_after();
-    float o[kDh];
-    {
-        float part[32];
-        tmem_ld_32x32b_x32(lane_base, part);
+    float o[32];  // this half's 32 output dims of row r
+    tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(hf * 32), o);
+    const float inv = 1.0f / (red_sum[0][r] + red_sum[1][r]);
+    uint4* dst = reinterpret_cast<uint4*>(ctx + (static_cast<size_t>(seq) * kS + r) * d + h * kDh + hf * 32);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) o[j] = part[j];
-        tmem_ld_32x32b_x32(lane_base + 32, part);
-#pragma unroll
-        for (int j = 0; j < 32; ++j) o[32 + j] = part[j];
-    }
-    const float inv = 1.0f / sum;
-    uint4* dst = reinterpret_cast<uint4*>(ctx + (static_cast<size_t>(seq) * kS + r) * d + h * kDh);
-#pragma unroll
-    for (int c = 0; c < kDh / 8; ++c) {
+    for (int c = 0; c < 4; ++c) {
         uint4 u;
         __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
 #pragma unroll
@@ -1158,7 +1155,7 @@ int bert_forward(const char* arena, const PageTable& pt, const BertLayout& lay, 
                                       CU_TENSOR_MAP_SWIZZLE_128B))
                 throw CudaError("cuTensorMapEncodeTiled failed (attention)");
             ensure_max_dynamic_smem(reinterpret_cast<const void*>(attention_tc_kernel), static_cast<int>(kAttnSmem));
-            launch_pdl(attention_tc_kernel, dim3(batch * lay.heads), dim3(128), kAttnSmem, s, true, tq, ws.ctx, lay.heads,
+            launch_pdl(attention_tc_kernel, dim3(batch * lay.heads), dim3(kAttnThreads), kAttnSmem, s, true, tq, ws.ctx, lay.heads,
                        next_span("attention"));
         }
         gemm_resid_ln(arena, pt, o.wo, o.bo, o.ln1_g, o.ln1_b, ws.ctx, ws.h, x, ws.t, T, d, d, s, true, ws.gemm_pair);
