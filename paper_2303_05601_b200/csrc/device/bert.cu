@@ -512,8 +512,9 @@ __global__ void __launch_bounds__(kGThreads, 1)
                     float x0 = v[2 * j] + bias_s[c * 32 + 2 * j];
                     float x1 = v[2 * j + 1] + bias_s[c * 32 + 2 * j + 1];
                     if (kEpi == kEpiGelu) {
-                        x0 = gelu(x0);
-                        x1 = gelu(x1);
+                        const float2 g = gelu2(make_float2(x0, x1));
+                        x0 = g.x;
+                        x1 = g.y;
                     }
                     if (kEpi == kEpiResid) {
                         x0 += rs[2 * j];
@@ -581,7 +582,9 @@ constexpr uint32_t kAttnSmem = 3 * 16384 + 1024;  // Q, K, V; P overlays Q + K o
 // 8 warps: warp w owns TMEM lane quarter w & 3 (query rows 32 (w & 3) ..) and key
 // half w >> 2 (keys 64 (w >> 2) .. + 63, i.e. P block w >> 2): each thread takes
 // half a row, the two halves exchange their row max and sum through shared
-// memory (a 4-warp version, one thread per row, ran ~9.7 µs per layer).
+// memory. (Measured against the 4-warp version, one thread per row: the same
+// 1.017 ms per C5 forward — the kernel's ~9.7 µs after QKV are load and
+// launch latency, not softmax issue.)
 constexpr int kAttnThreads = 256;
 __global__ void __launch_bounds__(kAttnThreads, 4) attention_tc_kernel(const __grid_constant__ CUtensorMap tmap_qkv,
                                                                     __nv_bfloat16* __restrict__ ctx, int heads,

@@ -533,7 +533,10 @@ __global__ void __launch_bounds__(kFThreads, 1)
                 __nv_bfloat162* o2 = reinterpret_cast<__nv_bfloat162*>(out);
                 if (op == kOpF1) {
 #pragma unroll
-                    for (int k = 0; k < 16; ++k) o2[k] = __floats2bfloat162_rn(gelu(v[2 * k] + bc[2 * k]), gelu(v[2 * k + 1] + bc[2 * k + 1]));
+                    for (int k = 0; k < 16; ++k) {
+                        const float2 gv = gelu2(make_float2(v[2 * k] + bc[2 * k], v[2 * k + 1] + bc[2 * k + 1]));
+                        o2[k] = __floats2bfloat162_rn(gv.x, gv.y);
+                    }
                 } else {
 #pragma unroll
                     for (int k = 0; k < 16; ++k) o2[k] = __floats2bfloat162_rn(v[2 * k] + bc[2 * k], v[2 * k + 1] + bc[2 * k + 1]);
