@@ -36,8 +36,8 @@ run_task() {
   k1)
     timeout 300 python tools/k1_bench.py 300 0,3,7,12,15,16,18,21 2>&1 | tail -12 ;;
   bert)
-    timeout 300 python tools/bert_bench.py 50 0
-    timeout 300 python tools/bert_bench.py 50 1
+    timeout 300 python tools/bert_bench.py 50 perop
+    timeout 300 python tools/bert_bench.py 50 pair
     timeout 300 python tools/cublas_bert.py 50 ;;
   launches)
     timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none \
@@ -49,10 +49,10 @@ run_task() {
     echo "rc=$?" ;;
   ncu-bert)
     timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed \
-      --clock-control none -s 130 -c 61 --csv --log-file gpurun_out/bert_launches.csv python tools/bert_bench.py 2 0 > /dev/null 2>&1
+      --clock-control none -s 130 -c 61 --csv --log-file gpurun_out/bert_launches.csv python tools/bert_bench.py 2 perop > /dev/null 2>&1
     echo "list rc=$?"
     timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"gemm_bf16|attention" -s 130 -c 5 \
-      -o gpurun_out/bert_full -f python tools/bert_bench.py 2 0
+      -o gpurun_out/bert_full -f python tools/bert_bench.py 2 perop
     echo "full rc=$?" ;;
   sanitize)
     for tool in memcheck synccheck racecheck; do
