@@ -118,10 +118,11 @@ constexpr int kGEpiWarps = 16, kGAWarp = 16, kGMmaWarp = 17, kGBWarp0 = 18;
 constexpr uint32_t kGATile = 128 * 128;  // A: 128 rows x 64 bf16 (16 KB)
 constexpr uint32_t kGSmem = 192 * 1024;  // stage ring budget
 
-// kEpiResidLN: bias + residual + the post-LN LayerNorm of the whole d = 768 row,
-// fused (K4 disappears from the forward). The row's three 256-column tiles are
-// computed by the three CTAs of a cluster; each CTA reduces its tile's per-row
-// (mean, M2) and sends it to all three CTAs by st.async into their shared
+// kEpiResidLN: bias + residual + the post-LN LayerNorm of the whole d-wide row,
+// fused (K4 disappears from the forward). The row's d / 256 column tiles (3 for
+// BERT-base, 4 for BERT-large) are computed by the CTAs of one cluster; each
+// CTA reduces its tile's per-row (mean, M2) and sends it to every CTA of the
+// cluster by st.async into their shared
 // memory (DSMEM, completing a tx-counted mbarrier), so the statistics never
 // touch global memory and no CTA waits on a flag in L2. One tile per CTA (the
 // host falls back to kEpiResid + layernorm_kernel when the row blocks exceed
@@ -208,9 +209,9 @@ __global__ void __launch_bounds__(kGThreads, 1)
         for (int g = 0; g < 4; ++g) mbar_init(&res_bar[g], 1);
         if (kLN) mbar_init(&stat_bar, 1);
         mbar_fence_init();
-        // 3 senders x 128 rows x (mean, M2); remote bytes may land before this
-        // CTA's epilogue runs, never before the cluster_sync below.
-        if (kLN) mbar_arrive_expect_tx(&stat_bar, 3 * 128 * 8);
+        // n_tiles senders x 128 rows x (mean, M2); remote bytes may land before
+        // this CTA's epilogue runs, never before the cluster_sync below.
+        if (kLN) mbar_arrive_expect_tx(&stat_bar, static_cast<uint32_t>(n_tiles) * 128 * 8);
         tma_prefetch_desc(&tmap_x);
         tma_prefetch_desc(&tmap_y);
         if (kEpi == kEpiResid || kLN) tma_prefetch_desc(&tmap_r);
@@ -330,7 +331,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
         }
     } else if constexpr (kLN) {
         // Fused residual + LayerNorm epilogue (one 128 x 256 tile per CTA, the
-        // cluster's three CTAs hold the row's three column tiles). Thread = row
+        // cluster's n_tiles = d / 256 CTAs hold the row's column tiles). Thread = row
         // r (TMEM lane), group gp = column chunks gp and gp + 4 (32 each).
         // t1 = bf16(acc + bias + resid) stays in registers as bf16 pairs; the
         // row's (mean, M2) is reduced over chunks (registers), groups (shared
@@ -345,7 +346,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
         float* gam_s = reinterpret_cast<float*>(smem + kGSmem);
         float* bet_s = gam_s + kBN;
         float2* part = reinterpret_cast<float2*>(smem + kGSmem + 4096);   // [4 groups][128 rows]
-        float2* xbuf = reinterpret_cast<float2*>(smem + kGSmem + 8192);   // [3 CTAs][128 rows]
+        float2* xbuf = reinterpret_cast<float2*>(smem + kGSmem + 8192);   // [<= 8 CTAs][128 rows]
         const int t = t_first;
         const int m0 = tile_m0(t), n0 = (t % n_tiles) * kBN;
         for (int c = tid; c < kBN; c += kGEpiWarps * 32) {
@@ -407,7 +408,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
             }
             const uint32_t my = static_cast<uint32_t>(t % n_tiles);
 #pragma unroll
-            for (uint32_t dst = 0; dst < 3; ++dst)
+            for (uint32_t dst = 0; dst < static_cast<uint32_t>(n_tiles); ++dst)
                 st_async_v2f32(mapa_u32(&xbuf[my * 128 + r], dst), mean, m2, mapa_u32(&stat_bar, dst));
         }
         if (tid == 0) K2_MARK(8);
@@ -419,13 +420,12 @@ __global__ void __launch_bounds__(kGThreads, 1)
             float n_r = 256.f;
             mean = p.x;
             m2 = p.y;
-#pragma unroll
-            for (int k = 1; k < 3; ++k) {
+            for (int k = 1; k < n_tiles; ++k) {
                 p = xbuf[k * 128 + r];
                 chan_combine(n_r, mean, m2, 256.f, p.x, p.y);
             }
         }
-        const float rstd = rsqrtf(m2 * (1.f / 768.f) + 1e-12f);
+        const float rstd = rsqrtf(m2 * (1.f / static_cast<float>(a.N)) + 1e-12f);
 #pragma unroll
         for (int j = 0; j < 2; ++j) {
             const int c = gp + 4 * j;
@@ -796,12 +796,13 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const __nv_bfloat16* __r
 // each); the [CLS] rows are staged in shared memory once per block; each lane
 // holds 3 16-byte chunks of its warp's weight row in registers (swizzled blob
 // tile layout, one page translation per chunk).
+template <int kD>
 __global__ void __launch_bounds__(256) pooler_kernel(const __nv_bfloat16* __restrict__ x, float* __restrict__ out,
                                                      const char* arena, const __grid_constant__ PageTable ptab,
                                                      uint64_t w_off, uint64_t b_off, int d, int seq, int batch,
                                                      unsigned long long* span) {
     K2_SPAN_BEGIN(span);
-    constexpr int kD = 768, kChunks = kD / 8 / 32;  // 16-byte chunks per lane
+    constexpr int kChunks = kD / 8 / 32;  // 16-byte chunks per lane
     extern __shared__ __align__(16) uint8_t cls_raw[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int n = blockIdx.x * 8 + warp;
@@ -935,7 +936,7 @@ void gemm_bn(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_
         attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
         attr[0].val.programmaticStreamSerializationAllowed = pdl ? 1 : 0;
         attr[1].id = cudaLaunchAttributeClusterDimension;
-        attr[1].val.clusterDim.x = kPair ? 2 : 3;
+        attr[1].val.clusterDim.x = kPair ? 2u : static_cast<unsigned>(N / kBN);
         attr[1].val.clusterDim.y = 1;
         attr[1].val.clusterDim.z = 1;
         cfg.attrs = attr;
@@ -995,30 +996,30 @@ void gemm(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_off
 // epilogue when every 128-row block gets its own resident 3-CTA cluster
 // (T <= 128 x max active clusters; 4096 tokens = 32 clusters); otherwise the
 // residual GEMM and layernorm_kernel (via `t`).
-int ln_max_clusters() {
+int ln_max_clusters(int nc) {
     static std::mutex mu;
-    static std::map<int, int> cache;
+    static std::map<std::pair<int, int>, int> cache;
     const int dev = current_device();
     std::lock_guard<std::mutex> lk(mu);
-    auto it = cache.find(dev);
+    auto it = cache.find({dev, nc});
     if (it != cache.end()) return it->second;
     auto k = gemm_bf16_kernel<kEpiResidLN, 256, false>;
     const size_t smem = kGSmem + 4 * 8192 + 1024;
     ensure_max_dynamic_smem(reinterpret_cast<const void*>(k), static_cast<int>(smem));
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(3 * 64);
+    cfg.gridDim = dim3(static_cast<unsigned>(nc * 32));
     cfg.blockDim = dim3(kGThreads);
     cfg.dynamicSmemBytes = smem;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 3;
+    attr[0].val.clusterDim.x = static_cast<unsigned>(nc);
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     int n = 0;
     GFX_CUDA(cudaOccupancyMaxActiveClusters(&n, k, &cfg));
-    cache[dev] = n;
+    cache[{dev, nc}] = n;
     return n;
 }
 
@@ -1026,7 +1027,7 @@ bool ln_fusable(int T, int N) {
 #ifdef GFX_K2_DEBUG
     if (std::getenv("GFX_K2_NOLN")) return false;  // debug A/B only
 #endif
-    return N == 768 && T % kGM == 0 && T / kGM <= ln_max_clusters();
+    return N % 256 == 0 && N / 256 >= 2 && N / 256 <= 8 && T % kGM == 0 && T / kGM <= ln_max_clusters(N / 256);
 }
 
 void gemm_resid_ln(const char* arena, const PageTable& pt, uint64_t w_off, uint64_t b_off, uint64_t g_off,
@@ -1038,8 +1039,10 @@ void gemm_resid_ln(const char* arena, const PageTable& pt, uint64_t w_off, uint6
         return;
     }
     gemm<kEpiResid>(arena, pt, w_off, b_off, x, t, resid, T, K, N, s, pdl, pair);
-    launch_pdl(layernorm_kernel<768>, dim3((T + 15) / 16), dim3(256), 0, s, true, static_cast<const __nv_bfloat16*>(t),
-               y, arena, pt, g_off, be_off, T, next_span("layernorm"));
+    auto ln = N == 512 ? layernorm_kernel<512> : N == 1024 ? layernorm_kernel<1024> : layernorm_kernel<768>;
+    if (N != 512 && N != 768 && N != 1024) throw std::runtime_error("bert layernorm: d must be 512, 768 or 1024");
+    launch_pdl(ln, dim3((T + 15) / 16), dim3(256), 0, s, true, static_cast<const __nv_bfloat16*>(t), y, arena, pt, g_off,
+               be_off, T, next_span("layernorm"));
 }
 
 }  // namespace
@@ -1121,8 +1124,8 @@ void BertWorkspace::release() {
 int bert_forward(const char* arena, const PageTable& pt, const BertLayout& lay, int batch, const __nv_bfloat16* in,
                  float* out, BertWorkspace& ws, cudaStream_t s, __nv_bfloat16* hidden) {
     const int d = lay.d, T = batch * lay.seq;
-    if (lay.seq != kS || d / lay.heads != kDh || d != 768)
-        throw std::runtime_error("bert: this build serves seq 128, d_head 64, d 768");
+    if (lay.seq != kS || d / lay.heads != kDh || d % lay.heads || (d != 512 && d != 768 && d != 1024))
+        throw std::runtime_error("bert: this build serves seq 128, d_head 64, d 512 / 768 / 1024");
     ws.ensure(T, d, lay.ffn);
     int launches = 0;
 #ifdef GFX_K2_DEBUG
@@ -1171,12 +1174,13 @@ int bert_forward(const char* arena, const PageTable& pt, const BertLayout& lay, 
             GFX_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(hidden) + (l + 1) * hbytes, ws.x, hbytes,
                                      cudaMemcpyDeviceToDevice, s));
     }
-    if (d != 768 || static_cast<size_t>(batch) * d * 2 > 160 * 1024)
-        throw std::runtime_error("bert pooler: d = 768 and at most 106 sequences per request");
-    ensure_max_dynamic_smem(reinterpret_cast<const void*>(pooler_kernel), 160 * 1024);
-    launch_pdl(pooler_kernel, dim3((d + 7) / 8), dim3(256), static_cast<size_t>(batch) * d * 2, s, !hidden,
-               static_cast<const __nv_bfloat16*>(x), out,
-               arena, pt, lay.wp, lay.bp, d, lay.seq, batch, next_span("pooler"));
+    if (static_cast<size_t>(batch) * d * 2 > 160 * 1024)
+        throw std::runtime_error("bert pooler: at most 160 KB of [CLS] rows per request (106 sequences at d = 768)");
+    auto pool = d == 512 ? pooler_kernel<512> : d == 1024 ? pooler_kernel<1024> : pooler_kernel<768>;
+    ensure_max_dynamic_smem(reinterpret_cast<const void*>(pool), 160 * 1024);
+    launch_pdl(pool, dim3((d + 7) / 8), dim3(256), static_cast<size_t>(batch) * d * 2, s, !hidden,
+               static_cast<const __nv_bfloat16*>(x), out, arena, pt, lay.wp, lay.bp, d, lay.seq, batch,
+               next_span("pooler"));
 #ifdef GFX_K2_DEBUG
     if (g_span.on) {
         std::vector<unsigned long long> v(2 * g_span.names.size());

@@ -67,12 +67,12 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / np.linalg.norm(b))
 
 
-def run_gpu(gfx, idx, layers, seqs, seed, request_id=7, debug=True, mode="perop"):
-    desc = gfx.models.bert_desc(layers, seqs, seed)
+def run_gpu(gfx, idx, layers, seqs, seed, request_id=7, debug=True, mode="perop", d=D, ffn=3072):
+    desc = gfx.models.bert_desc(layers, seqs, seed, d=d, heads=d // 64, ffn=ffn)
     gfx.check(gfx._ffi.gfx_model_register(idx, C.byref(desc)))
     inb, outb = C.c_uint64(), C.c_uint64()
     gfx.check(gfx._ffi.gfx_model_io_bytes(idx, C.byref(inb), C.byref(outb)))
-    assert inb.value == seqs * SEQ * D * 2 and outb.value == seqs * D * 4
+    assert inb.value == seqs * SEQ * d * 2 and outb.value == seqs * d * 4
     pages = C.c_int32()
     gfx.check(gfx._ffi.gfx_model_pages(idx, C.byref(pages)))
     a = C.c_void_p()
@@ -90,7 +90,7 @@ def run_gpu(gfx, idx, layers, seqs, seed, request_id=7, debug=True, mode="perop"
         gfx.check(gfx._ffi.gfx_memcpy_h2d(a, xd, x_bits.ctypes.data, inb.value))
         gfx.check(gfx._ffi.gfx_load_h2d(a, idx, None))
         gfx.check(gfx._ffi.gfx_infer(a, idx, xd, yd, seqs, None))  # production (PDL-chained) path
-        pooled = np.zeros((seqs, D), np.float32)
+        pooled = np.zeros((seqs, d), np.float32)
         gfx.check(gfx._ffi.gfx_memcpy_d2h(a, pooled.ctypes.data, yd, outb.value))
         gfx.check(gfx._ffi.gfx_infer(a, idx, xd, yd, seqs, None))
         again = np.zeros_like(pooled)
@@ -98,7 +98,7 @@ def run_gpu(gfx, idx, layers, seqs, seed, request_id=7, debug=True, mode="perop"
         hidden = None
         if debug:
             gfx.check(gfx._ffi.gfx_infer_debug(a, idx, xd, yd, seqs, hd))
-            hidden = np.zeros((layers + 1, seqs * SEQ * D), np.uint16)
+            hidden = np.zeros((layers + 1, seqs * SEQ * d), np.uint16)
             gfx.check(gfx._ffi.gfx_memcpy_d2h(a, hidden.ctypes.data, hd, hbytes))
             dbg = np.zeros_like(pooled)
             gfx.check(gfx._ffi.gfx_memcpy_d2h(a, dbg.ctypes.data, yd, outb.value))
@@ -143,18 +143,18 @@ def test_bert_one_layer_end_to_end(gfx, olib):
     assert rel(pooled, want) <= TOL
 
 
-def teacher_forced(olib, seed, layers, seqs, hidden, pooled, check_layers=None):
+def teacher_forced(olib, seed, layers, seqs, hidden, pooled, check_layers=None, d=D, ffn=3072):
     threads = os.cpu_count() or 1
     worst = 0.0
     for l in (range(layers) if check_layers is None else check_layers):
         want = np.zeros_like(hidden[l])
-        assert olib.orc_bert_layer(seed, l, D, 12, 3072, SEQ, seqs, hidden[l].ctypes.data, want.ctypes.data,
+        assert olib.orc_bert_layer(seed, l, d, d // 64, ffn, SEQ, seqs, hidden[l].ctypes.data, want.ctypes.data,
                                    threads) == 0
         err = rel(bf16_to_f32(hidden[l + 1]), bf16_to_f32(want))
         worst = max(worst, err)
         assert err <= TOL, f"layer {l}: {err:.3e}"
-    want_pool = np.zeros((seqs, D), np.float32)
-    assert olib.orc_bert_pool(seed, layers, D, SEQ, seqs, hidden[layers].ctypes.data, want_pool.ctypes.data) == 0
+    want_pool = np.zeros((seqs, d), np.float32)
+    assert olib.orc_bert_pool(seed, layers, d, SEQ, seqs, hidden[layers].ctypes.data, want_pool.ctypes.data) == 0
     assert rel(pooled, want_pool) <= TOL
     return worst
 
@@ -173,6 +173,21 @@ def test_bert_c5_shape_teacher_forced(gfx, olib, mode):
     assert np.isfinite(pooled).all()
     worst = teacher_forced(olib, seed, layers, seqs, hidden, pooled, None if mode != "pair" else (0, 1, 6, 11))
     print(f"C5 shape ({mode}): worst per-layer normwise error {worst:.2e}")
+
+
+@pytest.mark.parametrize("d,ffn,layers,seqs", [(1024, 4096, 2, 32), (1024, 4096, 3, 3), (512, 2048, 3, 5)])
+def test_bert_other_widths_teacher_forced(gfx, olib, d, ffn, layers, seqs):
+    """Widths beyond BERT-base on the per-op path: BERT-large layers (d 1024, 16
+    heads, ffn 4096) at the C5 request shape (32 x 128 tokens: persistent GEMMs
+    with 2-3 tiles per CTA, the residual + LayerNorm epilogue in 4-CTA clusters)
+    and at 3 sequences, and d 512 (8 heads, 2-CTA clusters); every layer and the
+    pooler teacher-forced against the oracle."""
+    seed = gfx.model_seed(f"bert-width-{d}-{layers}-{seqs}")
+    x_bits, pooled, again, hidden = run_gpu(gfx, 74, layers, seqs, seed, request_id=3, d=d, ffn=ffn)
+    assert np.array_equal(pooled, again)
+    assert np.array_equal(hidden[0], x_bits)
+    worst = teacher_forced(olib, seed, layers, seqs, hidden, pooled, d=d, ffn=ffn)
+    print(f"d {d}: worst per-layer normwise error {worst:.2e}")
 
 
 @pytest.mark.parametrize("seqs", [1, 3, 37])
