@@ -413,7 +413,6 @@ __global__ void __launch_bounds__(kGThreads, 1)
         }
         if (tid == 0) K2_MARK(8);
         mbar_wait(&stat_bar, 0);
-        cluster_arrive();  // every statistic this CTA expects has landed: peers may exit once all arrived
         if (tid == 0) K2_MARK(9);
         {
             float2 p = xbuf[r];
@@ -550,7 +549,7 @@ __global__ void __launch_bounds__(kGThreads, 1)
     tc_fence_before();
     __syncthreads();
     if (kCluster) {  // no MMA / remote arrive / st.async may target an exited CTA
-        if (!(kLN && warp < kGEpiWarps)) cluster_arrive();  // (kLN epilogue threads arrived after their statistics)
+        cluster_arrive();  // every CTA's remote writes into its peers have landed (their waits passed)
         cluster_wait();
     }
     tc_fence_after();

@@ -442,6 +442,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // here) landed with the first: wait on the first slot's barrier.
                 const bool second = (g & 1) && s > rg.s0;
                 K1_WAIT(&w_full[second ? slot - 1 : slot], (g / kSlots) & 1, 6, g);
+                // The producer's plain arrive on the second slot's barrier (its phase completes at once):
+                // consumed here, so every phase of every barrier has a waiter (compute-sanitizer synccheck).
+                if (second) K1_WAIT(&w_full[slot], (g / kSlots) & 1, 6, g);
                 if (q == 0 && lane == 0) K1_STEP(g, 2);
                 if (l < 4 && lane == 0) K1_MARK(2 + 6 * l);
                 // Stage `slot` of the W_lo ring was last read by the MMAs of step
@@ -461,6 +464,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (q == 0 && lane == 0) K1_STEP(g, 6);
                 // X: warp q converts K columns 8q .. 8q+7 (16-byte chunks 2q, 2q+1) of all 32 rows; lane = batch row.
                 K1_WAIT(&raw_full[second && l > 0 ? slot - 1 : slot], (g / kSlots) & 1, 7, g);
+                if (second && l > 0) K1_WAIT(&raw_full[slot], (g / kSlots) & 1, 7, g);
                 if (q == 0 && lane == 0) K1_STEP(g, 3);
                 if (l == 0 && lane == 0) {
                     K1_MARK(3);

@@ -375,6 +375,10 @@ __device__ __forceinline__ void mbar_wait_cluster(uint64_t* bar, uint32_t parity
 __device__ __forceinline__ void st_cluster_u32(uint32_t remote_addr, uint32_t v) {
     asm volatile("st.shared::cluster.u32 [%0], %1;\n" ::"r"(remote_addr), "r"(v) : "memory");
 }
+// 8-byte (two f32) store into a cluster CTA's shared memory.
+__device__ __forceinline__ void st_cluster_v2f32(uint32_t remote_addr, float x, float y) {
+    asm volatile("st.shared::cluster.v2.f32 [%0], {%1, %2};\n" ::"r"(remote_addr), "f"(x), "f"(y) : "memory");
+}
 __device__ __forceinline__ void fence_acq_rel_cluster() { asm volatile("fence.acq_rel.cluster;\n" ::: "memory"); }
 __device__ __forceinline__ void st_release_gpu_u32(uint32_t* p, uint32_t v) {
     asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
