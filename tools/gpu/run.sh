@@ -12,7 +12,10 @@
 #   launches   ncu launch list of one bench step (gpu__time_duration + DRAM bytes per launch)
 #   ncu-k1     ncu --set full of two K1 forwards (tools/k1_prof.py)
 #   ncu-bert   ncu launch list of one BERT forward + --set full of its K2 GEMMs / attention
-#   sanitize   compute-sanitizer memcheck / synccheck / racecheck on K1 and BERT
+#   sanitize   compute-sanitizer memcheck / synccheck on K1, BERT per-op (d 768 / 1024), 2-SM, K5; racecheck BERT
+#   bertmodes  C5 forward per BERT path (per-op, 2-SM GEMMs, K5 dataflow) + the BERT parity tests
+#   k5trace    K5 debug build (make K5_DEBUG=1) and one forward's per-item timeline (tools/k5_trace.py)
+#   h2d        pinned host -> device copy rate (tools/h2d_rate.cu)
 set -u
 mkdir -p gpurun_out
 export PATH=/usr/local/cuda/bin:$PATH
@@ -55,12 +58,25 @@ run_task() {
       -o gpurun_out/bert_full -f python tools/bert_bench.py 2 perop
     echo "full rc=$?" ;;
   sanitize)
-    for tool in memcheck synccheck racecheck; do
-      echo "---- $tool mlp"
-      timeout 900 compute-sanitizer --tool $tool --print-limit 20 python tools/kernel_bench.py 0 1 2>&1 | tail -8
+    san() { echo "---- $1 $2"; shift 2; timeout 600 compute-sanitizer --print-limit 4 "$@" 2>&1 | tail -3; }
+    for tool in memcheck synccheck; do
+      san $tool "K1 mlp" --tool $tool python tools/kernel_bench.py 0 1
+      san $tool "BERT per-op 2 layers" --tool $tool python tools/bert_small.py 2 2 perop
+      san $tool "BERT per-op d1024" --tool $tool python tools/bert_small.py 1 2 perop 1024
+      san $tool "BERT 2-SM pair" --tool $tool python tools/bert_small.py 1 2 pair
+      san $tool "BERT flow K5" --tool $tool python tools/bert_small.py 2 3 flow
     done
-    echo "---- memcheck bert"
-    timeout 900 compute-sanitizer --tool memcheck --print-limit 20 python tools/bert_bench.py 1 2>&1 | tail -8 ;;
+    san racecheck "BERT per-op" --tool racecheck python tools/bert_small.py 1 2 perop ;;
+  bertmodes)
+    for m in perop pair flow; do timeout 300 python tools/bert_bench.py 50 $m; done
+    timeout 1500 python -m pytest tests/test_gpu_bert.py -q 2>&1 | tail -3 ;;
+  k5trace)
+    make K5_DEBUG=1 -j16 > gpurun_out/k5build.log 2>&1 || { tail -20 gpurun_out/k5build.log; return 1; }
+    GFX_K5_TRACE=gpurun_out/k5.trace timeout 120 python tools/bert_bench.py 10 flow
+    python tools/k5_trace.py gpurun_out/k5.trace ;;
+  h2d)
+    mkdir -p tools/_bin && nvcc -O2 -gencode arch=compute_100a,code=sm_100a tools/h2d_rate.cu -o tools/_bin/h2d_rate \
+      && timeout 120 tools/_bin/h2d_rate ;;
   *) echo "unknown task $t"; return 2 ;;
   esac
 }
