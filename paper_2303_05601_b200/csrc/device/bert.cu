@@ -792,9 +792,11 @@ __global__ void __launch_bounds__(256) layernorm_kernel(const __nv_bfloat16* __r
 
 // Pooler: out[b][n] = tanh(Wp[n] . x[b, token 0] + bp[n]) for the batch's
 // [CLS] rows — a 32 x 768 x 768 product. Block = 8 output features (one warp
-// each); the [CLS] rows are staged in shared memory once per block; each lane
+// each) x up to kPoolRows sequences (blockIdx.y); the block's [CLS] rows are
+// staged in shared memory once; each lane
 // holds 3 16-byte chunks of its warp's weight row in registers (swizzled blob
 // tile layout, one page translation per chunk).
+constexpr int kPoolRows = 64;  // sequences per pooler block (shared memory: 64 x d bf16)
 template <int kD>
 __global__ void __launch_bounds__(256) pooler_kernel(const __nv_bfloat16* __restrict__ x, float* __restrict__ out,
                                                      const char* arena, const __grid_constant__ PageTable ptab,
@@ -819,15 +821,16 @@ __global__ void __launch_bounds__(256) pooler_kernel(const __nv_bfloat16* __rest
         bias = *reinterpret_cast<const float*>(translate(arena, ptab.page, b_off + 4ull * n));
     }
     pdl_wait();
-    for (int i = threadIdx.x; i < batch * kD / 8; i += 256) {
+    const int b0 = blockIdx.y * kPoolRows, nb = min(kPoolRows, batch - b0);
+    for (int i = threadIdx.x; i < nb * kD / 8; i += 256) {
         const int b = i / (kD / 8), c = i % (kD / 8);
         reinterpret_cast<uint4*>(cls_raw)[i] =
-            *reinterpret_cast<const uint4*>(x + static_cast<size_t>(b) * seq * kD + c * 8);
+            *reinterpret_cast<const uint4*>(x + static_cast<size_t>(b0 + b) * seq * kD + c * 8);
     }
     __syncthreads();
     K2_SPAN_END(span);  // (pooler: start of the per-row loop)
     if (n >= d) return;
-    for (int b = 0; b < batch; ++b) {
+    for (int b = 0; b < nb; ++b) {
         float acc = 0.f;
 #pragma unroll
         for (int i = 0; i < kChunks; ++i) {
@@ -843,7 +846,7 @@ __global__ void __launch_bounds__(256) pooler_kernel(const __nv_bfloat16* __rest
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-        if (lane == 0) out[static_cast<size_t>(b) * d + n] = tanhf(acc + bias);
+        if (lane == 0) out[static_cast<size_t>(b0 + b) * d + n] = tanhf(acc + bias);
     }
 }
 
@@ -1173,12 +1176,11 @@ int bert_forward(const char* arena, const PageTable& pt, const BertLayout& lay, 
             GFX_CUDA(cudaMemcpyAsync(reinterpret_cast<char*>(hidden) + (l + 1) * hbytes, ws.x, hbytes,
                                      cudaMemcpyDeviceToDevice, s));
     }
-    if (static_cast<size_t>(batch) * d * 2 > 160 * 1024)
-        throw std::runtime_error("bert pooler: at most 160 KB of [CLS] rows per request (106 sequences at d = 768)");
     auto pool = d == 512 ? pooler_kernel<512> : d == 1024 ? pooler_kernel<1024> : pooler_kernel<768>;
-    ensure_max_dynamic_smem(reinterpret_cast<const void*>(pool), 160 * 1024);
-    launch_pdl(pool, dim3((d + 7) / 8), dim3(256), static_cast<size_t>(batch) * d * 2, s, !hidden,
-               static_cast<const __nv_bfloat16*>(x), out, arena, pt, lay.wp, lay.bp, d, lay.seq, batch,
+    const int rows = batch < kPoolRows ? batch : kPoolRows;
+    ensure_max_dynamic_smem(reinterpret_cast<const void*>(pool), kPoolRows * 1024 * 2);
+    launch_pdl(pool, dim3((d + 7) / 8, (batch + kPoolRows - 1) / kPoolRows), dim3(256), static_cast<size_t>(rows) * d * 2,
+               s, !hidden, static_cast<const __nv_bfloat16*>(x), out, arena, pt, lay.wp, lay.bp, d, lay.seq, batch,
                next_span("pooler"));
 #ifdef GFX_K2_DEBUG
     if (g_span.on) {

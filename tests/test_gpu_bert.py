@@ -190,6 +190,15 @@ def test_bert_other_widths_teacher_forced(gfx, olib, d, ffn, layers, seqs):
     print(f"d {d}: worst per-layer normwise error {worst:.2e}")
 
 
+def test_bert_large_batch_pooler(gfx, olib):
+    """A request of 130 sequences (more [CLS] rows than one pooler block stages:
+    pooler blocks of 64 sequences) through one layer; teacher-forced + pooler."""
+    seed = gfx.model_seed("bert-batch-130")
+    x_bits, pooled, again, hidden = run_gpu(gfx, 75, 1, 130, seed, request_id=9)
+    assert np.array_equal(pooled, again)
+    teacher_forced(olib, seed, 1, 130, hidden, pooled)
+
+
 @pytest.mark.parametrize("seqs", [1, 3, 37])
 def test_bert_flow_ragged_batches(gfx, olib, seqs):
     """K5 at batches that do not fill the 148 SMs (1, 3 row blocks) or leave a

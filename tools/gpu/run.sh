@@ -14,6 +14,7 @@
 #   ncu-bert   ncu launch list of one BERT forward + --set full of its K2 GEMMs / attention
 #   sanitize   compute-sanitizer memcheck / synccheck on K1, BERT per-op (d 768 / 1024), 2-SM, K5; racecheck BERT
 #   bertmodes  C5 forward per BERT path (per-op, 2-SM GEMMs, K5 dataflow) + the BERT parity tests
+#   bertbatch  12-layer BERT-base forward at 32 / 64 / 128 sequences, per-op vs K5
 #   k5trace    K5 debug build (make K5_DEBUG=1) and one forward's per-item timeline (tools/k5_trace.py)
 #   h2d        pinned host -> device copy rate (tools/h2d_rate.cu)
 set -u
@@ -70,6 +71,8 @@ run_task() {
   bertmodes)
     for m in perop pair flow; do timeout 300 python tools/bert_bench.py 50 $m; done
     timeout 1500 python -m pytest tests/test_gpu_bert.py -q 2>&1 | tail -3 ;;
+  bertbatch)
+    for S in 32 64 128; do for m in perop flow; do timeout 300 python tools/bert_small.py 12 $S $m 768 20 | head -1; done; done ;;
   k5trace)
     make K5_DEBUG=1 -j16 > gpurun_out/k5build.log 2>&1 || { tail -20 gpurun_out/k5build.log; return 1; }
     GFX_K5_TRACE=gpurun_out/k5.trace timeout 120 python tools/bert_bench.py 10 flow
