@@ -57,13 +57,13 @@ def test_c3_fleet_bit_exact_and_outputs(gfx, olib, policy):  # noqa: F811
 
 
 @pytest.mark.parametrize("gpus,zipf", [(2, 1.2), (4, 1.0), (8, 1.2)])
-def test_c4_peer_fetch_vs_host_reload(gfx, gpus, zipf):
+def test_c4_peer_fetch_vs_host_reload(gfx, olib, gpus, zipf):  # noqa: F811
     cfg = gfx.c3_config(gpus=gpus, policy="lalbo3", zipf=zipf)
     got = {}
     for p2p in (True, False):
         rep = gfx.Replay(gfx.catalog_text("mlp_c3"), cfg, n_devices=1, use_p2p=p2p, keep_outputs=True)
         res = rep.run()
-        got[p2p] = (res, rep.outputs(int(res.n_requests)))
+        got[p2p] = (res, rep.outputs(int(res.n_requests)), rep.request_info(int(res.n_requests))[0])
         rep.close()
     a, b = got[True][0], got[False][0]
     assert int(a.decision_digest) == int(b.decision_digest)
@@ -71,3 +71,10 @@ def test_c4_peer_fetch_vs_host_reload(gfx, gpus, zipf):
     assert a.loads_p2p + a.loads_h2d == b.loads_h2d == a.misses
     assert a.h2d_bytes + a.p2p_bytes == b.h2d_bytes
     assert np.array_equal(got[True][1], got[False][1])
+    # ... and the peer-fetch replay's outputs are the oracle's (not only the reload replay's).
+    n, models = int(a.n_requests), got[True][2]
+    specs = gfx.load_model_specs("mlp_c3")
+    for rid in np.linspace(0, n - 1, 4).astype(int):
+        _, lo, pr = oracle_forward(olib, gfx, specs[int(models[rid])], rid)
+        assert rel(got[True][1][rid, 0], lo) <= TOL
+        assert rel(got[True][1][rid, 1], pr) <= TOL

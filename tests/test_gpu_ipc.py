@@ -6,15 +6,19 @@ fetches the model out of the holder's arena with device-side ordering
 is done). On one device the "peer" copy is D2D; the ordering, page-table
 shadowing and counters are the same code as across NVLink.
 
-Checks: peer fetches happen on both runs, and every request's output is bit-for-
+Checks: peer fetches happen on both runs, every request's output is bit-for-
 bit the output of the single-process replay (two managers, in-process peer
-path) on the same schedule."""
+path) on the same schedule, and sampled outputs of that replay — requests
+served after peer fetches included — are within the fp32 tolerance of the
+oracle's forward."""
 import hashlib
 import os
 import socket
 
 import numpy as np
 import pytest
+
+from test_gpu_parity import TOL, olib, oracle_forward, rel  # noqa: F401
 
 pytestmark = pytest.mark.gpu
 
@@ -67,11 +71,11 @@ def _worker(rank, port, q, distinct_devices=False):
         dist.destroy_process_group()
 
 
-def test_cross_process_peer_fetch_matches_single_process():
-    run_cross_process(distinct_devices=False)
+def test_cross_process_peer_fetch_matches_single_process(olib):  # noqa: F811
+    run_cross_process(distinct_devices=False, olib=olib)
 
 
-def run_cross_process(distinct_devices):
+def run_cross_process(distinct_devices, olib=None):
     import torch.multiprocessing as mp
 
     import paper_2303_05601_b200 as gfx
@@ -80,9 +84,17 @@ def run_cross_process(distinct_devices):
     ref = gfx.Replay(cat, _cfg(gfx), n_devices=1, use_p2p=True, keep_outputs=True)
     rres = ref.run()
     n = int(rres.n_requests)
-    want = _digests(ref.outputs(n))
+    outs = ref.outputs(n)
+    want = _digests(outs)
+    models, _ = ref.request_info(n)
     ref.close()
     assert rres.loads_p2p > 0
+    if olib is not None:
+        specs = gfx.load_model_specs("mlp_c2")
+        for rid in np.linspace(0, n - 1, 6).astype(int):
+            _, lo, pr = oracle_forward(olib, gfx, specs[int(models[rid])], rid)
+            assert rel(outs[rid, 0], lo) <= TOL
+            assert rel(outs[rid, 1], pr) <= TOL
 
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
