@@ -160,6 +160,13 @@ int gfx_infer_sequence(gfx_arena_t a, const int32_t* models, int n, const void* 
  * hidden ([L+1][batch*seq][d] bf16, device) for teacher-forced parity checks. */
 int gfx_infer_debug(gfx_arena_t a, int model_idx, const void* in, void* out, int batch, void* hidden);
 
+/* BERT inference of padded sequences: lengths (HOST, [batch] int32, each in
+ * 1..seq) = valid tokens per sequence; attention ignores keys at or beyond a
+ * sequence's length (the additive -inf padding mask of BERT serving). hidden:
+ * optional, as gfx_infer_debug (then synchronous). Status 1 on a bad length. */
+int gfx_infer_masked(gfx_arena_t a, int model_idx, const void* in, void* out, int batch, const int32_t* lengths,
+                     void* hidden, gfx_event_t* done);
+
 /* Test/debug: one encoder GEMM of a resident BERT model with its fused epilogue,
  * on `tokens` rows (bf16, device pointers). op 0: QKV (+bias) [tokens x 3d];
  * 1: attention output (+bias, +resid) [tokens x d]; 2: FFN1 (+bias, GELU)

@@ -125,6 +125,10 @@ int orc_bert_forward(uint64_t seed, int L, int d, int heads, int ffn, int seq, i
  * pooler applied to a given final hidden state. */
 int orc_bert_layer(uint64_t seed, int l, int d, int heads, int ffn, int seq, int batch, const uint16_t* x_in,
                    uint16_t* x_out, int threads);
+/* orc_bert_layer with a padding mask: sequence s attends to its first lengths[s]
+ * keys (1 <= lengths[s] <= seq). Returns -1 on a bad length. */
+int orc_bert_layer_masked(uint64_t seed, int l, int d, int heads, int ffn, int seq, int batch, const int32_t* lengths,
+                          const uint16_t* x_in, uint16_t* x_out, int threads);
 int orc_bert_pool(uint64_t seed, int L, int d, int seq, int batch, const uint16_t* x_bits, float* pooled);
 /* Test hook: fp32 (k-order) GEMM accumulation, to measure intrinsic sensitivity. */
 void orc_set_acc32(int on);

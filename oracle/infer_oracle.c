@@ -302,8 +302,12 @@ static void layernorm_rows(const float* x, float* y, const float* g, const float
     }
 }
 
-/* One encoder layer l on x (in place): fp64 accumulation, bf16 rounding points. */
-static int bert_layer(uint64_t seed, int l, int d, int heads, int ffn, int seq, int batch, float* x, int threads) {
+/* One encoder layer l on x (in place): fp64 accumulation, bf16 rounding points.
+ * lengths (NULL: every sequence is full): sequence s attends to its first
+ * lengths[s] keys only (padding mask: keys j >= len excluded from the softmax,
+ * as transformers' additive -inf attention mask); every query row is computed. */
+static int bert_layer(uint64_t seed, int l, int d, int heads, int ffn, int seq, int batch, float* x, int threads,
+                      const int32_t* lengths) {
     const int T = batch * seq, dh = d / heads;
     float* qkv = malloc((size_t)T * 3 * (size_t)d * sizeof(float));
     float* ctx = malloc((size_t)T * (size_t)d * sizeof(float));
@@ -335,9 +339,10 @@ static int bert_layer(uint64_t seed, int l, int d, int heads, int ffn, int seq, 
     for (int s = 0; s < batch; ++s)
         for (int hh = 0; hh < heads; ++hh)
             for (int i = 0; i < seq; ++i) {
+                const int nk = lengths ? lengths[s] : seq; /* valid keys of this sequence */
                 const float* q = qkv + ((size_t)s * seq + (size_t)i) * 3 * (size_t)d + (size_t)hh * dh;
                 double m = -INFINITY;
-                for (int j = 0; j < seq; ++j) {
+                for (int j = 0; j < nk; ++j) {
                     const float* k = qkv + ((size_t)s * seq + (size_t)j) * 3 * (size_t)d + (size_t)d + (size_t)hh * dh;
                     double sc = 0;
                     for (int e = 0; e < dh; ++e) sc += (double)q[e] * k[e];
@@ -345,13 +350,13 @@ static int bert_layer(uint64_t seed, int l, int d, int heads, int ffn, int seq, 
                     if (sc > m) m = sc;
                 }
                 double lsum = 0;
-                for (int j = 0; j < seq; ++j) {
+                for (int j = 0; j < nk; ++j) {
                     srow[j] = exp((srow[j] - m) * 0.125);
                     lsum += srow[j];
                 }
                 for (int e = 0; e < dh; ++e) {
                     double o = 0;
-                    for (int j = 0; j < seq; ++j) {
+                    for (int j = 0; j < nk; ++j) {
                         const float* v = qkv + ((size_t)s * seq + (size_t)j) * 3 * (size_t)d + 2 * (size_t)d + (size_t)hh * dh;
                         o += (double)bf16_round((float)srow[j]) * v[e];
                     }
@@ -413,7 +418,21 @@ int orc_bert_layer(uint64_t seed, int l, int d, int heads, int ffn, int seq, int
     float* x = malloc(n * sizeof(float));
     if (!x) return -1;
     bits_to_float(x_in, x, n);
-    int rc = bert_layer(seed, l, d, heads, ffn, seq, batch, x, threads);
+    int rc = bert_layer(seed, l, d, heads, ffn, seq, batch, x, threads, NULL);
+    float_to_bits(x, x_out, n);
+    free(x);
+    return rc;
+}
+
+int orc_bert_layer_masked(uint64_t seed, int l, int d, int heads, int ffn, int seq, int batch, const int32_t* lengths,
+                          const uint16_t* x_in, uint16_t* x_out, int threads) {
+    for (int s = 0; s < batch; ++s)
+        if (lengths[s] < 1 || lengths[s] > seq) return -1;
+    const size_t n = (size_t)batch * seq * (size_t)d;
+    float* x = malloc(n * sizeof(float));
+    if (!x) return -1;
+    bits_to_float(x_in, x, n);
+    int rc = bert_layer(seed, l, d, heads, ffn, seq, batch, x, threads, lengths);
     float_to_bits(x, x_out, n);
     free(x);
     return rc;
@@ -436,7 +455,7 @@ int orc_bert_forward(uint64_t seed, int L, int d, int heads, int ffn, int seq, i
     if (!x) return -1;
     bits_to_float(x_bits, x, n);
     for (int l = 0; l < L; ++l)
-        if (bert_layer(seed, l, d, heads, ffn, seq, batch, x, threads)) { free(x); return -1; }
+        if (bert_layer(seed, l, d, heads, ffn, seq, batch, x, threads, NULL)) { free(x); return -1; }
     bert_pool(seed, L, d, seq, batch, x, pooled);
     free(x);
     return 0;

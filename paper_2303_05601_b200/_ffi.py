@@ -100,6 +100,7 @@ gfx_fetch_p2p = _sig("gfx_fetch_p2p", C.c_int, [_vp, _vp, C.c_int, C.POINTER(_vp
 gfx_evict = _sig("gfx_evict", C.c_int, [_vp, C.c_int])
 gfx_infer = _sig("gfx_infer", C.c_int, [_vp, C.c_int, _vp, _vp, C.c_int, C.POINTER(_vp)])
 gfx_infer_debug = _sig("gfx_infer_debug", C.c_int, [_vp, C.c_int, _vp, _vp, C.c_int, _vp])
+gfx_infer_masked = _sig("gfx_infer_masked", C.c_int, [_vp, C.c_int, _vp, _vp, C.c_int, _vp, _vp, C.POINTER(_vp)])
 gfx_event_query = _sig("gfx_event_query", C.c_int, [_vp])
 gfx_event_sync = _sig("gfx_event_sync", C.c_int, [_vp])
 gfx_event_release = _sig("gfx_event_release", C.c_int, [_vp])

@@ -746,6 +746,18 @@ int gfx_infer_sequence(gfx_arena_t a, const int32_t* models, int n, const void* 
     });
 }
 
+int gfx_infer_masked(gfx_arena_t a, int model_idx, const void* in, void* out, int batch, const int32_t* lengths,
+                     void* hidden, gfx_event_t* done) {
+    return guarded([&] {
+        const gfx::ModelBlob& b = ModelStore::get().at(model_idx);
+        if (b.desc.family != GFX_MODEL_BERT) throw std::invalid_argument("gfx_infer_masked: BERT models only");
+        if (batch != b.desc.batch) throw std::invalid_argument("batch does not match the registered model");
+        if (!lengths) throw std::invalid_argument("gfx_infer_masked: lengths required");
+        a->mgr->infer(model_idx, in, out, hidden, lengths);
+        if (hidden) GFX_CUDA(cudaStreamSynchronize(a->mgr->compute_stream()));
+        make_event(*a->mgr, a->mgr->compute_stream(), done);
+    });
+}
 int gfx_infer_debug(gfx_arena_t a, int model_idx, const void* in, void* out, int batch, void* hidden) {
     return guarded([&] {
         const gfx::ModelBlob& b = ModelStore::get().at(model_idx);

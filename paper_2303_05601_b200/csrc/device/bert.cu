@@ -585,8 +585,11 @@ constexpr uint32_t kAttnSmem = 3 * 16384 + 1024;  // Q, K, V; P overlays Q + K o
 // 1.017 ms per C5 forward — the kernel's ~9.7 µs after QKV are load and
 // launch latency, not softmax issue.)
 constexpr int kAttnThreads = 256;
+// lengths (nullptr: every sequence full): padding mask — keys j >= lengths[seq] get
+// probability 0 (excluded from the row max and sum, as an additive -inf mask).
 __global__ void __launch_bounds__(kAttnThreads, 4) attention_tc_kernel(const __grid_constant__ CUtensorMap tmap_qkv,
                                                                     __nv_bfloat16* __restrict__ ctx, int heads,
+                                                                    const int* __restrict__ lengths,
                                                                     unsigned long long* span) {
     K2_SPAN_BEGIN(span);
     extern __shared__ uint8_t smem_raw[];
@@ -632,17 +635,19 @@ __global__ void __launch_bounds__(kAttnThreads, 4) attention_tc_kernel(const __g
     mbar_wait(&s_bar, 0);
     tc_fence_after();
     const uint32_t row_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(hf * 64);
+    const int nvalid = lengths ? lengths[seq] - hf * 64 : 64;  // this half's valid keys (<= 0: none)
     float mx = -INFINITY;
 #pragma unroll
     for (int c = 0; c < 2; ++c) {
         float part[32];
         tmem_ld_32x32b_x32(row_base + static_cast<uint32_t>(c * 32), part);
 #pragma unroll
-        for (int j = 0; j < 32; ++j) mx = fmaxf(mx, part[j]);
+        for (int j = 0; j < 32; ++j)
+            if (c * 32 + j < nvalid) mx = fmaxf(mx, part[j]);
     }
     red_max[hf][r] = mx;
     __syncthreads();
-    mx = fmaxf(red_max[0][r], red_max[1][r]);
+    mx = fmaxf(red_max[0][r], red_max[1][r]);  // finite: every sequence has >= 1 valid key (host-checked)
     const float off = mx * kAttnScaleLog2;
     float sum = 0.f;
     uint8_t* pb = ps + hf * 16384;  // this half's 64 keys = P block hf
@@ -657,8 +662,9 @@ __global__ void __launch_bounds__(kAttnThreads, 4) attention_tc_kernel(const __g
             __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const float p0 = ex2_approx(fmaf(part[q8 * 8 + 2 * j], kAttnScaleLog2, -off));
-                const float p1 = ex2_approx(fmaf(part[q8 * 8 + 2 * j + 1], kAttnScaleLog2, -off));
+                const int key = cc * 8 + 2 * j;  // within this half
+                const float p0 = key < nvalid ? ex2_approx(fmaf(part[q8 * 8 + 2 * j], kAttnScaleLog2, -off)) : 0.f;
+                const float p1 = key + 1 < nvalid ? ex2_approx(fmaf(part[q8 * 8 + 2 * j + 1], kAttnScaleLog2, -off)) : 0.f;
                 sum += p0 + p1;
                 h2[j] = __floats2bfloat162_rn(p0, p1);
             }
@@ -1124,7 +1130,7 @@ void BertWorkspace::release() {
 }
 
 int bert_forward(const char* arena, const PageTable& pt, const BertLayout& lay, int batch, const __nv_bfloat16* in,
-                 float* out, BertWorkspace& ws, cudaStream_t s, __nv_bfloat16* hidden) {
+                 float* out, BertWorkspace& ws, cudaStream_t s, __nv_bfloat16* hidden, const int* lengths) {
     const int d = lay.d, T = batch * lay.seq;
     if (lay.seq != kS || d / lay.heads != kDh || d % lay.heads || (d != 512 && d != 768 && d != 1024))
         throw std::runtime_error("bert: this build serves seq 128, d_head 64, d 512 / 768 / 1024");
@@ -1145,7 +1151,7 @@ int bert_forward(const char* arena, const PageTable& pt, const BertLayout& lay, 
     const __nv_bfloat16* x = in;
     const size_t hbytes = static_cast<size_t>(T) * d * 2;
     if (hidden) GFX_CUDA(cudaMemcpyAsync(hidden, in, hbytes, cudaMemcpyDeviceToDevice, s));
-    const bool flow = ws.flow && bert_flow_supported(lay, batch);
+    const bool flow = ws.flow && !lengths && bert_flow_supported(lay, batch);  // K5 serves unmasked requests
     if (flow) {
         // K5: every layer in one dataflow launch; with `hidden`, layer l's output lands in hidden[l + 1].
         __nv_bfloat16* xout = hidden ? hidden + static_cast<size_t>(T) * d : ws.x;
@@ -1164,6 +1170,7 @@ int bert_forward(const char* arena, const PageTable& pt, const BertLayout& lay, 
                 throw CudaError("cuTensorMapEncodeTiled failed (attention)");
             ensure_max_dynamic_smem(reinterpret_cast<const void*>(attention_tc_kernel), static_cast<int>(kAttnSmem));
             launch_pdl(attention_tc_kernel, dim3(batch * lay.heads), dim3(kAttnThreads), kAttnSmem, s, true, tq, ws.ctx, lay.heads,
+                       lengths,
                        next_span("attention"));
         }
         gemm_resid_ln(arena, pt, o.wo, o.bo, o.ln1_g, o.ln1_b, ws.ctx, ws.h, x, ws.t, T, d, d, s, true, ws.gemm_pair);

@@ -76,9 +76,12 @@ int bert_encoder_flow(const char* arena, const PageTable& pt, const BertLayout& 
 
 // One forward of a resident BERT model: in = [batch*seq x d] bf16 embeddings,
 // out = [batch x d] fp32 pooled output. Returns kernel launches.
+// lengths (device, [batch] int32 in 1..seq, optional): padding mask — sequence b
+// attends to its first lengths[b] tokens.
 int bert_forward(const char* arena, const PageTable& pt, const BertLayout& lay, int batch,
                  const __nv_bfloat16* in, float* out, BertWorkspace& ws, cudaStream_t s,
-                 __nv_bfloat16* hidden = nullptr);  // debug: [L+1][T][d] hidden states
+                 __nv_bfloat16* hidden = nullptr,  // debug: [L+1][T][d] hidden states
+                 const int* lengths = nullptr);
 
 // Test hook: one K2 GEMM of layer l with its fused epilogue. op 0: QKV (+bias),
 // 1: attention output (+bias +resid), 2: FFN1 (+bias, GELU), 3: FFN2 (+bias +resid);

@@ -306,6 +306,9 @@ GpuManager::~GpuManager() {
     cudaFree(arena_);
     cudaFree(fwd_act_);
     bert_ws_.release();
+    if (bert_lengths_) cudaFree(bert_lengths_);
+    bert_lengths_ = nullptr;
+    bert_lengths_cap_ = 0;
     cudaStreamDestroy(compute_);
     cudaStreamDestroy(copy_);
 }
@@ -498,18 +501,37 @@ void GpuManager::build_page_table(const Slot& s, PageTable& pt) const {
 // The batched inference that replaces profile.infer_time_us
 // (proj/src/cluster.cpp:161,167): MLP -> one K1 launch (the whole forward),
 // BERT -> the K2-K4 chain, on the compute stream.
-void GpuManager::infer(int model, const void* in_v, void* out_v, void* debug_hidden) {
+void GpuManager::infer(int model, const void* in_v, void* out_v, void* debug_hidden, const int32_t* lengths) {
     const ModelBlob& blob = ModelStore::get().at(model);
     Slot& s = slot(model);
     if (!s.live) throw std::logic_error("inference of non-resident model " + std::to_string(model));
+    if (lengths && blob.desc.family != GFX_MODEL_BERT) throw std::invalid_argument("sequence lengths: BERT models only");
     activate();
     if (blob.desc.family == GFX_MODEL_BERT) {
         PageTable pt;
         build_page_table(s, pt);
+        const int* dlen = nullptr;
+        if (lengths) {
+            const int batch = blob.desc.batch, seq = blob.bert.seq;
+            for (int b = 0; b < batch; ++b)
+                if (lengths[b] < 1 || lengths[b] > seq)
+                    throw std::invalid_argument("sequence length " + std::to_string(lengths[b]) + " outside 1.." +
+                                                std::to_string(seq));
+            if (bert_lengths_cap_ < batch) {
+                if (bert_lengths_) GFX_CUDA(cudaFree(bert_lengths_));
+                GFX_CUDA(cudaMalloc(&bert_lengths_, sizeof(int) * static_cast<size_t>(batch)));
+                bert_lengths_cap_ = batch;
+            }
+            // Ordered on the compute stream before the forward; the host array may be reused on return
+            // (pageable source: the copy is staged before cudaMemcpyAsync returns).
+            GFX_CUDA(cudaMemcpyAsync(bert_lengths_, lengths, sizeof(int) * static_cast<size_t>(batch),
+                                     cudaMemcpyHostToDevice, compute_));
+            dlen = bert_lengths_;
+        }
         if (layer_timer) GFX_CUDA(cudaEventRecord(layer_timer->next(), compute_));
         kernel_launches += bert_forward(arena_, pt, blob.bert, blob.desc.batch,
                                         static_cast<const __nv_bfloat16*>(in_v), static_cast<float*>(out_v), bert_ws_,
-                                        compute_, static_cast<__nv_bfloat16*>(debug_hidden));
+                                        compute_, static_cast<__nv_bfloat16*>(debug_hidden), dlen);
         if (layer_timer) GFX_CUDA(cudaEventRecord(layer_timer->next(), compute_));
         GFX_CUDA(cudaEventRecord(s.last_use, compute_));
         return;

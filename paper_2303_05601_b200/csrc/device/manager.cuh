@@ -88,7 +88,8 @@ public:
     void evict(int model);
     // Returns bytes copied. src == nullptr -> pinned host store.
     uint64_t load(int model, GpuManager* src);
-    void infer(int model, const void* in, void* out, void* debug_hidden = nullptr);
+    // BERT only: lengths (HOST, [batch] int32 in 1..seq) = padding mask per sequence.
+    void infer(int model, const void* in, void* out, void* debug_hidden = nullptr, const int32_t* lengths = nullptr);
     void reset();  // synchronise and drop every resident model
     // Test hook: one BERT GEMM (bert_gemm_op) of a resident model on the compute stream.
     void bert_gemm(int model, int layer, int op, const void* x, const void* resid, void* y, int tokens);
@@ -141,6 +142,8 @@ private:
     int sm_count_ = 148;
     // inference workspaces
     BertWorkspace bert_ws_;
+    int* bert_lengths_ = nullptr;  // device copy of a masked request's sequence lengths
+    int bert_lengths_cap_ = 0;
     // K1 forward workspace: layer outputs, two banks by launch parity
     unsigned long long* fwd_act_ = nullptr;
     unsigned fwd_epoch_ = 0;      // launches of the forward kernel on this manager's workspace

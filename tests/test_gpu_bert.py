@@ -50,6 +50,9 @@ def olib():
     lib.orc_bert_layer.restype = C.c_int
     lib.orc_bert_layer.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
                                    C.c_void_p, C.c_int]
+    lib.orc_bert_layer_masked.restype = C.c_int
+    lib.orc_bert_layer_masked.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
     lib.orc_bert_pool.restype = C.c_int
     lib.orc_bert_pool.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
     lib.orc_fill_params.restype = None
@@ -67,7 +70,7 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / np.linalg.norm(b))
 
 
-def run_gpu(gfx, idx, layers, seqs, seed, request_id=7, debug=True, mode="perop", d=D, ffn=3072):
+def run_gpu(gfx, idx, layers, seqs, seed, request_id=7, debug=True, mode="perop", d=D, ffn=3072, lengths=None):
     desc = gfx.models.bert_desc(layers, seqs, seed, d=d, heads=d // 64, ffn=ffn)
     gfx.check(gfx._ffi.gfx_model_register(idx, C.byref(desc)))
     inb, outb = C.c_uint64(), C.c_uint64()
@@ -89,15 +92,24 @@ def run_gpu(gfx, idx, layers, seqs, seed, request_id=7, debug=True, mode="perop"
         gfx.check(gfx._ffi.gfx_device_alloc(a, hbytes, C.byref(hd)))
         gfx.check(gfx._ffi.gfx_memcpy_h2d(a, xd, x_bits.ctypes.data, inb.value))
         gfx.check(gfx._ffi.gfx_load_h2d(a, idx, None))
-        gfx.check(gfx._ffi.gfx_infer(a, idx, xd, yd, seqs, None))  # production (PDL-chained) path
+        lp = None if lengths is None else np.ascontiguousarray(lengths, np.int32)
+
+        def infer(hid=None):
+            if lp is None and hid is None:
+                gfx.check(gfx._ffi.gfx_infer(a, idx, xd, yd, seqs, None))  # production (PDL-chained) path
+            elif lp is None:
+                gfx.check(gfx._ffi.gfx_infer_debug(a, idx, xd, yd, seqs, hid))
+            else:
+                gfx.check(gfx._ffi.gfx_infer_masked(a, idx, xd, yd, seqs, lp.ctypes.data, hid, None))
+        infer()
         pooled = np.zeros((seqs, d), np.float32)
         gfx.check(gfx._ffi.gfx_memcpy_d2h(a, pooled.ctypes.data, yd, outb.value))
-        gfx.check(gfx._ffi.gfx_infer(a, idx, xd, yd, seqs, None))
+        infer()
         again = np.zeros_like(pooled)
         gfx.check(gfx._ffi.gfx_memcpy_d2h(a, again.ctypes.data, yd, outb.value))
         hidden = None
         if debug:
-            gfx.check(gfx._ffi.gfx_infer_debug(a, idx, xd, yd, seqs, hd))
+            infer(hd)
             hidden = np.zeros((layers + 1, seqs * SEQ * d), np.uint16)
             gfx.check(gfx._ffi.gfx_memcpy_d2h(a, hidden.ctypes.data, hd, hbytes))
             dbg = np.zeros_like(pooled)
@@ -197,6 +209,34 @@ def test_bert_large_batch_pooler(gfx, olib):
     x_bits, pooled, again, hidden = run_gpu(gfx, 75, 1, 130, seed, request_id=9)
     assert np.array_equal(pooled, again)
     teacher_forced(olib, seed, 1, 130, hidden, pooled)
+
+
+def test_bert_padding_mask_teacher_forced(gfx, olib):
+    """Padded sequences (gfx_infer_masked): lengths 1, 64, 65, 127, 128 and random
+    ones at the C5 request shape (32 x 128 tokens) through 3 layers; every layer
+    teacher-forced against the oracle's masked layer, the pooler too; a bad
+    length is refused."""
+    seqs, layers = 32, 3
+    rng = np.random.default_rng(5)
+    lengths = rng.integers(1, 129, seqs).astype(np.int32)
+    lengths[:5] = [1, 64, 65, 127, 128]
+    seed = gfx.model_seed("bert-masked")
+    x_bits, pooled, again, hidden = run_gpu(gfx, 76, layers, seqs, seed, request_id=4, lengths=lengths)
+    assert np.array_equal(pooled, again)
+    threads = os.cpu_count() or 1
+    for l in range(layers):
+        want = np.zeros_like(hidden[l])
+        assert olib.orc_bert_layer_masked(seed, l, D, 12, 3072, SEQ, seqs, lengths.ctypes.data, hidden[l].ctypes.data,
+                                          want.ctypes.data, threads) == 0
+        err = rel(bf16_to_f32(hidden[l + 1]), bf16_to_f32(want))
+        assert err <= TOL, f"layer {l}: {err:.3e}"
+    want_pool = np.zeros((seqs, D), np.float32)
+    assert olib.orc_bert_pool(seed, layers, D, SEQ, seqs, hidden[layers].ctypes.data, want_pool.ctypes.data) == 0
+    assert rel(pooled, want_pool) <= TOL
+    with pytest.raises(gfx.GfxError):
+        bad = lengths.copy()
+        bad[3] = 0
+        run_gpu(gfx, 76, layers, seqs, seed, request_id=4, lengths=bad, debug=False)
 
 
 @pytest.mark.parametrize("seqs", [1, 3, 37])

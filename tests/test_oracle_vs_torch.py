@@ -42,6 +42,9 @@ def olib():
     lib.orc_bert_layer.restype = C.c_int
     lib.orc_bert_layer.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p,
                                    C.c_void_p, C.c_int]
+    lib.orc_bert_layer_masked.restype = C.c_int
+    lib.orc_bert_layer_masked.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                          C.c_void_p, C.c_void_p, C.c_void_p, C.c_int]
     lib.orc_bert_pool.restype = C.c_int
     lib.orc_bert_pool.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]
     return lib
@@ -159,6 +162,33 @@ def test_bert_layer_oracle_matches_transformers(olib):
         other = layer(torch.from_numpy(x).double().reshape(seqs, SEQ, D))
         other = (other[0] if isinstance(other, tuple) else other).reshape(-1).numpy()
     assert rel(got_f, other) > 5 * 5e-3
+
+
+def test_bert_masked_layer_oracle_matches_transformers(olib):
+    """Padding mask: the oracle's masked layer (keys j >= lengths[s] excluded) =
+    transformers BertLayer with the additive -inf attention mask; query rows past
+    a sequence's length are computed too (and compared)."""
+    seed, seqs, l = 0xB0B0 + 21, 3, 1
+    lengths = np.array([1, 77, 128], np.int32)
+    x, xb = bert_input(olib, seqs)
+    got = np.zeros_like(xb)
+    assert olib.orc_bert_layer_masked(seed, l, D, HEADS, FFN, SEQ, seqs, lengths.ctypes.data, xb.ctypes.data,
+                                      got.ctypes.data, 8) == 0
+    got_f = (got.astype(np.uint32) << 16).view(np.float32)
+    mask = torch.zeros(seqs, 1, 1, SEQ, dtype=torch.float64)
+    for s_, n in enumerate(lengths):
+        mask[s_, :, :, n:] = float("-inf")
+    layer = hf_bert_layer(olib, seed, l)
+    with torch.no_grad():
+        want = layer(torch.from_numpy(x).double().reshape(seqs, SEQ, D), attention_mask=mask)
+        want = (want[0] if isinstance(want, tuple) else want).reshape(-1).numpy()
+        unmasked = layer(torch.from_numpy(x).double().reshape(seqs, SEQ, D))
+        unmasked = (unmasked[0] if isinstance(unmasked, tuple) else unmasked).reshape(-1).numpy()
+    assert rel(got_f, want) < 5e-3
+    assert rel(got_f, unmasked) > 5 * 5e-3  # the mask matters at these lengths
+    bad = np.array([0, 5, 5], np.int32)
+    assert olib.orc_bert_layer_masked(seed, l, D, HEADS, FFN, SEQ, seqs, bad.ctypes.data, xb.ctypes.data,
+                                      got.ctypes.data, 8) == -1
 
 
 def test_bert_pooler_oracle_matches_transformers(olib):
