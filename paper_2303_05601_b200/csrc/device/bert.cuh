@@ -63,7 +63,12 @@ struct BertWorkspace {
     void* flow_stats = nullptr;  // per-row LayerNorm statistics of the residual tiles
     int flow_n_items = 0, flow_L = 0, flow_M = 0, flow_F = 0, flow_ctas = 0;
     size_t flow_cnt_words = 0;
+    // Second stream (+ fork / join events) for the two-half per-op forward, created on first use
+    // on the device current at the time (the manager's).
+    cudaStream_t side = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
     void ensure(int tokens, int d, int ffn);
+    void ensure_side_stream();
     void release();
 };
 
