@@ -9,7 +9,7 @@
 //                         double-buffered TMEM accumulators; fused bias / GELU /
 //                         residual epilogue (16 warps) through TMA stores; bf16 out.
 //                         Tensor-core bound. Opt-in 2-SM (cta_group::2) variant.
-//   K3 attention_tc_kernel softmax(Q K^T / sqrt(64)) V per (sequence, head),
+//   K3 attention_tc_kernel softmax(Q K^T / sqrt(64)) V per (sequence, head, query tile),
 //                         S = 128: one CTA of 4 warps, both products on tcgen05
 //                         (V read MN-major), softmax from TMEM by the row's thread.
 //   K4 layernorm_kernel   one warp per token row, 16-byte vector loads, fp32
@@ -567,41 +567,49 @@ __global__ void __launch_bounds__(kGThreads, 1)
 
 constexpr int kS = 128, kDh = 64;
 
-// One CTA (4 warps) per (sequence, head): S = Q K^T (M = 128 queries, N = 128
-// keys, K = 64: four kind::f16 MMAs into TMEM), row softmax by the thread that
-// owns the row's TMEM lane (P = exp((s - max) / 8) unnormalised, bf16, written
-// as the next MMA's K-major SWIZZLE_128B A operand), O = P V (M = 128, N = 64,
-// K = 128: V is read MN-major straight from its token-major tile), O / sum.
-// Q, K, V arrive by three 2-D TMA boxes (64 dims x 128 tokens) from the fused
-// QKV activation. (The first version used warp-level mma.sync; 2.7 % of the
-// model's flops took 12 % of its time there.)
-constexpr uint32_t kAttnSmem = 3 * 16384 + 1024;  // Q, K, V; P overlays Q + K once S is computed
-
+// One CTA (8 warps) per (sequence, head, 128-query tile) for sequences of
+// 128 kNK tokens (kNK = 1..4: 128 / 256 / 384 / 512): S = Q K^T for all kNK key
+// tiles into TMEM (M = 128 queries, N = 128 keys per tile, K = 64: four
+// kind::f16 MMAs each — the whole score row is resident, so the softmax is
+// exact, no online rescaling), row softmax by the threads owning the row's TMEM
+// lane (P = exp((s - max) / 8) unnormalised, bf16, written as the next MMA's
+// K-major SWIZZLE_128B A operand), O = P V (M = 128, N = 64, K = 128 kNK: V
+// read MN-major straight from its token-major tiles), O / sum. Q, K, V arrive by
+// 2-D TMA boxes (64 dims x 128 tokens) from the fused QKV activation.
+// Shared memory: [V: kNK x 16 KB][Q 16 KB][K: kNK x 16 KB][pad]; P (kNK x 32 KB)
+// overlays Q, K and the pad once the S MMAs have read them. (The first version
+// used warp-level mma.sync; 2.7 % of the model's flops took 12 % of its time.)
+template <int kNK>
+constexpr uint32_t attn_smem() {
+    return static_cast<uint32_t>(kNK) * 16384 + static_cast<uint32_t>(kNK) * 32768 + 1024;
+}
 
 // 8 warps: warp w owns TMEM lane quarter w & 3 (query rows 32 (w & 3) ..) and key
-// half w >> 2 (keys 64 (w >> 2) .. + 63, i.e. P block w >> 2): each thread takes
-// half a row, the two halves exchange their row max and sum through shared
-// memory. (Measured against the 4-warp version, one thread per row: the same
-// 1.017 ms per C5 forward — the kernel's ~9.7 µs after QKV are load and
-// launch latency, not softmax issue.)
+// half w >> 2 (keys 64 kNK (w >> 2) .. + 64 kNK - 1): each thread takes half a row,
+// the two halves exchange their row max and sum through shared memory. (Measured
+// against the 4-warp version, one thread per row: the same 1.017 ms per C5
+// forward — the kernel's ~9.7 µs after QKV are load and launch latency.)
 constexpr int kAttnThreads = 256;
 // lengths (nullptr: every sequence full): padding mask — keys j >= lengths[seq] get
 // probability 0 (excluded from the row max and sum, as an additive -inf mask).
-__global__ void __launch_bounds__(kAttnThreads, 4) attention_tc_kernel(const __grid_constant__ CUtensorMap tmap_qkv,
+template <int kNK>
+__global__ void __launch_bounds__(kAttnThreads, kNK == 1 ? 4 : 1) attention_tc_kernel(const __grid_constant__ CUtensorMap tmap_qkv,
                                                                     __nv_bfloat16* __restrict__ ctx, int heads,
                                                                     const int* __restrict__ lengths,
                                                                     unsigned long long* span) {
+    constexpr int kSeq = kNK * kS, kHalf = kSeq / 2;  // tokens per sequence, keys per thread
+    constexpr uint32_t kTmemCols = kNK == 1 ? 128 : kNK == 2 ? 256 : 512;
     K2_SPAN_BEGIN(span);
     extern __shared__ uint8_t smem_raw[];
     uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    uint8_t* qs = sm;
-    uint8_t* ks = sm + 16384;
-    uint8_t* vs = sm + 32768;
-    uint8_t* ps = sm;  // P (keys 0-63 block, keys 64-127 block) over Q and K: dead after the S MMAs
+    uint8_t* vs = sm;
+    uint8_t* qs = sm + kNK * 16384;
+    uint8_t* ks = qs + 16384;
+    uint8_t* ps = qs;  // P: 2 kNK blocks of 64 keys (16 KB each) over Q, K and the pad
     __shared__ __align__(8) uint64_t ld_bar, s_bar, o_bar;
     __shared__ uint32_t tmem_s;
     __shared__ float red_max[2][kS], red_sum[2][kS];
-    const int seq = blockIdx.x / heads, h = blockIdx.x % heads;
+    const int bid = blockIdx.x, qt = bid % kNK, h = (bid / kNK) % heads, seq = bid / (kNK * heads);
     const int d = heads * kDh;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int q = warp & 3, hf = warp >> 2, r = q * 32 + lane;
@@ -612,33 +620,40 @@ __global__ void __launch_bounds__(kAttnThreads, 4) attention_tc_kernel(const __g
         mbar_fence_init();
         tma_prefetch_desc(&tmap_qkv);
     }
-    if (warp == 0) tmem_alloc<128>(&tmem_s);  // S: columns 0-127; O reuses 0-63 after the softmax read S
+    if (warp == 0) tmem_alloc<kTmemCols>(&tmem_s);  // S: columns 0 .. 128 kNK - 1; O reuses 0-63 after the softmax
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = tmem_s;
     pdl_wait();
     if (tid == 0) {
-        mbar_arrive_expect_tx(&ld_bar, 3 * 16384);
-        tma_tile2d_g2s(qs, &tmap_qkv, h * kDh, seq * kS, &ld_bar);
-        tma_tile2d_g2s(ks, &tmap_qkv, d + h * kDh, seq * kS, &ld_bar);
-        tma_tile2d_g2s(vs, &tmap_qkv, 2 * d + h * kDh, seq * kS, &ld_bar);
+        const int row0 = seq * kSeq;
+        mbar_arrive_expect_tx(&ld_bar, (1 + 2 * kNK) * 16384);
+        tma_tile2d_g2s(qs, &tmap_qkv, h * kDh, row0 + qt * kS, &ld_bar);
+#pragma unroll
+        for (int j = 0; j < kNK; ++j) {
+            tma_tile2d_g2s(ks + j * 16384, &tmap_qkv, d + h * kDh, row0 + j * kS, &ld_bar);
+            tma_tile2d_g2s(vs + j * 16384, &tmap_qkv, 2 * d + h * kDh, row0 + j * kS, &ld_bar);
+        }
         mbar_wait(&ld_bar, 0);
         tc_fence_after();
         constexpr uint32_t idesc_s = umma_idesc<128, 128, 1>();  // bf16 x bf16 -> f32, both K-major
 #pragma unroll
-        for (int kk = 0; kk < kDh / 16; ++kk)
-            umma_f16(tmem, umma_desc_sw128(qs, kk * 32), umma_desc_sw128(ks, kk * 32), idesc_s, kk ? 1u : 0u);
+        for (int j = 0; j < kNK; ++j)
+#pragma unroll
+            for (int kk = 0; kk < kDh / 16; ++kk)
+                umma_f16(tmem + static_cast<uint32_t>(j * kS), umma_desc_sw128(qs, kk * 32),
+                         umma_desc_sw128(ks + j * 16384, kk * 32), idesc_s, kk ? 1u : 0u);
         umma_commit(&s_bar);
     }
     pdl_trigger();
     mbar_wait(&s_bar, 0);
     tc_fence_after();
-    const uint32_t row_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(hf * 64);
-    const int nvalid = lengths ? lengths[seq] - hf * 64 : 64;  // this half's valid keys (<= 0: none)
+    const uint32_t row_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(hf * kHalf);
+    const int nvalid = lengths ? lengths[seq] - hf * kHalf : kHalf;  // this half's valid keys (<= 0: none)
     float mx = -INFINITY;
 #pragma unroll
-    for (int c = 0; c < 2; ++c) {
+    for (int c = 0; c < kHalf / 32; ++c) {
         float part[32];
         tmem_ld_32x32b_x32(row_base + static_cast<uint32_t>(c * 32), part);
 #pragma unroll
@@ -650,19 +665,20 @@ __global__ void __launch_bounds__(kAttnThreads, 4) attention_tc_kernel(const __g
     mx = fmaxf(red_max[0][r], red_max[1][r]);  // finite: every sequence has >= 1 valid key (host-checked)
     const float off = mx * kAttnScaleLog2;
     float sum = 0.f;
-    uint8_t* pb = ps + hf * 16384;  // this half's 64 keys = P block hf
 #pragma unroll
-    for (int c32 = 0; c32 < 2; ++c32) {
+    for (int c32 = 0; c32 < kHalf / 32; ++c32) {
         float part[32];
         tmem_ld_32x32b_x32(row_base + static_cast<uint32_t>(c32 * 32), part);
+        const int key0 = hf * kHalf + c32 * 32;  // first key of this chunk within the sequence
+        uint8_t* pb = ps + (key0 >> 6) * 16384;  // its 64-key P block
 #pragma unroll
         for (int q8 = 0; q8 < 4; ++q8) {  // 16-byte chunks of 8 keys
-            const int cc = c32 * 4 + q8;
+            const int cc = ((key0 & 63) >> 3) + q8;
             uint4 u;
             __nv_bfloat162* h2 = reinterpret_cast<__nv_bfloat162*>(&u);
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
-                const int key = cc * 8 + 2 * j;  // within this half
+                const int key = c32 * 32 + q8 * 8 + 2 * j;  // within this half
                 const float p0 = key < nvalid ? ex2_approx(fmaf(part[q8 * 8 + 2 * j], kAttnScaleLog2, -off)) : 0.f;
                 const float p1 = key + 1 < nvalid ? ex2_approx(fmaf(part[q8 * 8 + 2 * j + 1], kAttnScaleLog2, -off)) : 0.f;
                 sum += p0 + p1;
@@ -678,10 +694,10 @@ __global__ void __launch_bounds__(kAttnThreads, 4) attention_tc_kernel(const __g
     if (tid == 0) {
         tc_fence_after();
         // B = V as an MN-major operand: N = 64 dims contiguous (one 128-byte swizzle
-        // span per key), K = keys in 8-key atoms 1024 B apart (SBO).
+        // span per key), K = keys in 8-key atoms 1024 B apart (SBO), the tiles contiguous.
         constexpr uint32_t idesc_o = umma_idesc<128, kDh, 1>() | (1u << 16);  // b_major = MN
 #pragma unroll
-        for (int kk = 0; kk < kS / 16; ++kk)
+        for (int kk = 0; kk < kSeq / 16; ++kk)
             umma_f16(tmem, umma_desc_sw128(ps + (kk >> 2) * 16384, (kk & 3) * 32),
                      umma_desc_sw128(vs, kk * 2048), idesc_o, kk ? 1u : 0u);
         umma_commit(&o_bar);
@@ -691,7 +707,7 @@ __global__ void __launch_bounds__(kAttnThreads, 4) attention_tc_kernel(const __g
     float o[32];  // this half's 32 output dims of row r
     tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(hf * 32), o);
     const float inv = 1.0f / (red_sum[0][r] + red_sum[1][r]);
-    uint4* dst = reinterpret_cast<uint4*>(ctx + (static_cast<size_t>(seq) * kS + r) * d + h * kDh + hf * 32);
+    uint4* dst = reinterpret_cast<uint4*>(ctx + (static_cast<size_t>(seq) * kSeq + qt * kS + r) * d + h * kDh + hf * 32);
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
         uint4 u;
@@ -703,7 +719,7 @@ __global__ void __launch_bounds__(kAttnThreads, 4) attention_tc_kernel(const __g
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    if (warp == 0) tmem_dealloc<128>(tmem);
+    if (warp == 0) tmem_dealloc<kTmemCols>(tmem);
     K2_SPAN_END(span);
 }
 
@@ -1164,9 +1180,13 @@ int encode_rows(const char* arena, const PageTable& pt, const BertLayout& lay, i
                                       static_cast<uint64_t>(T), static_cast<uint64_t>(3 * d) * 2, kDh, kS,
                                       CU_TENSOR_MAP_SWIZZLE_128B))
                 throw CudaError("cuTensorMapEncodeTiled failed (attention)");
-            ensure_max_dynamic_smem(reinterpret_cast<const void*>(attention_tc_kernel), static_cast<int>(kAttnSmem));
-            launch_pdl(attention_tc_kernel, dim3(nb * lay.heads), dim3(kAttnThreads), kAttnSmem, s, true, tq, ctx,
-                       lay.heads, len, next_span("attention"));
+            const int nk = lay.seq / kS;
+            auto att = nk == 1 ? attention_tc_kernel<1> : nk == 2 ? attention_tc_kernel<2>
+                       : nk == 3 ? attention_tc_kernel<3> : attention_tc_kernel<4>;
+            const uint32_t asmem = nk == 1 ? attn_smem<1>() : nk == 2 ? attn_smem<2>() : nk == 3 ? attn_smem<3>() : attn_smem<4>();
+            ensure_max_dynamic_smem(reinterpret_cast<const void*>(att), static_cast<int>(asmem));
+            launch_pdl(att, dim3(nb * lay.heads * nk), dim3(kAttnThreads), asmem, s, true, tq, ctx, lay.heads, len,
+                       next_span("attention"));
         }
         gemm_resid_ln(arena, pt, o.wo, o.bo, o.ln1_g, o.ln1_b, ctx, h, x, t, T, d, d, s, true, ws.gemm_pair);
         gemm<kEpiGelu>(arena, pt, o.w1, o.b1, h, f, nullptr, T, d, lay.ffn, s, true, ws.gemm_pair);
@@ -1183,8 +1203,8 @@ int encode_rows(const char* arena, const PageTable& pt, const BertLayout& lay, i
 int bert_forward(const char* arena, const PageTable& pt, const BertLayout& lay, int batch, const __nv_bfloat16* in,
                  float* out, BertWorkspace& ws, cudaStream_t s, __nv_bfloat16* hidden, const int* lengths) {
     const int d = lay.d, T = batch * lay.seq;
-    if (lay.seq != kS || d / lay.heads != kDh || d % lay.heads || (d != 512 && d != 768 && d != 1024))
-        throw std::runtime_error("bert: this build serves seq 128, d_head 64, d 512 / 768 / 1024");
+    if (lay.seq % kS || lay.seq > 4 * kS || d / lay.heads != kDh || d % lay.heads || (d != 512 && d != 768 && d != 1024))
+        throw std::runtime_error("bert: this build serves seq 128 / 256 / 384 / 512, d_head 64, d 512 / 768 / 1024");
     ws.ensure(T, d, lay.ffn);
     int launches = 0;
 #ifdef GFX_K2_DEBUG

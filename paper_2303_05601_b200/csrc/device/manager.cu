@@ -141,10 +141,10 @@ void ModelStore::add(int idx, const gfx_model_desc& desc) {
     if (idx < 0) throw std::invalid_argument("model index must be >= 0");
     if (desc.family == GFX_MODEL_BERT) {
         const int L = desc.n_layers, D = desc.dims[0], H = desc.dims[1], F = desc.dims[2], S = desc.dims[3];
-        if (L < 1 || (D != 512 && D != 768 && D != 1024) || H * 64 != D || F % 256 || F < 256 || S != 128 ||
-            desc.batch < 1 || desc.batch * S % 128)
-            throw std::invalid_argument(
-                "bert: supported shapes are d = 512 / 768 / 1024 with d / 64 heads, seq 128, ffn % 256 == 0");
+        if (L < 1 || (D != 512 && D != 768 && D != 1024) || H * 64 != D || F % 256 || F < 256 || S % 128 || S < 128 ||
+            S > 512 || desc.batch < 1)
+            throw std::invalid_argument("bert: supported shapes are d = 512 / 768 / 1024 with d / 64 heads, seq 128 / "
+                                        "256 / 384 / 512, ffn % 256 == 0");
         auto blob = std::make_unique<ModelBlob>();
         blob->desc = desc;
         blob->bert = bert_layout(L, D, H, F, S);

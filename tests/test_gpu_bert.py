@@ -70,12 +70,13 @@ def rel(a, b):
     return float(np.linalg.norm(a - b) / np.linalg.norm(b))
 
 
-def run_gpu(gfx, idx, layers, seqs, seed, request_id=7, debug=True, mode="perop", d=D, ffn=3072, lengths=None):
-    desc = gfx.models.bert_desc(layers, seqs, seed, d=d, heads=d // 64, ffn=ffn)
+def run_gpu(gfx, idx, layers, seqs, seed, request_id=7, debug=True, mode="perop", d=D, ffn=3072, lengths=None,
+            seq=SEQ):
+    desc = gfx.models.bert_desc(layers, seqs, seed, d=d, heads=d // 64, ffn=ffn, seq=seq)
     gfx.check(gfx._ffi.gfx_model_register(idx, C.byref(desc)))
     inb, outb = C.c_uint64(), C.c_uint64()
     gfx.check(gfx._ffi.gfx_model_io_bytes(idx, C.byref(inb), C.byref(outb)))
-    assert inb.value == seqs * SEQ * d * 2 and outb.value == seqs * d * 4
+    assert inb.value == seqs * seq * d * 2 and outb.value == seqs * d * 4
     pages = C.c_int32()
     gfx.check(gfx._ffi.gfx_model_pages(idx, C.byref(pages)))
     a = C.c_void_p()
@@ -110,7 +111,7 @@ def run_gpu(gfx, idx, layers, seqs, seed, request_id=7, debug=True, mode="perop"
         hidden = None
         if debug:
             infer(hd)
-            hidden = np.zeros((layers + 1, seqs * SEQ * d), np.uint16)
+            hidden = np.zeros((layers + 1, seqs * seq * d), np.uint16)
             gfx.check(gfx._ffi.gfx_memcpy_d2h(a, hidden.ctypes.data, hd, hbytes))
             dbg = np.zeros_like(pooled)
             gfx.check(gfx._ffi.gfx_memcpy_d2h(a, dbg.ctypes.data, yd, outb.value))
@@ -155,18 +156,22 @@ def test_bert_one_layer_end_to_end(gfx, olib):
     assert rel(pooled, want) <= TOL
 
 
-def teacher_forced(olib, seed, layers, seqs, hidden, pooled, check_layers=None, d=D, ffn=3072):
+def teacher_forced(olib, seed, layers, seqs, hidden, pooled, check_layers=None, d=D, ffn=3072, seq=SEQ, lengths=None):
     threads = os.cpu_count() or 1
     worst = 0.0
     for l in (range(layers) if check_layers is None else check_layers):
         want = np.zeros_like(hidden[l])
-        assert olib.orc_bert_layer(seed, l, d, d // 64, ffn, SEQ, seqs, hidden[l].ctypes.data, want.ctypes.data,
-                                   threads) == 0
+        if lengths is None:
+            assert olib.orc_bert_layer(seed, l, d, d // 64, ffn, seq, seqs, hidden[l].ctypes.data, want.ctypes.data,
+                                       threads) == 0
+        else:
+            assert olib.orc_bert_layer_masked(seed, l, d, d // 64, ffn, seq, seqs, lengths.ctypes.data,
+                                              hidden[l].ctypes.data, want.ctypes.data, threads) == 0
         err = rel(bf16_to_f32(hidden[l + 1]), bf16_to_f32(want))
         worst = max(worst, err)
         assert err <= TOL, f"layer {l}: {err:.3e}"
     want_pool = np.zeros((seqs, d), np.float32)
-    assert olib.orc_bert_pool(seed, layers, d, SEQ, seqs, hidden[layers].ctypes.data, want_pool.ctypes.data) == 0
+    assert olib.orc_bert_pool(seed, layers, d, seq, seqs, hidden[layers].ctypes.data, want_pool.ctypes.data) == 0
     assert rel(pooled, want_pool) <= TOL
     return worst
 
@@ -200,6 +205,23 @@ def test_bert_other_widths_teacher_forced(gfx, olib, d, ffn, layers, seqs):
     assert np.array_equal(hidden[0], x_bits)
     worst = teacher_forced(olib, seed, layers, seqs, hidden, pooled, d=d, ffn=ffn)
     print(f"d {d}: worst per-layer normwise error {worst:.2e}")
+
+
+@pytest.mark.parametrize("seq,seqs,layers,masked", [(256, 4, 2, False), (384, 2, 2, False), (512, 9, 2, False),
+                                                    (512, 4, 2, True)])
+def test_bert_longer_sequences_teacher_forced(gfx, olib, seq, seqs, layers, masked):
+    """Sequences of 256 / 384 / 512 tokens (K3 with every key tile's scores in TMEM:
+    exact softmax over up to 512 keys; P over 2-8 swizzled 64-key blocks), padded
+    ones (lengths 1 .. seq) included; every layer and the pooler teacher-forced."""
+    seed = gfx.model_seed(f"bert-seq-{seq}-{seqs}-{masked}")
+    lengths = None
+    if masked:
+        lengths = np.random.default_rng(seq).integers(1, seq + 1, seqs).astype(np.int32)
+        lengths[:2] = [1, seq]
+    x_bits, pooled, again, hidden = run_gpu(gfx, 77, layers, seqs, seed, request_id=2, seq=seq, lengths=lengths)
+    assert np.array_equal(pooled, again)
+    assert np.array_equal(hidden[0], x_bits)
+    teacher_forced(olib, seed, layers, seqs, hidden, pooled, seq=seq, lengths=lengths)
 
 
 def test_bert_large_batch_pooler(gfx, olib):
