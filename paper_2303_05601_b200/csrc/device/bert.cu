@@ -10,8 +10,9 @@
 //                         residual epilogue (16 warps) through TMA stores; bf16 out.
 //                         Tensor-core bound. Opt-in 2-SM (cta_group::2) variant.
 //   K3 attention_tc_kernel softmax(Q K^T / sqrt(64)) V per (sequence, head, query tile),
-//                         S = 128: one CTA of 4 warps, both products on tcgen05
-//                         (V read MN-major), softmax from TMEM by the row's thread.
+//                         sequences of 128-512 tokens: one CTA of 8 warps, both
+//                         products on tcgen05 (V read MN-major), exact softmax from
+//                         TMEM, optional padding mask (valid length per sequence).
 //   K4 layernorm_kernel   one warp per token row, 16-byte vector loads, fp32
 //                         two-pass statistics; HBM bound.
 //   pooler_kernel         tanh(Wp . x_cls + bp) per sequence, fp32 out.
