@@ -288,6 +288,8 @@ GpuManager::GpuManager(int device, uint64_t capacity_bytes, int manager_id) : de
     sm_count_ = device_sm_count(device_);
     GFX_CUDA(cudaMalloc(&fwd_act_, sizeof(unsigned long long) * 2 * kMlpActWords));
     GFX_CUDA(cudaMemset(fwd_act_, 0, sizeof(unsigned long long) * 2 * kMlpActWords));
+    GFX_CUDA(cudaMalloc(&fwd_claim_, sizeof(unsigned) * 4));
+    GFX_CUDA(cudaMemset(fwd_claim_, 0, sizeof(unsigned) * 4));
     GFX_CUDA(cudaDeviceSynchronize());
 }
 
@@ -305,6 +307,7 @@ GpuManager::~GpuManager() {
     }
     cudaFree(arena_);
     cudaFree(fwd_act_);
+    cudaFree(fwd_claim_);
     bert_ws_.release();
     if (bert_lengths_) cudaFree(bert_lengths_);
     bert_lengths_ = nullptr;
@@ -566,6 +569,12 @@ void GpuManager::infer(int model, const void* in_v, void* out_v, void* debug_hid
     f.act = fwd_act_ + p * kMlpActWords;
     f.act_clear = reinterpret_cast<uint4*>(fwd_act_ + (p ^ 1u) * kMlpActWords);
     f.clear_vec = act_dirty_[p ^ 1u] / 2;
+    // Layer 0 dynamically split: this launch claims from counter epoch % 4 and zeroes
+    // counter (epoch + 2) % 4 once its predecessor completed (then launch epoch - 2, its
+    // last user, has completed too; launch epoch + 2 cannot start before every CTA of this
+    // launch has left its SM).
+    f.claim = fwd_claim_ + (fwd_epoch_ & 3u);
+    f.claim_reset = fwd_claim_ + ((fwd_epoch_ + 2u) & 3u);
 #ifdef GFX_K1_DEBUG
     // Four consecutive launches (8..11 of every 64) mark into their own tables,
     // then one report: the chain's per-launch CTA start / end spread (does the
@@ -643,6 +652,8 @@ void GpuManager::reset() {
         if (act_dirty_[p])
             GFX_CUDA(cudaMemset(fwd_act_ + p * kMlpActWords, 0, sizeof(unsigned long long) * act_dirty_[p]));
     act_dirty_[0] = act_dirty_[1] = 0;
+    GFX_CUDA(cudaMemset(fwd_claim_, 0, sizeof(unsigned) * 4));
+    fwd_epoch_ = 0;
     GFX_CUDA(cudaDeviceSynchronize());
 }
 

@@ -147,6 +147,7 @@ private:
     // K1 forward workspace: layer outputs, two banks by launch parity
     unsigned long long* fwd_act_ = nullptr;
     unsigned fwd_epoch_ = 0;      // launches of the forward kernel on this manager's workspace
+    unsigned* fwd_claim_ = nullptr;  // K1 layer-0 claim counters, one per launch mod 4 (zero when due)
     uint32_t act_dirty_[2] = {0, 0};  // words of each act bank written and not yet cleared
 };
 

@@ -45,10 +45,16 @@ struct MlpFwdArgs {
     int L;
     int grid;
     int pdl;                  // 1: chained to the previous launch by PDL (device owned by one manager), 0: cooperative
+    // Layer 0 split dynamically (nullptr: static stream-K ranges like the other layers):
+    // CTAs claim kMlpChunk0-step ranges from *claim (zero at launch); CTA 0 zeroes
+    // *claim_reset (the counter of launch + 2) once the previous launch completed.
+    unsigned* claim;
+    unsigned* claim_reset;
     MlpFwdLayer layer[GFX_MAX_LAYERS];
     PageTable pt;
 };
 
+constexpr int kMlpChunk0 = 4;  // layer-0 steps per dynamic claim (two paired 32 KB weight copies)
 size_t mlp_fwd_smem();
 // GFX_K1_DEBUG builds: phase-mark table of the last launch (stderr).
 void mlp_debug_report(const unsigned long long* dbg, int grid, int L, int model, cudaStream_t s);

@@ -7,6 +7,10 @@
 //   (swap AB: 128 weight rows fill the MMA M side, the 32 batch rows are N),
 //   act = ReLU on hidden layers; the last layer's rows go through softmax.
 //
+// Layer 0 (v9) is split dynamically instead: CTAs claim kMlpChunk0-step ranges from a
+// per-launch counter, so the CTAs a PDL-chained launch places last (up to ~5 µs late)
+// take less of it (profiles/r2_k1_v7.md); the static split below holds for layers >= 1.
+//
 // Work split (stream-K): a layer is tiles x nkt steps, step s = (feature tile
 // s / nkt, K tile s % nkt); the blob stores weight tiles in exactly that order,
 // so step s reads the 16 KB tile at w_off + 16 KB * s. CTA c takes the
@@ -251,6 +255,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     __shared__ __align__(8) uint64_t w_full[kSlots], raw_full[kSlots], ready[kSlots], step_done[kSlots];
     __shared__ __align__(8) uint64_t tfull[kAccBufs], tempty[kAccBufs];
+    // Layer-0 claims (a.claim): the W producer's claimed step ranges, read in order by every role.
+    constexpr int kQ0 = 8;
+    __shared__ __align__(8) uint64_t q0_full[kQ0], q0_empty[kQ0];
+    __shared__ int2 q0_range[kQ0];
     __shared__ uint32_t tmem_base_s;
     __shared__ float red_s[2][4];
 #ifdef GFX_K1_DEBUG
@@ -288,6 +296,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&tfull[b], 1);
             mbar_init(&tempty[b], 4);  // one arrival per drain warp
         }
+        for (int i = 0; i < kQ0; ++i) {
+            mbar_init(&q0_full[i], 1);
+            mbar_init(&q0_empty[i], 1 + 8 + 2 + 4);  // X producer, converter warps, MMA warps, drain warps
+        }
         mbar_fence_init();
         tma_prefetch_desc(&a.tmap_in);
     }
@@ -298,16 +310,55 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t tmem = tmem_base_s;
     if (tid == 0) K1_MARK(1);
 
+    // Step ranges of layer l: the static stream-K range once, or (layer 0 under a dynamic
+    // split) the W producer's successive claims until its sentinel. A warp-wide role reads a
+    // claim with every lane and releases it from lane 0; a single-lane role does both.
+    const bool dyn0 = a.claim != nullptr;
+    auto next_range = [&](int l, int jq, Range& r, bool single_lane) -> bool {
+        if (l != 0 || !dyn0) {
+            if (jq) return false;
+            r = range_of(a.layer[l], cta, grid);
+            return true;
+        }
+        const int qi = jq % kQ0;
+        K1_WAIT(&q0_full[qi], (jq / kQ0) & 1, 12, jq);
+        const int2 v = q0_range[qi];
+        if (!single_lane) __syncwarp();
+        if (single_lane || lane == 0) mbar_arrive(&q0_empty[qi]);
+        r = Range{v.x, v.y};
+        return v.x >= 0;
+    };
+
     if (warp == 0) {
         // ---------------- W producer: never waits on activations ----------------
         if (lane == 0) {
             int g = 0;
+            const int S0 = a.layer[0].tiles * a.layer[0].nkt;
+            // Claims are software-pipelined: the atomic for claim j + 1 is issued before claim j's
+            // steps, so its L2 round trip overlaps the ring waits instead of stalling the stream.
+            unsigned claim_next = dyn0 ? atomicAdd(a.claim, 1u) : 0u;
             for (int l = 0; l < L; ++l) {
                 const MlpFwdLayer& ly = a.layer[l];
-                const Range r = range_of(ly, cta, grid);
+              for (int jq = 0;; ++jq) {
+                Range r;
+                if (l == 0 && dyn0) {
+                    // Claim the next kMlpChunk0 steps of layer 0 (a CTA that started late — under
+                    // the PDL chain launch CTAs start over a ~5 µs window — simply claims fewer).
+                    const int qi = jq % kQ0;
+                    if (jq >= kQ0) K1_WAIT(&q0_empty[qi], ((jq / kQ0) & 1) ^ 1, 11, jq);
+                    const int s0 = static_cast<int>(claim_next) * kMlpChunk0;
+                    r = s0 < S0 ? Range{s0, s0 + kMlpChunk0 < S0 ? s0 + kMlpChunk0 : S0} : Range{-1, -1};
+                    if (r.s0 >= 0) claim_next = atomicAdd(a.claim, 1u);  // (monotonic: none valid is ever dropped)
+                    q0_range[qi] = make_int2(r.s0, r.s1);
+                    mbar_arrive(&q0_full[qi]);
+                    if (r.s0 < 0) break;
+                } else {
+                    if (jq) break;
+                    r = range_of(ly, cta, grid);
+                }
                 for (int s = r.s0; s < r.s1;) {
                     const int slot = g % kSlots;
-                    const bool pair = (g & 1) == 0 && s + 1 < r.s1;  // steps g, g+1 of this layer
+                    const bool pair = (g & 1) == 0 && s + 1 < r.s1;  // steps g, g+1 of this range
                     if (g >= kSlots) K1_WAIT(&step_done[slot], ((g / kSlots) & 1) ^ 1, 1, g);
                     if (pair && g + 1 >= kSlots) K1_WAIT(&step_done[slot + 1], (((g + 1) / kSlots) & 1) ^ 1, 1, g + 1);
                     K1_STEP(g, 0);
@@ -325,6 +376,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     s += pair ? 2 : 1;
                     g += pair ? 2 : 1;
                 }
+              }
             }
         }
     } else if (warp == 14) {
@@ -333,7 +385,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             int g = 0;
             for (int l = 0; l < L; ++l) {
                 const MlpFwdLayer& ly = a.layer[l];
-                const Range r = range_of(ly, cta, grid);
+                Range r;
+              for (int jq = 0; next_range(l, jq, r, true); ++jq) {
                 const unsigned long long* src_act = l > 0 ? a.act + a.layer[l - 1].act_off : nullptr;
                 int seen = -1;  // last source tile seen complete
                 // Wait until source tile kt >> 2 shows a complete word (its partials have landed).
@@ -346,7 +399,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     complete_words(v, pp, static_cast<unsigned>(a.layer[l - 1].nkt), 10, g_);
                     seen = src;
                 };
-                if (l == 1) asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the buffers' clear by the predecessor
+                if (l == 1 && jq == 0) asm volatile("griddepcontrol.wait;\n" ::: "memory");  // the buffers' clear by the predecessor
                 for (int s = r.s0; s < r.s1;) {
                     const int slot = g % kSlots, kt = s % ly.nkt;
                     const bool pair = l > 0 && (g & 1) == 0 && s + 1 < r.s1;
@@ -376,6 +429,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     s += pair ? 2 : 1;
                     g += pair ? 2 : 1;
                 }
+              }
             }
         }
     } else if (warp == 1 || warp == 15) {
@@ -390,7 +444,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         int g = 0, chunk = 0;
         for (int l = 0; l < L; ++l) {
             const MlpFwdLayer& ly = a.layer[l];
-            const Range r = range_of(ly, cta, grid);
+            Range r;
+          for (int jq = 0; next_range(l, jq, r, false); ++jq) {
             for (int s = r.s0; s < r.s1;) {
                 const int e = seg_end(ly, r, s);
                 for (; s < e; ++chunk) {
@@ -424,6 +479,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     umma_commit_elect(&tfull[buf]);
                 }
             }
+          }
         }
     } else if (warp < 10) {
         // ---------------- converters: W_lo -> TMEM stage, raw X -> operand ----------------
@@ -433,7 +489,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         int g = 0;
         for (int l = 0; l < L; ++l) {
             const MlpFwdLayer& ly = a.layer[l];
-            const Range rg = range_of(ly, cta, grid);
+            Range rg;
+          for (int jq = 0; next_range(l, jq, rg, false); ++jq) {
             for (int s = rg.s0; s < rg.s1; ++s, ++g) {
                 if ((g & 1) != group) continue;
                 const int slot = g % kSlots;
@@ -524,6 +581,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (l == 1 && lane == 0) K1_MARK(28);
                 if (q == 0 && lane == 0) K1_STEP(g, 4);
             }
+          }
         }
     } else if (warp < 14) {
         // ---------------- drain + epilogue warps ----------------
@@ -536,6 +594,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         asm volatile("griddepcontrol.wait;\n" ::: "memory");
         for (uint32_t i = static_cast<uint32_t>(cta * 128 + ct); i < a.clear_vec; i += static_cast<uint32_t>(grid * 128))
             a.act_clear[i] = make_uint4(0u, 0u, 0u, 0u);
+        // The launch before the predecessor has completed: its claim counter is free for launch + 2.
+        if (cta == 0 && ct == 0 && a.claim_reset) atomicExch(a.claim_reset, 0u);
         // Staging (after the ring): half h holds rows 16h..16h+15 as [128 features][128 B], 16-byte chunk j of
         // feature f at j ^ (f & 7) (the TMA SWIZZLE_128B image); warp q owns features 32q..32q+31 of both halves.
         uint8_t* const stg = smem + kStageOff;
@@ -543,8 +603,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         int chunk = 0;
         for (int l = 0; l < L; ++l) {
             const MlpFwdLayer& ly = a.layer[l];
-            const Range r = range_of(ly, cta, grid);
-            const bool last = l == L - 1;
+            Range r;
+          for (int jq = 0; next_range(l, jq, r, false); ++jq) {
             for (int s = r.s0; s < r.s1;) {
                 const int e = seg_end(ly, r, s);
                 const int tile = s / ly.nkt;
@@ -595,6 +655,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 if (l < 4 && ct == 0) K1_SET(6 + 6 * l);
             }
+          }
         }
 
         if (lane == 0) bulk_wait_group<0>();  // every reduction of this CTA issued and complete
