@@ -593,12 +593,23 @@ constexpr uint32_t attn_smem() {
 constexpr int kAttnThreads = 256;
 // lengths (nullptr: every sequence full): padding mask — keys j >= lengths[seq] get
 // probability 0 (excluded from the row max and sum, as an additive -inf mask).
-template <int kNK>
+template <int kNK, bool kMasked>
 __global__ void __launch_bounds__(kAttnThreads, kNK == 1 ? 4 : 1) attention_tc_kernel(const __grid_constant__ CUtensorMap tmap_qkv,
                                                                     __nv_bfloat16* __restrict__ ctx, int heads,
                                                                     const int* __restrict__ lengths,
-                                                                    unsigned long long* span) {
+                                                                    unsigned long long* span,
+                                                                    unsigned long long* marks) {
     constexpr int kSeq = kNK * kS, kHalf = kSeq / 2;  // tokens per sequence, keys per thread
+    // Debug builds: per-CTA %globaltimer marks (0 start, 1 after the PDL wait, 2 Q/K/V landed,
+    // 3 S in TMEM, 4 P written, 5 O in TMEM, 6 end); nullptr otherwise.
+    auto mark = [&](int i) {
+        if (marks && threadIdx.x == 0) {
+            unsigned long long t_;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));
+            marks[blockIdx.x * 8 + i] = t_;
+        }
+    };
+    mark(0);
     constexpr uint32_t kTmemCols = kNK == 1 ? 128 : kNK == 2 ? 256 : 512;
     K2_SPAN_BEGIN(span);
     extern __shared__ uint8_t smem_raw[];
@@ -627,6 +638,7 @@ __global__ void __launch_bounds__(kAttnThreads, kNK == 1 ? 4 : 1) attention_tc_k
     tc_fence_after();
     const uint32_t tmem = tmem_s;
     pdl_wait();
+    mark(1);
     if (tid == 0) {
         const int row0 = seq * kSeq;
         mbar_arrive_expect_tx(&ld_bar, (1 + 2 * kNK) * 16384);
@@ -637,6 +649,7 @@ __global__ void __launch_bounds__(kAttnThreads, kNK == 1 ? 4 : 1) attention_tc_k
             tma_tile2d_g2s(vs + j * 16384, &tmap_qkv, 2 * d + h * kDh, row0 + j * kS, &ld_bar);
         }
         mbar_wait(&ld_bar, 0);
+        mark(2);
         tc_fence_after();
         constexpr uint32_t idesc_s = umma_idesc<128, 128, 1>();  // bf16 x bf16 -> f32, both K-major
 #pragma unroll
@@ -649,9 +662,10 @@ __global__ void __launch_bounds__(kAttnThreads, kNK == 1 ? 4 : 1) attention_tc_k
     }
     pdl_trigger();
     mbar_wait(&s_bar, 0);
+    mark(3);
     tc_fence_after();
     const uint32_t row_base = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(hf * kHalf);
-    const int nvalid = lengths ? lengths[seq] - hf * kHalf : kHalf;  // this half's valid keys (<= 0: none)
+    const int nvalid = kMasked ? lengths[seq] - hf * kHalf : kHalf;  // this half's valid keys (<= 0: none)
     float mx = -INFINITY;
 #pragma unroll
     for (int c = 0; c < kHalf / 32; ++c) {
@@ -659,7 +673,7 @@ __global__ void __launch_bounds__(kAttnThreads, kNK == 1 ? 4 : 1) attention_tc_k
         tmem_ld_32x32b_x32(row_base + static_cast<uint32_t>(c * 32), part);
 #pragma unroll
         for (int j = 0; j < 32; ++j)
-            if (c * 32 + j < nvalid) mx = fmaxf(mx, part[j]);
+            if (!kMasked || c * 32 + j < nvalid) mx = fmaxf(mx, part[j]);
     }
     red_max[hf][r] = mx;
     __syncthreads();
@@ -680,8 +694,9 @@ __global__ void __launch_bounds__(kAttnThreads, kNK == 1 ? 4 : 1) attention_tc_k
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
                 const int key = c32 * 32 + q8 * 8 + 2 * j;  // within this half
-                const float p0 = key < nvalid ? ex2_approx(fmaf(part[q8 * 8 + 2 * j], kAttnScaleLog2, -off)) : 0.f;
-                const float p1 = key + 1 < nvalid ? ex2_approx(fmaf(part[q8 * 8 + 2 * j + 1], kAttnScaleLog2, -off)) : 0.f;
+                const float p0 = !kMasked || key < nvalid ? ex2_approx(fmaf(part[q8 * 8 + 2 * j], kAttnScaleLog2, -off)) : 0.f;
+                const float p1 =
+                    !kMasked || key + 1 < nvalid ? ex2_approx(fmaf(part[q8 * 8 + 2 * j + 1], kAttnScaleLog2, -off)) : 0.f;
                 sum += p0 + p1;
                 h2[j] = __floats2bfloat162_rn(p0, p1);
             }
@@ -692,6 +707,7 @@ __global__ void __launch_bounds__(kAttnThreads, kNK == 1 ? 4 : 1) attention_tc_k
     fence_proxy_async_smem();  // P (generic-proxy writes) -> the PV MMA reads
     tc_fence_before();
     __syncthreads();
+    mark(4);
     if (tid == 0) {
         tc_fence_after();
         // B = V as an MN-major operand: N = 64 dims contiguous (one 128-byte swizzle
@@ -704,6 +720,7 @@ __global__ void __launch_bounds__(kAttnThreads, kNK == 1 ? 4 : 1) attention_tc_k
         umma_commit(&o_bar);
     }
     mbar_wait(&o_bar, 0);
+    mark(5);
     tc_fence_after();
     float o[32];  // this half's 32 output dims of row r
     tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(hf * 32), o);
@@ -721,6 +738,7 @@ __global__ void __launch_bounds__(kAttnThreads, kNK == 1 ? 4 : 1) attention_tc_k
     __syncthreads();
     tc_fence_after();
     if (warp == 0) tmem_dealloc<kTmemCols>(tmem);
+    mark(6);
     K2_SPAN_END(span);
 }
 
@@ -1182,12 +1200,47 @@ int encode_rows(const char* arena, const PageTable& pt, const BertLayout& lay, i
                                       CU_TENSOR_MAP_SWIZZLE_128B))
                 throw CudaError("cuTensorMapEncodeTiled failed (attention)");
             const int nk = lay.seq / kS;
-            auto att = nk == 1 ? attention_tc_kernel<1> : nk == 2 ? attention_tc_kernel<2>
-                       : nk == 3 ? attention_tc_kernel<3> : attention_tc_kernel<4>;
+            auto att = len ? (nk == 1 ? attention_tc_kernel<1, true> : nk == 2 ? attention_tc_kernel<2, true>
+                              : nk == 3 ? attention_tc_kernel<3, true> : attention_tc_kernel<4, true>)
+                           : (nk == 1 ? attention_tc_kernel<1, false> : nk == 2 ? attention_tc_kernel<2, false>
+                              : nk == 3 ? attention_tc_kernel<3, false> : attention_tc_kernel<4, false>);
             const uint32_t asmem = nk == 1 ? attn_smem<1>() : nk == 2 ? attn_smem<2>() : nk == 3 ? attn_smem<3>() : attn_smem<4>();
             ensure_max_dynamic_smem(reinterpret_cast<const void*>(att), static_cast<int>(asmem));
+            unsigned long long* marks = nullptr;
+#ifdef GFX_K2_DEBUG
+            static unsigned long long* mbuf = nullptr;
+            static int att_calls = 0;
+            const bool report = ++att_calls == 13;  // the second forward's first layer
+            if (report) {
+                if (!mbuf) GFX_CUDA(cudaMalloc(&mbuf, sizeof(unsigned long long) * 8 * 8192));
+                GFX_CUDA(cudaMemsetAsync(mbuf, 0, sizeof(unsigned long long) * 8 * 8192, s));
+                marks = mbuf;
+            }
+#endif
             launch_pdl(att, dim3(nb * lay.heads * nk), dim3(kAttnThreads), asmem, s, true, tq, ctx, lay.heads, len,
-                       next_span("attention"));
+                       next_span("attention"), marks);
+#ifdef GFX_K2_DEBUG
+            if (report) {
+                const int grid = nb * lay.heads * nk;
+                std::vector<unsigned long long> m(static_cast<size_t>(grid) * 8);
+                GFX_CUDA(cudaStreamSynchronize(s));
+                GFX_CUDA(cudaMemcpy(m.data(), mbuf, m.size() * 8, cudaMemcpyDeviceToHost));
+                unsigned long long t0 = ~0ull;
+                for (int c = 0; c < grid; ++c) t0 = std::min(t0, m[static_cast<size_t>(c) * 8]);
+                static const char* nm[7] = {"start", "after PDL wait", "Q/K/V landed", "S in TMEM", "P written", "O in TMEM", "end"};
+                std::fprintf(stderr, "[K3 attention, %d CTAs] us after the first CTA start: min p10 median p90 max\n", grid);
+                for (int i = 0; i < 7; ++i) {
+                    std::vector<double> v;
+                    for (int c = 0; c < grid; ++c)
+                        if (m[static_cast<size_t>(c) * 8 + i]) v.push_back((m[static_cast<size_t>(c) * 8 + i] - t0) * 1e-3);
+                    if (v.empty()) continue;
+                    std::sort(v.begin(), v.end());
+                    const size_t n = v.size();
+                    std::fprintf(stderr, "  %-16s %7.2f %7.2f %7.2f %7.2f %7.2f\n", nm[i], v[0], v[n / 10], v[n / 2],
+                                 v[n * 9 / 10], v[n - 1]);
+                }
+            }
+#endif
         }
         gemm_resid_ln(arena, pt, o.wo, o.bo, o.ln1_g, o.ln1_b, ctx, h, x, t, T, d, d, s, true, ws.gemm_pair);
         gemm<kEpiGelu>(arena, pt, o.w1, o.b1, h, f, nullptr, T, d, lay.ffn, s, true, ws.gemm_pair);
