@@ -1167,12 +1167,11 @@ void BertWorkspace::release() {
     if (join) cudaEventDestroy(join);
     side = nullptr;
     fork = join = nullptr;
-    if (flow_items) cudaFree(flow_items);
     if (flow_cnt) cudaFree(flow_cnt);
     if (flow_stats) cudaFree(flow_stats);
-    flow_items = flow_cnt = nullptr;
+    flow_cnt = nullptr;
     flow_stats = nullptr;
-    flow_n_items = flow_L = flow_M = flow_F = flow_ctas = 0;
+    flow_L = flow_M = flow_F = flow_ctas = 0;
     flow_cnt_words = 0;
 }
 

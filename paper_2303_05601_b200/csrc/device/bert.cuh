@@ -58,10 +58,10 @@ struct BertWorkspace {
     bool gemm_pair = false;  // 2-SM (cta_group::2) GEMMs where the shape allows (gfx_arena_set_option)
     bool flow = false;       // the encoder dataflow kernel K5 instead of per-op launches (K2-K4)
     __nv_bfloat16 *x = nullptr, *qkv = nullptr, *ctx = nullptr, *h = nullptr, *f = nullptr, *t = nullptr;
-    // K5: claim list and dataflow counters for one (layers, row blocks, ffn, SMs) shape.
-    uint32_t *flow_items = nullptr, *flow_cnt = nullptr;
+    // K5: dataflow counters + ready-queue slots for one (layers, row blocks, ffn) shape.
+    uint32_t* flow_cnt = nullptr;
     void* flow_stats = nullptr;  // per-row LayerNorm statistics of the residual tiles
-    int flow_n_items = 0, flow_L = 0, flow_M = 0, flow_F = 0, flow_ctas = 0;
+    int flow_L = 0, flow_M = 0, flow_F = 0, flow_ctas = 0;
     size_t flow_cnt_words = 0;
     // Second stream (+ fork / join events) for the two-half per-op forward, created on first use
     // on the device current at the time (the manager's).

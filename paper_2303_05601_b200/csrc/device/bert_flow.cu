@@ -54,9 +54,7 @@
 #include <cstdlib>
 #include <map>
 #include <mutex>
-#include <queue>
 #include <stdexcept>
-#include <tuple>
 #include <vector>
 
 #include "bert.cuh"
@@ -738,16 +736,14 @@ int bert_encoder_flow(const char* arena, const PageTable& pt, const BertLayout& 
     // Cluster items per (layer, row block): 3 QKV, 4 attention, 1 O, ffn / 768 FFN1, 1 FFN2.
     const int n_items = L * M * (3 + 4 + 1 + F / 768 + 1);
     if (ws.flow_L != L || ws.flow_M != M || ws.flow_F != F) {
-        if (ws.flow_items) GFX_CUDA(cudaFree(ws.flow_items));
         if (ws.flow_cnt) GFX_CUDA(cudaFree(ws.flow_cnt));
         if (ws.flow_stats) GFX_CUDA(cudaFree(ws.flow_stats));
-        ws.flow_items = ws.flow_cnt = nullptr;
+        ws.flow_cnt = nullptr;
         ws.flow_stats = nullptr;
         // One allocation: [L][M][kCSlots] counters, head, tail, then n_items queue slots.
         ws.flow_cnt_words = static_cast<size_t>(L) * M * kCSlots + 2 + static_cast<size_t>(n_items);
         GFX_CUDA(cudaMalloc(&ws.flow_cnt, ws.flow_cnt_words * 4));
         GFX_CUDA(cudaMalloc(&ws.flow_stats, static_cast<size_t>(L) * M * 2 * 3 * 128 * sizeof(float2)));
-        ws.flow_n_items = n_items;
         ws.flow_L = L, ws.flow_M = M, ws.flow_F = F, ws.flow_ctas = ctas;
     }
     FlowMaps mp;

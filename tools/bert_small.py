@@ -44,4 +44,4 @@ if iters:
     flops = L * (2.0 * T * (4 * d * d + 2 * d * 4 * d) + 4.0 * T * 128 * d) + 2.0 * S * d * d
     print(f"bert L={L} S={S} d={d} {mode}: {dt * 1e3:.3f} ms/forward  {flops / dt / 1e12:.1f} TFLOP/s", flush=True)
 F.check(F.gfx_arena_destroy(a))
-print(f"bert small L={L} S={S} d={d} {mode}: done")
+print(f"bert small L={L} S={S} d={d} {mode}: done", flush=True)
