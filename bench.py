@@ -798,7 +798,7 @@ def c5_extras(gfx, world, peaks, peak_kind):
                         "avg_latency_ms": round(r.report["avg_latency_s"] * 1e3, 3),
                         "p99_latency_ms": round(r.percentile_s(99) * 1e3, 3)}
         fleet8[f"arena_{arena}"] = row
-    out_c5 = {"c5_fleet8_schedule_sweep": fleet8}
+    out_c5 = {"c5_fleet8_schedule_sweep": fleet8, "c5_forward_batch_sweep": c5_batch_sweep(gfx, peak)}
     return {**out_c5, "c5_bert_base_arena_sweep": {
         "workload": "C5: 20 BERT-base bf16 encoders (12x768, ffn 3072), 32x128 tokens/request, ws 20, "
                     "325 rpm x 1 min, LALBO3, 1 GPU", "requests": int(rs[-1].n_requests),
@@ -808,6 +808,45 @@ def c5_extras(gfx, world, peaks, peak_kind):
                              "(B200_PROFILING.md; MEASURED_PEAKS.json absent)"),
         "note": "tensor_tflops = model flops (GEMMs + attention) / CUDA-event time of the whole forward "
                 "(GEMMs, attention, LayerNorm, pooler, launch gaps)", "sweep": sweep}}
+
+
+def c5_batch_sweep(gfx, peak):
+    """One 12-layer BERT-base forward per request size (32 = the C5 request, 64, 128
+    sequences of 128 tokens), resident weights, CUDA events around 20 back-to-back
+    forwards on the arena's compute stream; from 64 sequences the per-op forward runs
+    as two halves on two streams."""
+    import ctypes as C
+    F = gfx._ffi
+    out = []
+    for seqs in (32, 64, 128):
+        idx = 60
+        desc = gfx.models.bert_desc(12, seqs, gfx.model_seed(f"bench-bert-{seqs}"))
+        F.check(F.gfx_model_register(idx, C.byref(desc)))
+        pages = C.c_int32()
+        F.check(F.gfx_model_pages(idx, C.byref(pages)))
+        a = C.c_void_p()
+        F.check(F.gfx_arena_create(0, C.c_uint64((pages.value + 1) << 21), C.byref(a)))
+        try:
+            F.check(F.gfx_load_h2d(a, idx, None))
+            inb, outb = C.c_uint64(), C.c_uint64()
+            F.check(F.gfx_model_io_bytes(idx, C.byref(inb), C.byref(outb)))
+            x, y = C.c_void_p(), C.c_void_p()
+            F.check(F.gfx_device_alloc(a, inb.value, C.byref(x)))
+            F.check(F.gfx_device_alloc(a, outb.value, C.byref(y)))
+            models = (C.c_int32 * 20)(*([idx] * 20))
+            ms = C.c_double()
+            F.check(F.gfx_infer_sequence(a, models, 3, x, 0, y, 0, C.byref(ms)))  # warm-up
+            F.check(F.gfx_infer_sequence(a, models, 20, x, 0, y, 0, C.byref(ms)))
+            per = ms.value / 20
+            T = seqs * 128
+            flops = 12 * (2.0 * T * (4 * 768 * 768 + 2 * 768 * 3072) + 4.0 * T * 128 * 768) + 2.0 * seqs * 768 * 768
+            tf = flops / (per / 1e3) / 1e12
+            out.append({"sequences": seqs, "ms_per_forward": round(per, 4), "tensor_tflops": round(tf, 1),
+                        "tensor_frac": round(tf / peak, 4)})
+        finally:
+            F.gfx_arena_destroy(a)
+    return {"note": "BERT-base (12 x 768, ffn 3072) forward per request size, per-op K2-K4 launches, resident "
+                    "weights, events around 20 back-to-back forwards (gfx_infer_sequence)", "sweep": out}
 
 
 if __name__ == "__main__":
