@@ -207,9 +207,9 @@ def test_bert_other_widths_teacher_forced(gfx, olib, d, ffn, layers, seqs):
     print(f"d {d}: worst per-layer normwise error {worst:.2e}")
 
 
-@pytest.mark.parametrize("seq,seqs,layers,masked", [(256, 4, 2, False), (384, 2, 2, False), (512, 9, 2, False),
-                                                    (512, 4, 2, True)])
-def test_bert_longer_sequences_teacher_forced(gfx, olib, seq, seqs, layers, masked):
+@pytest.mark.parametrize("seq,seqs,layers,masked,d", [(256, 4, 2, False, D), (384, 2, 2, False, D), (512, 9, 2, False, D),
+                                                      (512, 4, 2, True, D), (512, 3, 1, True, 1024)])
+def test_bert_longer_sequences_teacher_forced(gfx, olib, seq, seqs, layers, masked, d):
     """Sequences of 256 / 384 / 512 tokens (K3 with every key tile's scores in TMEM:
     exact softmax over up to 512 keys; P over 2-8 swizzled 64-key blocks), padded
     ones (lengths 1 .. seq) included; every layer and the pooler teacher-forced."""
@@ -218,10 +218,12 @@ def test_bert_longer_sequences_teacher_forced(gfx, olib, seq, seqs, layers, mask
     if masked:
         lengths = np.random.default_rng(seq).integers(1, seq + 1, seqs).astype(np.int32)
         lengths[:2] = [1, seq]
-    x_bits, pooled, again, hidden = run_gpu(gfx, 77, layers, seqs, seed, request_id=2, seq=seq, lengths=lengths)
+    ffn = 4 * d
+    x_bits, pooled, again, hidden = run_gpu(gfx, 77, layers, seqs, seed, request_id=2, seq=seq, lengths=lengths, d=d,
+                                            ffn=ffn)
     assert np.array_equal(pooled, again)
     assert np.array_equal(hidden[0], x_bits)
-    teacher_forced(olib, seed, layers, seqs, hidden, pooled, seq=seq, lengths=lengths)
+    teacher_forced(olib, seed, layers, seqs, hidden, pooled, seq=seq, lengths=lengths, d=d, ffn=ffn)
 
 
 def test_bert_large_batch_pooler(gfx, olib):

@@ -191,6 +191,20 @@ def test_bert_masked_layer_oracle_matches_transformers(olib):
                                       got.ctypes.data, 8) == -1
 
 
+def test_bert_masked_layer_full_lengths_equals_unmasked(olib):
+    """Consistency of the oracle's two entry points: lengths = seq everywhere is the
+    unmasked layer, bit for bit."""
+    seed, seqs, l = 0xB0B0 + 23, 2, 0
+    x, xb = bert_input(olib, seqs)
+    a = np.zeros_like(xb)
+    b = np.zeros_like(xb)
+    assert olib.orc_bert_layer(seed, l, D, HEADS, FFN, SEQ, seqs, xb.ctypes.data, a.ctypes.data, 8) == 0
+    full = np.full(seqs, SEQ, np.int32)
+    assert olib.orc_bert_layer_masked(seed, l, D, HEADS, FFN, SEQ, seqs, full.ctypes.data, xb.ctypes.data,
+                                      b.ctypes.data, 8) == 0
+    assert np.array_equal(a, b)
+
+
 def test_bert_pooler_oracle_matches_transformers(olib):
     from transformers.models.bert.modeling_bert import BertPooler
     seed, seqs, L = 0xB0B0 + 9, 3, 12
